@@ -1,0 +1,62 @@
+"""The five BASELINE.json workloads (``configs[0..4]``) as seeded builders.
+
+Each entry gives the graph recipe and the filter / clustering parameters the
+config names.  ``build_graph(name)`` returns the CSR graph; the random signal
+block is ``signals.gaussian_block(seed, N, R)``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import graphs
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    n: int
+    k: int
+    R: int            # number of random signals eta
+    order: int        # Chebyshev order p
+    jackson: bool
+    graph: dict
+    kmeans_restarts: int = 10
+    note: str = ""
+
+
+WORKLOADS = {
+    # configs[0]: SBM N=2,000, k=5 equal, avg degree 10, eps=0.1, unit weights;
+    # R=32, p=50, Jackson; cut at estimated lambda_k; k-means k=5, 10 restarts.
+    "c0_sbm2k": Workload("c0_sbm2k", 2000, 5, 32, 50, True,
+                         dict(kind="sbm", n=2000, k=5, avg_degree=10, eps=0.1, sizes="equal")),
+    # configs[1]: GMM kNN N=20,000, d=10, 10 Gaussians sigma=1, centers U[0,10]^d,
+    # symmetrised 10-NN, Gaussian weights with sigma = mean 10-NN distance; R=24, p=100.
+    "c1_gmm20k": Workload("c1_gmm20k", 20000, 10, 24, 100, False,
+                          dict(kind="gmm_knn", n=20000, dim=10, n_comp=10, knn=10)),
+    # configs[2]: SBM N=100,000, k=20 equal, avg degree 16, eps=0.05; R=48, p=150;
+    # stability over 10 redraws for k in [10,30]; fp32 and fp64 filter.
+    "c2_sbm100k": Workload("c2_sbm100k", 100_000, 20, 48, 150, False,
+                           dict(kind="sbm", n=100_000, k=20, avg_degree=16, eps=0.05, sizes="equal")),
+    # configs[3]: SBM N=1,000,000, k=100 power-law sizes (exp 2, min 1000), avg degree 20,
+    # eps=0.03; R=64, p=200, fp32; row-partitioned over 1/2/4/8 GPUs.
+    "c3_sbm1m": Workload("c3_sbm1m", 1_000_000, 100, 64, 200, False,
+                         dict(kind="sbm", n=1_000_000, k=100, avg_degree=20, eps=0.03,
+                              sizes="powerlaw", exponent=2.0, min_size=1000)),
+    # configs[4]: SBM N=10,000,000, k=200 equal, avg degree 20, eps=0.02; R=96, p=300, fp32.
+    "c4_sbm10m": Workload("c4_sbm10m", 10_000_000, 200, 96, 300, False,
+                          dict(kind="sbm", n=10_000_000, k=200, avg_degree=20, eps=0.02,
+                               sizes="equal")),
+}
+
+ORDER = ["c0_sbm2k", "c1_gmm20k", "c2_sbm100k", "c3_sbm1m", "c4_sbm10m"]
+
+
+def build_graph(name: str, seed: int = 1234) -> graphs.CSRGraph:
+    spec = dict(WORKLOADS[name].graph)
+    kind = spec.pop("kind")
+    if kind == "sbm":
+        return graphs.sbm(seed=seed, **spec)
+    if kind == "gmm_knn":
+        return graphs.gmm_knn(seed=seed, **spec)
+    raise ValueError(kind)
