@@ -1,0 +1,331 @@
+"""Benchmark of the hot path: the fused Chebyshev low-pass filter of R random
+signals (§4.1 steps 3-5) on a BASELINE.json workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3_sbm1m] [--impl ours|reference]
+
+One "step" = one full filtering pass F^p X of the N x R signal block resident in
+HBM (coefficients for the cut lambda~_k computed on the host + p fused
+recurrence launches per column chunk).  lambda_max and lambda~_k are computed
+once per graph before timing (per-graph setup, not per batch).
+
+Metric (BASELINE.json): filter nnz*R*p/s, nnz = nnz(L) = nnz(W) + N.  ``value``
+is device-timed (CUDA events on the launching stream, barrier + synchronize on
+both sides, max over ranks); ``e2e`` is the same metric through the C ABI with
+pinned HOST buffers (H2D of X and D2H of Y inside the timed region).
+
+``--impl reference`` times the fp64 CPU oracle (the only reference this run
+has) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "filter nnz·R·p/s"
+UNIT = "nnz·R·p/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c3_sbm1m")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(workload)
+    return None
+
+
+# ---------------------------------------------------------------------------
+# oracle (CPU) timing -- cpu_baseline and --impl reference
+# ---------------------------------------------------------------------------
+def oracle_sample(g, w, lam_c, lmax, cols=1, order=None, budget_s=20.0):
+    """Time the fp64 oracle filter on `cols` columns and `order` recurrence steps of
+    the same graph (bounded sample); returns (nnz*R*p per second, description)."""
+    import scinputs
+    from oracle import chebyshev, laplacian
+    L = laplacian.laplacian(g)
+    X = scinputs.gaussian_block(7, g.n, cols).astype(np.float64)
+    # calibrate the order so that the sample stays within budget
+    t0 = time.perf_counter()
+    chebyshev.lowpass_filter(L, X, lam_c, lmax, 2, w.jackson)
+    per_step = max((time.perf_counter() - t0) / 2.0, 1e-6)
+    if order is None:
+        order = int(max(2, min(w.order, budget_s / per_step)))
+    t0 = time.perf_counter()
+    chebyshev.lowpass_filter(L, X, lam_c, lmax, order, w.jackson)
+    dt = time.perf_counter() - t0
+    nnz_l = g.nnz + g.n
+    return nnz_l * cols * order / dt, dt, f"oracle fp64 filter, {cols} of {w.R} columns, order {order} of {w.order}"
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if world > 1 and rank != 0:
+        return
+    from scinputs import configs
+    w = configs.WORKLOADS[args.workload]
+    g = configs.build_graph(args.workload, seed=args.seed)
+    lmax = 2.0 * float(g.degrees().max() if g.values is None else np.max(np.add.reduceat(g.values, g.row_ptr[:-1])))
+    lam_c = 0.25 * lmax
+    vals = []
+    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    for i in range(args.warmup + args.steps):
+        v, dt, desc = oracle_sample(g, w, lam_c, lmax, cols=1, budget_s=budget)
+        if i >= args.warmup:
+            vals.append((v, dt, desc))
+    value = statistics.median(v for v, _, _ in vals)
+    ms = statistics.median(dt for _, dt, _ in vals) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "N": g.n, "nnz_L": g.nnz + g.n, "R": w.R, "order": w.order},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": vals[0][2]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1509_08863_b200 as sc
+    from scinputs import configs
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    w = configs.WORKLOADS[args.workload]
+    g = configs.build_graph(args.workload, seed=args.seed)
+    n, R, order = g.n, w.R, w.order
+    weighted = g.values is not None
+    stream = torch.cuda.current_stream()
+
+    # ---- per-graph setup (single-GPU view for lambda_max / lambda_k)
+    if world == 1:
+        G = sc.Graph.from_csr(g)
+        lmax = sc.sc_lambda_max(G.handle, 60, 0.01, args.seed)
+        lam_k, count_k = sc.sc_estimate_lambda_k(G.handle, w.k, lmax, min(order, 150), True, 32, args.seed + 1,
+                                                 40, 1e-4)
+        handle = G.handle
+    else:
+        from paper_1509_08863_b200 import dist as pdist
+        # lambda bounds on rank-local copies are not needed: Gershgorin bound + fixed cut
+        lmax = 2.0 * float(g.degrees().max())
+        lam_k, count_k = 0.25 * lmax, float("nan")
+        part = pdist.local_part(g.row_ptr, g.col_idx, g.values, n, rank, world)
+        part = pdist.exchange_send_lists(part)
+        Gl = sc.Graph(part.n_local, part.row_ptr, part.col_idx, part.values, n_cols=part.n_local + part.n_halo)
+        handle = Gl.handle
+    d = sc.sc_cheby_coeffs(lam_k, lmax, order, w.jackson)
+
+    if world == 1:
+        X = torch.empty((n, R), dtype=torch.float32, device=dev)
+        sc.sc_random_signals_f32(n, R, 0, args.seed, 0, 0.0, X)
+        Y = torch.empty_like(X)
+
+        def step():
+            dd = sc.sc_cheby_coeffs(lam_k, lmax, order, w.jackson)
+            sc.sc_filter_apply_f32(handle, dd, order, lmax, R, X, Y)
+    else:
+        from paper_1509_08863_b200 import dist as pdist
+        Xl = torch.empty((part.n_local, R), dtype=torch.float32, device=dev)
+        sc.sc_random_signals_f32(part.n_local, R, part.r0, args.seed, 0, 0.0, Xl)
+        fn = pdist.cuda_step_fn(handle)
+
+        def step():
+            dd = sc.sc_cheby_coeffs(lam_k, lmax, order, w.jackson)
+            pdist.run_filter(part, fn, dd, order, lmax, Xl)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    sc.sc_profile_begin()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    launches, step_launches, kern_ms, algo_bytes = sc.sc_profile_end()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nnz_l = g.nnz + n
+    work = float(nnz_l) * R * order * args.steps
+    value = work / (ms / 1e3)
+
+    peak, peak_src = measured_peaks()
+    avg_launch_s = (kern_ms / 1e3) / max(step_launches, 1)
+    bytes_per_launch = algo_bytes / max(step_launches, 1)
+    achieved = bytes_per_launch / avg_launch_s / 1e9
+    traffic = ncu_traffic(args.workload)
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "N": n, "nnz_W": int(g.nnz), "nnz_L": int(nnz_l), "R": R,
+                       "order": order, "jackson": w.jackson, "lambda_max": lmax, "lambda_cut": lam_k,
+                       "lambda_cut_count": count_k, "graph_seed": args.seed,
+                       "l2": "inputs larger than L2 (CSR + 3 dense N x R blocks > 126 MB); no flush",
+                       "parallelism": f"row-partitioned x{world}" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "cheb_step_kernel (fused SpMM + 3-term recurrence + Y accumulation)",
+                         "avg_launch_us": avg_launch_s * 1e6, "algo_bytes_per_launch": bytes_per_launch,
+                         "kernel_share_of_step": (kern_ms / ms) if ms > 0 else None},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+
+    # ---- e2e through the C ABI with pinned host buffers (single GPU)
+    if world == 1 and not args.no_e2e and rank == 0:
+        Xh = torch.empty((n, R), dtype=torch.float32, pin_memory=True)
+        Xh.copy_(X)
+        Yh = torch.empty((n, R), dtype=torch.float32, pin_memory=True)
+        for _ in range(2):
+            sc.sc_filter_lowpass_f32(handle, lam_k, lmax, order, w.jackson, R, 0, Xh, Yh)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            sc.sc_filter_lowpass_f32(handle, lam_k, lmax, order, w.jackson, R, 0, Xh, Yh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        out["e2e"] = {"value": work / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 4),
+                      "d2h_bytes_per_step": int(Yh.numel() * 4), "ms_per_step": ems / args.steps,
+                      "api": "sc_filter_lowpass_f32(host X, host Y)"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, desc = oracle_sample(g, w, lam_k, lmax, cols=1, budget_s=15.0)
+        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                               "seconds": dt}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,271 @@
+/*
+ * sc_b200.h -- C ABI of the B200-native accelerated spectral clustering hot path.
+ *
+ * Paper: N. Tremblay, G. Puy, P. Borgnat, R. Gribonval, P. Vandergheynst,
+ * "Accelerated spectral clustering using graph filtering of random signals"
+ * (arXiv:1509.08863), cited below as PAPER.md §x / line y.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Return value: SC_OK (0) on success, a negative SC_ERR_* code otherwise;
+ *    sc_last_error() returns a human-readable message for the calling thread.
+ *    On error no output is guaranteed to be written.
+ *  - Pointers: every array argument may live in host memory (pageable or pinned)
+ *    or in CUDA device memory of the current device; the library detects which
+ *    with cudaPointerGetAttributes and copies host arrays in/out itself (so the
+ *    same call serves an end-to-end host-buffer caller and a device-resident
+ *    caller).  The caller keeps ownership of every array it passes.
+ *  - Dense blocks (signals, filtered output, features) are row-major
+ *    n x R arrays (row i = node i, column q = signal q), contiguous.
+ *  - Graphs are symmetric CSR of the weighted adjacency W (§2 lines
+ *    59-63): row_ptr int64[n+1], col_idx int32[nnz] (no diagonal entries),
+ *    values float32[nnz] or NULL for a unit-weight ("pattern") graph.
+ *  - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls that return host scalars synchronise that stream before returning.
+ *  - Precision: "_f32" paths store and accumulate in fp32, "_f64" paths in fp64.
+ *    k-means decisions (argmin, D^2 sampling, best replicate) are taken in fp64.
+ *  - There is no CPU fallback: without a CUDA device every compute call
+ *    returns SC_ERR_CUDA.
+ */
+#ifndef SC_B200_H
+#define SC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SC_OK            0
+#define SC_ERR_ARG      -1   /* invalid argument (sizes, ranges, null pointers)   */
+#define SC_ERR_CUDA     -2   /* CUDA runtime error or no device                    */
+#define SC_ERR_STATE    -3   /* handle in the wrong state                          */
+#define SC_ERR_NOMEM    -4   /* device or host allocation failed                   */
+
+typedef struct sc_graph sc_graph;   /* opaque device-resident graph + workspace */
+
+/* Version of the ABI (major*10000 + minor*100 + patch). */
+int sc_version(void);
+
+/* Message describing the last error raised on the calling thread ("" if none). */
+const char* sc_last_error(void);
+
+/* ------------------------------------------------------------------------ */
+/* Graph                                                                    */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * sc_graph_load -- upload W and build the combinatorial Laplacian operator
+ * L = S - W, S = diag(s), s_i = sum_{j != i} W_ij (§2.1 lines 66-72).
+ *
+ *  n_rows   rows of W held by this process (all N nodes on one GPU; the local
+ *           row block of a row-partitioned multi-GPU run).
+ *  n_cols   number of distinct column indices the rows reference
+ *           (= N on one GPU; local rows + halo rows when partitioned; col_idx < n_cols).
+ *  nnz      stored entries = row_ptr[n_rows].
+ *  row_ptr, col_idx, values   CSR arrays as above (values may be NULL: unit weights).
+ *  out      receives the new handle; free it with sc_graph_free.
+ * The strengths s_i are computed on device in fp64 from the rows as given.
+ * Errors: SC_ERR_ARG for n_rows<1, n_cols<n_rows, nnz<0, null arrays;
+ *         SC_ERR_NOMEM / SC_ERR_CUDA on device failures.
+ */
+int sc_graph_load(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                  const int32_t* col_idx, const float* values, sc_graph** out);
+
+int sc_graph_free(sc_graph* g);
+
+/* n_rows, n_cols, nnz and max_i s_i (Gershgorin: lambda_N <= 2 max s_i). */
+int sc_graph_info(const sc_graph* g, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
+                  double* max_strength);
+
+/* Copy the fp64 strengths s (n_rows values) to `out` (host or device). */
+int sc_graph_strengths(const sc_graph* g, double* out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Spectral bounds and filter design (§2.4, §4.1 steps 1 and 3)    */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * sc_lambda_max -- upper bound of lambda_N, the largest eigenvalue of L
+ * (§4.1 step 1, line 309: "Estimate L's largest eigenvalue").
+ * Runs `iters` Lanczos steps (fp64, start vector from the counter-based
+ * generator with `seed`), takes the largest Ritz value theta and returns
+ * min((1+margin)*theta, 2*max_i s_i)  (the Chebyshev domain must contain the
+ * whole spectrum; 2 max s_i is Gershgorin's bound).  Single-GPU graphs only
+ * (n_cols == n_rows).  Errors: SC_ERR_ARG for iters<1 or margin<0.
+ */
+int sc_lambda_max(sc_graph* g, int iters, double margin, uint64_t seed, double* out,
+                  void* stream);
+
+/*
+ * sc_cheby_coeffs -- host: the order+1 coefficients d_j = g_j c_j of the
+ * Chebyshev approximation of the ideal low-pass h_{lambda_c}(lambda) =
+ * 1[lambda <= lambda_c] on [0, lambda_max] (Eq. (2) line 128 and
+ * §2.4):  c_0 = 1 - theta/pi,  c_j = -2 sin(j theta)/(pi j),
+ * theta = arccos(2 lambda_c/lambda_max - 1);  g_j = Jackson damping factors
+ * when `jackson` != 0 (else 1).  coeffs: host array of order+1 doubles.
+ * Errors: SC_ERR_ARG for order<0, lambda_max<=0.
+ */
+int sc_cheby_coeffs(double lambda_c, double lambda_max, int order, int jackson, double* coeffs);
+
+/* ------------------------------------------------------------------------ */
+/* Random signals (§3.1, §4.1 step 4 line 316)       */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * sc_random_signals -- rows [row0, row0+n) of the N x R block of i.i.d.
+ * N(0, variance) entries of the counter-based generator (splitmix64 +
+ * Box-Muller in fp64); variance <= 0 means
+ * 1/R (the paper's 1/eta).  stream_id: 0 = signals, 2 = eigencount probes.
+ * out: n x R, fp32 (_f32) or fp64 (_f64), host or device.
+ */
+int sc_random_signals_f32(int64_t n, int R, int64_t row0, uint64_t seed, int stream_id,
+                          double variance, float* out, void* stream);
+int sc_random_signals_f64(int64_t n, int R, int64_t row0, uint64_t seed, int stream_id,
+                          double variance, double* out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* The hot path: fused Chebyshev filter (§2.4 Eq. (3), §4.1 step 5) */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * sc_filter_apply -- Y = sum_{j=0}^{order} coeffs[j] T_j(L~) X, L~ = (2/lambda_max) L - I,
+ * by the three-term recurrence T_{j+1} = 2 L~ T_j - T_{j-1}, each step one fused
+ * CSR SpMM that also accumulates Y (O(m(|E|+N))).
+ *  X   n x R input block (signals), Y  n x R output block; X and Y must not alias.
+ *  coeffs  host array of order+1 doubles (e.g. from sc_cheby_coeffs).
+ *  order >= 1, R >= 1, lambda_max > 0.  Single-GPU graphs only (n_cols == n_rows).
+ */
+int sc_filter_apply_f32(sc_graph* g, const double* coeffs, int order, double lambda_max,
+                        int R, const float* X, float* Y, void* stream);
+int sc_filter_apply_f64(sc_graph* g, const double* coeffs, int order, double lambda_max,
+                        int R, const double* X, double* Y, void* stream);
+
+/*
+ * sc_filter_lowpass -- the paper's fast filtering of random signals
+ * (§4.1 steps 3-5, Eq. (10)): coefficients of h_{lambda_c} (with
+ * optional Jackson damping) applied to X.  If X is NULL the N x R signal block
+ * is drawn on device from `seed` (sc_random_signals, variance 1/R) first.
+ * Y receives the n x R filtered block F R whose rows are the features f~_i.
+ */
+int sc_filter_lowpass_f32(sc_graph* g, double lambda_c, double lambda_max, int order,
+                          int jackson, int R, uint64_t seed, const float* X, float* Y,
+                          void* stream);
+int sc_filter_lowpass_f64(sc_graph* g, double lambda_c, double lambda_max, int order,
+                          int jackson, int R, uint64_t seed, const double* X, double* Y,
+                          void* stream);
+
+/*
+ * sc_cheb_step -- one fused recurrence step on caller-owned device buffers, for
+ * the row-partitioned multi-GPU driver (rows [row_begin, row_end) of this
+ * rank's block; gathers read T_cur rows 0..n_cols-1, i.e. local + halo rows):
+ *    T_next = a * (L T_cur) + b_cur * T_cur + b_prev * T_prev
+ *    Y      (y_mode 1: =, 2: +=)  cy_prev T_prev + cy_cur T_cur + cy_next T_next
+ * T_prev may be NULL when b_prev == 0 and cy_prev == 0; T_next may be NULL to
+ * skip storing it (last step).  ld_* are row strides in elements.  All
+ * pointers device, fp32.
+ */
+int sc_cheb_step_f32(sc_graph* g, int64_t row_begin, int64_t row_end, int R,
+                     const float* T_prev, int64_t ld_prev, const float* T_cur, int64_t ld_cur,
+                     float* T_next, int64_t ld_next, float* Y, int64_t ld_y,
+                     double a, double b_cur, double b_prev, double cy_prev, double cy_cur,
+                     double cy_next, int y_mode, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* lambda_k estimation (§3.2)                        */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * sc_cheb_moments -- mu_m = <X, T_m(L~) X>_F for m = 0..2*order from `order`
+ * recurrence steps (T_{2j} = 2 T_j^2 - I, T_{2j+1} = 2 T_j T_{j+1} - T_1), fp64.
+ * X: n x R probes (host/device, fp64) or NULL = drawn from `seed` (stream 2,
+ * variance 1/R).  moments: 2*order+1 doubles (host or device).
+ */
+int sc_cheb_moments(sc_graph* g, double lambda_max, int order, int R, uint64_t seed,
+                    const double* X, double* moments, void* stream);
+
+/*
+ * sc_eigencount -- estimated number of eigenvalues <= lambda_c:
+ * ||F_{lambda_c} X||_F^2 evaluated from the moments (host arithmetic).
+ */
+int sc_eigencount_from_moments(const double* moments, int order, double lambda_c,
+                               double lambda_max, int jackson, double* count);
+
+/*
+ * sc_estimate_lambda_k -- dichotomy on [0, lambda_max] keeping
+ * count(lo) < k - 1/2 <= count(hi) (reading R6) until
+ * hi - lo <= rtol*lambda_max or max_iter; returns lambda_k = hi and count(hi).
+ * All counts come from ONE moments pass (n_probe probe columns, seed).
+ */
+int sc_estimate_lambda_k(sc_graph* g, int k, double lambda_max, int order, int jackson,
+                         int n_probe, uint64_t seed, int max_iter, double rtol,
+                         double* lambda_k, double* count_k, void* stream);
+
+/* Same dichotomy on precomputed moments (host only; k-scans reuse one pass). */
+int sc_lambda_k_from_moments(const double* moments, int order, int k, double lambda_max,
+                             int jackson, int max_iter, double rtol, double* lambda_k,
+                             double* count_k);
+
+/* ------------------------------------------------------------------------ */
+/* Features and k-means (§2.2 step 4, §4.1 step 6)                 */
+/* ------------------------------------------------------------------------ */
+
+/* f_i <- f_i / ||f_i||_2 in place (rows of zero norm stay zero); fp32. */
+int sc_normalize_rows_f32(float* F, int64_t n, int d, void* stream);
+
+/*
+ * sc_kmeans -- best of `restarts` k-means runs on the n x d fp32 features F.
+ * Replicate r seeds with k-means++ using uniforms u[r*k + t] (t < k): taken
+ * from `uniforms` (host/device, restarts*k doubles) or, if NULL, from the
+ * counter-based generator (seed, stream 1, counters r*k + t).  Lloyd: assign
+ * argmin_c sum_q (x_q - C_cq)^2 in fp64 (ascending q, no FMA contraction,
+ * lowest c on ties), update to member means (empty cluster keeps its centre),
+ * stop when an assignment repeats or after max_iter updates.  Lowest inertia
+ * wins, ties -> lowest r.
+ *  labels    n int32 (host/device);   centroids  k*d doubles or NULL;
+ *  inertia   host double or NULL;     iters      host int or NULL;
+ *  best_restart host int or NULL.
+ * Errors: SC_ERR_ARG for k<1, k>n, d<1, restarts<1, max_iter<1.
+ */
+int sc_kmeans(const float* F, int64_t n, int d, int k, int restarts, int max_iter,
+              uint64_t seed, const double* uniforms, int32_t* labels, double* centroids,
+              double* inertia, int* iters, int* best_restart, void* stream);
+
+/* Adjusted Rand index of two labelings of n nodes (§4.3, §5). */
+int sc_ari(const int32_t* a, const int32_t* b, int64_t n, double* out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Whole pipeline (§4.1 steps 1-6)                                 */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * sc_cluster -- lambda_max (Lanczos), lambda_k (moments + dichotomy, n_probe
+ * probes, Jackson), filter R random signals at lambda_k (order, jackson),
+ * optional row normalisation, k-means (restarts).  labels: n int32.
+ * info (host, may be NULL): [lambda_max, lambda_k, count_k, inertia,
+ * kmeans_iters, best_restart].
+ */
+int sc_cluster(sc_graph* g, int k, int R, int order, int jackson, int n_probe,
+               uint64_t seed, int restarts, int max_iter, int normalize, int32_t* labels,
+               double* info, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Instrumentation (bench.py)                                               */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * sc_profile_begin / sc_profile_end -- while on, every fused-step launch is
+ * bracketed by CUDA events recorded on its launching stream.  sc_profile_end
+ * synchronises those events and returns: all kernels launched by the filter
+ * path, fused-step launches, their summed device time (ms), and their summed
+ * algorithmic bytes (CSR share + each dense operand row read/written once;
+ * DESIGN.md "roofline").  Not thread-safe; profiling is process-global.
+ */
+int sc_profile_begin(void);
+int sc_profile_end(int64_t* launches, int64_t* step_launches, double* step_ms, double* algo_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SC_B200_H */

@@ -9,8 +9,10 @@ taken in fp64 on both sides (task rule: the paper's precision, Matlab double).
     seeding   : k-means++ (Arthur & Vassilvitskii 2007) with the uniforms u_0..u_{k-1}
                 passed in: first centre floor(u_0 N); centre t is the smallest i
                 with cumsum(D^2)_i > u_t * sum(D^2).
-    Lloyd     : assign = argmin_c sum_q (x_iq - C_cq)^2 (lowest c on ties);
-                update = member mean (an empty cluster keeps its centre);
+    Lloyd     : assign = argmin_c sum_q (x_iq - C_cq)^2 (lowest c on ties; the sum
+                in ascending q);
+                update = member mean, member sum correctly rounded (math.fsum),
+                an empty cluster keeps its centre;
                 stop when an assignment repeats or after max_iter updates.
     replicates: lowest inertia wins, ties -> lowest replicate index.
 
@@ -19,17 +21,24 @@ ORACLE -- test infrastructure only (see oracle/__init__.py).
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 
 def sq_dists(X: np.ndarray, C: np.ndarray) -> np.ndarray:
-    """D[i, c] = sum_q (X[i,q] - C[c,q])^2 in fp64 (explicit differences)."""
+    """D[i, c] = sum_q (X[i,q] - C[c,q])^2 in fp64, explicit differences, the sum
+    taken term by term in ascending q (reading R8: the decision
+    arithmetic is fixed so that both sides round identically)."""
     X = np.asarray(X, dtype=np.float64)
     C = np.asarray(C, dtype=np.float64)
-    D = np.empty((X.shape[0], C.shape[0]), dtype=np.float64)
+    D = np.zeros((X.shape[0], C.shape[0]), dtype=np.float64)
     for c in range(C.shape[0]):
-        diff = X - C[c]
-        D[:, c] = np.sum(diff * diff, axis=1)
+        acc = np.zeros(X.shape[0], dtype=np.float64)
+        for q in range(X.shape[1]):
+            diff = X[:, q] - C[c, q]
+            acc += diff * diff
+        D[:, c] = acc
     return D
 
 
@@ -45,8 +54,11 @@ def update(X, labels, C_prev):
     C = np.array(C_prev, dtype=np.float64, copy=True)
     for c in range(k):
         m = labels == c
-        if np.any(m):
-            C[c] = X[m].sum(axis=0) / m.sum()
+        cnt = int(m.sum())
+        if cnt:
+            M = X[m]
+            # member mean with the member sum correctly rounded (math.fsum)
+            C[c] = [math.fsum(M[:, q]) / cnt for q in range(X.shape[1])]
     return C
 
 

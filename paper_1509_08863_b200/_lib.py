@@ -1,0 +1,260 @@
+"""ctypes binding of libsc_b200.so -- argument marshalling only.
+
+Every function here has the name of the C entry point it calls
+(include/sc_b200.h) and does nothing but convert Python arguments (torch
+tensors, numpy arrays, scalars) into pointers and sizes, call the library and
+turn a non-zero status into an exception.  All arithmetic of the method runs in
+the library's CUDA kernels; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("SC_B200_LIB", os.path.join(_HERE, "libsc_b200.so"))
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libsc_b200.so not found at {LIB_PATH}: build it with `python native_build.py` "
+        "(or __graft_entry__.build()). There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+c_i64 = ctypes.c_int64
+c_i32 = ctypes.c_int
+c_u64 = ctypes.c_uint64
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+P = ctypes.POINTER
+
+
+def _sig(name, *args):
+    f = getattr(_lib, name)
+    f.restype = ctypes.c_int
+    f.argtypes = list(args)
+    return f
+
+
+_lib.sc_last_error.restype = ctypes.c_char_p
+_lib.sc_version.restype = ctypes.c_int
+
+_F = {
+    "sc_graph_load": _sig("sc_graph_load", c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, P(c_vp)),
+    "sc_graph_free": _sig("sc_graph_free", c_vp),
+    "sc_graph_info": _sig("sc_graph_info", c_vp, P(c_i64), P(c_i64), P(c_i64), P(c_dbl)),
+    "sc_graph_strengths": _sig("sc_graph_strengths", c_vp, c_vp, c_vp),
+    "sc_lambda_max": _sig("sc_lambda_max", c_vp, c_i32, c_dbl, c_u64, P(c_dbl), c_vp),
+    "sc_cheby_coeffs": _sig("sc_cheby_coeffs", c_dbl, c_dbl, c_i32, c_i32, c_vp),
+    "sc_random_signals_f32": _sig("sc_random_signals_f32", c_i64, c_i32, c_i64, c_u64, c_i32, c_dbl, c_vp, c_vp),
+    "sc_random_signals_f64": _sig("sc_random_signals_f64", c_i64, c_i32, c_i64, c_u64, c_i32, c_dbl, c_vp, c_vp),
+    "sc_filter_apply_f32": _sig("sc_filter_apply_f32", c_vp, c_vp, c_i32, c_dbl, c_i32, c_vp, c_vp, c_vp),
+    "sc_filter_apply_f64": _sig("sc_filter_apply_f64", c_vp, c_vp, c_i32, c_dbl, c_i32, c_vp, c_vp, c_vp),
+    "sc_filter_lowpass_f32": _sig("sc_filter_lowpass_f32", c_vp, c_dbl, c_dbl, c_i32, c_i32, c_i32, c_u64, c_vp,
+                                  c_vp, c_vp),
+    "sc_filter_lowpass_f64": _sig("sc_filter_lowpass_f64", c_vp, c_dbl, c_dbl, c_i32, c_i32, c_i32, c_u64, c_vp,
+                                  c_vp, c_vp),
+    "sc_cheb_step_f32": _sig("sc_cheb_step_f32", c_vp, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                             c_vp, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_i32, c_vp),
+    "sc_cheb_moments": _sig("sc_cheb_moments", c_vp, c_dbl, c_i32, c_i32, c_u64, c_vp, c_vp, c_vp),
+    "sc_eigencount_from_moments": _sig("sc_eigencount_from_moments", c_vp, c_i32, c_dbl, c_dbl, c_i32, P(c_dbl)),
+    "sc_estimate_lambda_k": _sig("sc_estimate_lambda_k", c_vp, c_i32, c_dbl, c_i32, c_i32, c_i32, c_u64, c_i32, c_dbl,
+                                 P(c_dbl), P(c_dbl), c_vp),
+    "sc_lambda_k_from_moments": _sig("sc_lambda_k_from_moments", c_vp, c_i32, c_i32, c_dbl, c_i32, c_i32, c_dbl,
+                                     P(c_dbl), P(c_dbl)),
+    "sc_normalize_rows_f32": _sig("sc_normalize_rows_f32", c_vp, c_i64, c_i32, c_vp),
+    "sc_kmeans": _sig("sc_kmeans", c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_u64, c_vp, c_vp, c_vp, P(c_dbl),
+                      P(c_i32), P(c_i32), c_vp),
+    "sc_ari": _sig("sc_ari", c_vp, c_vp, c_i64, P(c_dbl), c_vp),
+    "sc_cluster": _sig("sc_cluster", c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_u64, c_i32, c_i32, c_i32, c_vp, c_vp,
+                       c_vp),
+    "sc_profile_begin": _sig("sc_profile_begin"),
+    "sc_profile_end": _sig("sc_profile_end", P(c_i64), P(c_i64), P(c_dbl), P(c_dbl)),
+}
+
+EXPORTED = sorted(list(_F) + ["sc_version", "sc_last_error"])
+
+
+class SCError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[sc error {code}] {msg}")
+        self.code = code
+
+
+def _check(rc):
+    if rc != 0:
+        raise SCError(rc, _lib.sc_last_error().decode(errors="replace"))
+
+
+def _ptr(x):
+    """Pointer of a contiguous torch tensor / numpy array (host or device), or NULL."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("numpy array must be C-contiguous")
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    if isinstance(x, int):
+        return x
+    raise TypeError(f"cannot take the address of {type(x)}")
+
+
+def _stream(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return stream
+
+
+def sc_version() -> int:
+    return _lib.sc_version()
+
+
+def sc_last_error() -> str:
+    return _lib.sc_last_error().decode(errors="replace")
+
+
+def sc_graph_load(n_rows, n_cols, nnz, row_ptr, col_idx, values):
+    h = c_vp()
+    _check(_F["sc_graph_load"](n_rows, n_cols, nnz, _ptr(row_ptr), _ptr(col_idx), _ptr(values), ctypes.byref(h)))
+    return h.value
+
+
+def sc_graph_free(g):
+    _check(_F["sc_graph_free"](g))
+
+
+def sc_graph_info(g):
+    a, b, c, d = c_i64(), c_i64(), c_i64(), c_dbl()
+    _check(_F["sc_graph_info"](g, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)))
+    return a.value, b.value, c.value, d.value
+
+
+def sc_graph_strengths(g, out, stream=None):
+    _check(_F["sc_graph_strengths"](g, _ptr(out), _stream(stream)))
+
+
+def sc_lambda_max(g, iters=60, margin=0.01, seed=0, stream=None) -> float:
+    out = c_dbl()
+    _check(_F["sc_lambda_max"](g, iters, margin, seed, ctypes.byref(out), _stream(stream)))
+    return out.value
+
+
+def sc_cheby_coeffs(lambda_c, lambda_max, order, jackson) -> np.ndarray:
+    out = np.empty(order + 1, dtype=np.float64)
+    _check(_F["sc_cheby_coeffs"](lambda_c, lambda_max, order, int(jackson), out.ctypes.data))
+    return out
+
+
+def sc_random_signals_f32(n, R, row0, seed, stream_id, variance, out, stream=None):
+    _check(_F["sc_random_signals_f32"](n, R, row0, seed, stream_id, variance, _ptr(out), _stream(stream)))
+
+
+def sc_random_signals_f64(n, R, row0, seed, stream_id, variance, out, stream=None):
+    _check(_F["sc_random_signals_f64"](n, R, row0, seed, stream_id, variance, _ptr(out), _stream(stream)))
+
+
+def sc_filter_apply_f32(g, coeffs, order, lambda_max, R, X, Y, stream=None):
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    _check(_F["sc_filter_apply_f32"](g, coeffs.ctypes.data, order, lambda_max, R, _ptr(X), _ptr(Y), _stream(stream)))
+
+
+def sc_filter_apply_f64(g, coeffs, order, lambda_max, R, X, Y, stream=None):
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    _check(_F["sc_filter_apply_f64"](g, coeffs.ctypes.data, order, lambda_max, R, _ptr(X), _ptr(Y), _stream(stream)))
+
+
+def sc_filter_lowpass_f32(g, lambda_c, lambda_max, order, jackson, R, seed, X, Y, stream=None):
+    _check(_F["sc_filter_lowpass_f32"](g, lambda_c, lambda_max, order, int(jackson), R, seed, _ptr(X), _ptr(Y),
+                                       _stream(stream)))
+
+
+def sc_filter_lowpass_f64(g, lambda_c, lambda_max, order, jackson, R, seed, X, Y, stream=None):
+    _check(_F["sc_filter_lowpass_f64"](g, lambda_c, lambda_max, order, int(jackson), R, seed, _ptr(X), _ptr(Y),
+                                       _stream(stream)))
+
+
+def sc_cheb_step_f32(g, row_begin, row_end, R, T_prev, ld_prev, T_cur, ld_cur, T_next, ld_next, Y, ld_y,
+                     a, b_cur, b_prev, cy_prev, cy_cur, cy_next, y_mode, stream=None):
+    _check(_F["sc_cheb_step_f32"](g, row_begin, row_end, R, _ptr(T_prev), ld_prev, _ptr(T_cur), ld_cur, _ptr(T_next),
+                                  ld_next, _ptr(Y), ld_y, a, b_cur, b_prev, cy_prev, cy_cur, cy_next, y_mode,
+                                  _stream(stream)))
+
+
+def sc_cheb_moments(g, lambda_max, order, R, seed, X=None, stream=None) -> np.ndarray:
+    mu = np.empty(2 * order + 1, dtype=np.float64)
+    _check(_F["sc_cheb_moments"](g, lambda_max, order, R, seed, _ptr(X), mu.ctypes.data, _stream(stream)))
+    return mu
+
+
+def sc_eigencount_from_moments(moments, order, lambda_c, lambda_max, jackson) -> float:
+    mu = np.ascontiguousarray(moments, dtype=np.float64)
+    out = c_dbl()
+    _check(_F["sc_eigencount_from_moments"](mu.ctypes.data, order, lambda_c, lambda_max, int(jackson),
+                                            ctypes.byref(out)))
+    return out.value
+
+
+def sc_estimate_lambda_k(g, k, lambda_max, order, jackson, n_probe, seed, max_iter=40, rtol=1e-4, stream=None):
+    lk, ck = c_dbl(), c_dbl()
+    _check(_F["sc_estimate_lambda_k"](g, k, lambda_max, order, int(jackson), n_probe, seed, max_iter, rtol,
+                                      ctypes.byref(lk), ctypes.byref(ck), _stream(stream)))
+    return lk.value, ck.value
+
+
+def sc_lambda_k_from_moments(moments, order, k, lambda_max, jackson, max_iter=40, rtol=1e-4):
+    mu = np.ascontiguousarray(moments, dtype=np.float64)
+    lk, ck = c_dbl(), c_dbl()
+    _check(_F["sc_lambda_k_from_moments"](mu.ctypes.data, order, k, lambda_max, int(jackson), max_iter, rtol,
+                                          ctypes.byref(lk), ctypes.byref(ck)))
+    return lk.value, ck.value
+
+
+def sc_normalize_rows_f32(F, n, d, stream=None):
+    _check(_F["sc_normalize_rows_f32"](_ptr(F), n, d, _stream(stream)))
+
+
+def sc_kmeans(F, n, d, k, restarts, max_iter, seed, uniforms, labels, centroids=None, stream=None):
+    inertia, iters, best = c_dbl(), c_i32(), c_i32()
+    u = None if uniforms is None else np.ascontiguousarray(uniforms, dtype=np.float64)
+    _check(_F["sc_kmeans"](_ptr(F), n, d, k, restarts, max_iter, seed, _ptr(u), _ptr(labels), _ptr(centroids),
+                           ctypes.byref(inertia), ctypes.byref(iters), ctypes.byref(best), _stream(stream)))
+    return inertia.value, iters.value, best.value
+
+
+def sc_ari(a, b, n, stream=None) -> float:
+    out = c_dbl()
+    _check(_F["sc_ari"](_ptr(a), _ptr(b), n, ctypes.byref(out), _stream(stream)))
+    return out.value
+
+
+def sc_cluster(g, k, R, order, jackson, n_probe, seed, restarts, max_iter, normalize, labels, stream=None):
+    info = np.zeros(6, dtype=np.float64)
+    _check(_F["sc_cluster"](g, k, R, order, int(jackson), n_probe, seed, restarts, max_iter, int(normalize),
+                            _ptr(labels), info.ctypes.data, _stream(stream)))
+    return info
+
+
+def sc_profile_begin():
+    _check(_F["sc_profile_begin"]())
+
+
+def sc_profile_end():
+    """-> (launches, step_launches, step_ms, algo_bytes)"""
+    a, b, c, d = c_i64(), c_i64(), c_dbl(), c_dbl()
+    _check(_F["sc_profile_end"](ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)))
+    return a.value, b.value, c.value, d.value

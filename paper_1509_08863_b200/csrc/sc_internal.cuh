@@ -1,0 +1,176 @@
+// Internal declarations shared by the CUDA translation units of libsc_b200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "sc_b200.h"
+
+namespace sc {
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+struct Status {
+  int code = SC_OK;
+};
+
+#define SC_CUDA_TRY(expr)                                                         \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess)                                                        \
+      return ::sc::fail(SC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define SC_TRY(expr)                \
+  do {                              \
+    int _rc = (expr);               \
+    if (_rc != SC_OK) return _rc;   \
+  } while (0)
+
+#define SC_CHECK_ARG(cond, msg) \
+  do {                          \
+    if (!(cond)) return ::sc::fail(SC_ERR_ARG, msg); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device buffers
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  int ensure(size_t b) {   // grow-only
+    if (b <= bytes) return SC_OK;
+    release();
+    if (b == 0) return SC_OK;
+    cudaError_t e = cudaMalloc(&ptr, b);
+    if (e != cudaSuccess) { ptr = nullptr; return fail(SC_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e)); }
+    bytes = b;
+    return SC_OK;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+// Is p a device (or managed) pointer of the current device?
+bool is_device_ptr(const void* p);
+
+// Host<->device staging for an argument that may be host or device memory.
+// Owned staging memory comes from the stream-ordered pool (cudaMallocAsync), so
+// repeated host-buffer calls do not pay cudaMalloc/cudaFree.
+struct Staged {
+  void* dev = nullptr;          // device view
+  const void* host = nullptr;   // original host pointer (if staged)
+  size_t bytes = 0;
+  void* owned = nullptr;
+  cudaStream_t st = 0;
+  Staged() = default;
+  Staged(const Staged&) = delete;
+  Staged& operator=(const Staged&) = delete;
+  ~Staged() {
+    if (owned) cudaFreeAsync(owned, st);
+  }
+  int alloc(size_t b, cudaStream_t s);                           // owned device buffer
+  int in(const void* p, size_t b, cudaStream_t s, bool copy);   // stage to device
+  int out(void* p, cudaStream_t s);                               // copy back if host
+};
+
+// ---------------------------------------------------------------------------
+// graph handle
+// ---------------------------------------------------------------------------
+}  // namespace sc
+
+struct sc_graph {
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  bool unit_weights = true;
+  double max_strength = 0.0;
+  sc::DevBuf row_ptr;     // int64 [n_rows+1]
+  sc::DevBuf col_idx;     // int32 [nnz]
+  sc::DevBuf values;      // float [nnz] (empty if unit weights)
+  sc::DevBuf strength64;  // double [n_rows]
+  sc::DevBuf strength32;  // float  [n_rows]
+  // workspace (grow-only)
+  sc::DevBuf ws_a, ws_b, ws_sig, ws_part, ws_misc;
+  int num_sms = 148;
+  int device = 0;
+};
+
+namespace sc {
+
+// ---------------------------------------------------------------------------
+// kernels / drivers (defined in the .cu files)
+// ---------------------------------------------------------------------------
+struct StepParams {
+  int64_t row_begin, row_end;
+  const void* tprev; int64_t ld_prev;
+  const void* tcur;  int64_t ld_cur;
+  void* tnext;       int64_t ld_next;
+  void* y;           int64_t ld_y;
+  double a, b_cur, b_prev;
+  double cy_prev, cy_cur, cy_next;
+  int y_mode;        // 0 none, 1 write, 2 accumulate
+  int width;         // columns processed (chunk width)
+  int total_width;   // all columns of the block (for the profiler's CSR share)
+  // moments mode (fp64 only): per-block partial sums written to `part`
+  double* part;      // [gridDim.x][3] : <Tc,Tc>, <Tn,Tc>, <Tn,Tn>
+};
+
+// launch one fused step for `width` columns starting at the given pointers
+template <typename T>
+int launch_step(const sc_graph* g, const StepParams& p, cudaStream_t s);
+
+// full filter: Y = sum_j coeffs_j T_j X   (X, Y device, row-major n x R)
+template <typename T>
+int filter_apply(sc_graph* g, const double* coeffs, int order, double lambda_max, int R,
+                 const T* X, T* Y, cudaStream_t s);
+
+// launch profiler
+void profile_begin();
+int profile_end(int64_t* launches, int64_t* step_launches, double* step_ms, double* algo_bytes);
+
+// Chebyshev moments (fp64) into host vector
+int cheb_moments(sc_graph* g, double lambda_max, int order, int R, const double* X,
+                 std::vector<double>& mu, cudaStream_t s);
+
+// random signals on device
+template <typename T>
+int random_signals(int64_t n, int R, int64_t row0, uint64_t seed, int stream_id, double variance,
+                   T* out, cudaStream_t s);
+
+// Lanczos
+int lanczos_lambda_max(sc_graph* g, int iters, uint64_t seed, double* theta, cudaStream_t s);
+
+// host math (sc_host.cpp)
+void cheby_lowpass_coeffs(double lambda_c, double lambda_max, int order, bool jackson, double* out);
+double count_from_moments(const double* mu, int order, const double* d);
+int lambda_k_dichotomy(const double* mu, int order, int k, double lambda_max, bool jackson,
+                       int max_iter, double rtol, double* lambda_k, double* count_k);
+double tridiag_max_eig(const std::vector<double>& alpha, const std::vector<double>& beta);
+
+// k-means and friends
+int normalize_rows_f32(float* F, int64_t n, int d, cudaStream_t s);
+int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_iter,
+               uint64_t seed, const double* uniforms_host, int32_t* labels_dev,
+               double* centroids_host, double* inertia, int* iters, int* best_restart,
+               cudaStream_t s);
+int ari_dev(const int32_t* a, const int32_t* b, int64_t n, double* out, cudaStream_t s);
+
+// counter-based RNG (host side, identical to the device one)
+uint64_t splitmix64_host(uint64_t x);
+double uniform_host(uint64_t seed, int stream_id, uint64_t ctr);
+
+}  // namespace sc
