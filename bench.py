@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cluster", action="store_true")
     return ap.parse_args()
 
 
@@ -307,6 +308,23 @@ def run_ours(args):
         out["e2e"] = {"value": work / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 4),
                       "d2h_bytes_per_step": int(Yh.numel() * 4), "ms_per_step": ems / args.steps,
                       "api": "sc_filter_lowpass_f32(host X, host Y)"}
+
+    # ---- end-to-end clustering time (BASELINE metric: "end-to-end cluster time"): sc_cluster =
+    # lambda_max (Lanczos) + lambda_k (moments + dichotomy) + filter + k-means, graph resident
+    if world == 1 and rank == 0 and not args.no_cluster:
+        labels = torch.empty(n, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        info = sc.sc_cluster(handle, w.k, R, order, w.jackson, 32, args.seed, w.kmeans_restarts, 100, False, labels)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ari = sc.sc_ari(labels, torch.from_numpy(g.labels).to(dev), n) if g.labels is not None else None
+        out["cluster_e2e"] = {"seconds": wall, "device_ms": e0.elapsed_time(e1), "k": w.k,
+                              "restarts": w.kmeans_restarts, "lambda_max": info[0], "lambda_k": info[1],
+                              "count_k": info[2], "kmeans_iters": int(info[4]), "ari_vs_planted": ari,
+                              "api": "sc_cluster (device-resident graph)"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt, desc = oracle_sample(g, w, lam_k, lmax, cols=1, budget_s=15.0)

@@ -249,6 +249,30 @@ int sc_cluster(sc_graph* g, int k, int R, int order, int jackson, int n_probe,
                uint64_t seed, int restarts, int max_iter, int normalize, int32_t* labels,
                double* info, void* stream);
 
+/*
+ * sc_stability -- stability measure for the number of clusters (§4.3,
+ * Eq.(11)): for every k in [k_min, k_max], J clusterings from J
+ * independent draws of the R random signals (replicate j draws R with seed + j,
+ * stream 0, variance 1/R) and
+ *     gamma(k) = 2/(J(J-1)) * sum_{a<b} ari(C^a_k, C^b_k)          (R7).
+ * Each replicate runs the Chebyshev recurrence once (order fused steps, all
+ * order+1 terms T_m kept in device memory: (order+1)*n*ceil4(R)*4 bytes) and
+ * forms the filtered block of every cut lambda_k from it, then k-means with k
+ * clusters (`restarts` k-means++ replicates, uniforms from seed + j, stream 1).
+ *  lambda_max  > 0: the Chebyshev domain; <= 0: Lanczos estimate (as sc_lambda_max, 60 steps, 1%).
+ *  lambda_k    host array of K = k_max-k_min+1 cuts, or NULL: estimated from one moments
+ *              pass of n_probe probes (seed ^ 0x5e5e5e5e, stream 2), Jackson-damped
+ *              counts, dichotomy as sc_lambda_k_from_moments (40 steps, rtol 1e-4).
+ *  gamma       host double[K] (out);  lambda_k_out host double[K] or NULL (out: cuts used).
+ *  labels      NULL or int32 [K][J][n] (host or device; out): every clustering.
+ * Single-GPU graphs only.  Errors: SC_ERR_ARG for 1 <= k_min <= k_max < n, J >= 2,
+ * R >= 1, order >= 1, restarts >= 1, max_iter >= 1 violated; SC_ERR_NOMEM when the
+ * T_m stack does not fit.
+ */
+int sc_stability(sc_graph* g, int k_min, int k_max, int J, int R, int order, int jackson, int n_probe,
+                 uint64_t seed, int restarts, int max_iter, double lambda_max, const double* lambda_k,
+                 double* gamma, double* lambda_k_out, int32_t* labels, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Instrumentation (bench.py)                                               */
 /* ------------------------------------------------------------------------ */

@@ -26,12 +26,12 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I", os.
           "-I", CSRC]
 
 
-def _compile(src: str, verbose_ptxas: bool) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+def _compile(src: str, verbose_ptxas: bool, defs=(), tag="") -> str:
+    obj = os.path.join(BUILD, os.path.basename(src) + tag + ".o")
     deps = [src] + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "sc_b200.h")]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
-    cmd = [NVCC, *ARCH, *COMMON, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *COMMON, *defs, "-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd = [NVCC, *COMMON, "-x", "c++", "-c", src, "-o", obj]
     elif verbose_ptxas:
@@ -44,14 +44,17 @@ def _compile(src: str, verbose_ptxas: bool) -> str:
     return obj
 
 
-def build(verbose_ptxas: bool = False) -> str:
+def build(verbose_ptxas: bool = False, defs=(), out: str = LIB) -> str:
+    """Compile every source and link ``out``.  ``defs`` (e.g. ["-DSC_EB_F32=12"]) build a
+    tuning variant; its objects get their own names so variants do not clobber each other."""
     os.makedirs(BUILD, exist_ok=True)
+    tag = "" if not defs else "." + "_".join(d.lstrip("-D").replace("=", "") for d in defs)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose_ptxas), srcs))
-    if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
-        return LIB
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+        objs = list(ex.map(lambda s: _compile(s, verbose_ptxas, defs, tag), srcs))
+    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(o) for o in objs):
+        return out
+    cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
@@ -59,4 +62,6 @@ def build(verbose_ptxas: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose_ptxas="--verbose-ptxas" in sys.argv))
+    defs = sys.argv[sys.argv.index("--defs") + 1].split() if "--defs" in sys.argv else []
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else LIB
+    print(build(verbose_ptxas="--verbose-ptxas" in sys.argv, defs=defs, out=out))

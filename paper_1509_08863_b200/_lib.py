@@ -71,6 +71,8 @@ _F = {
     "sc_ari": _sig("sc_ari", c_vp, c_vp, c_i64, P(c_dbl), c_vp),
     "sc_cluster": _sig("sc_cluster", c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_u64, c_i32, c_i32, c_i32, c_vp, c_vp,
                        c_vp),
+    "sc_stability": _sig("sc_stability", c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_u64, c_i32, c_i32,
+                         c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp),
     "sc_profile_begin": _sig("sc_profile_begin"),
     "sc_profile_end": _sig("sc_profile_end", P(c_i64), P(c_i64), P(c_dbl), P(c_dbl)),
 }
@@ -247,6 +249,19 @@ def sc_cluster(g, k, R, order, jackson, n_probe, seed, restarts, max_iter, norma
     _check(_F["sc_cluster"](g, k, R, order, int(jackson), n_probe, seed, restarts, max_iter, int(normalize),
                             _ptr(labels), info.ctypes.data, _stream(stream)))
     return info
+
+
+def sc_stability(g, k_min, k_max, J, R, order, jackson, n_probe, seed, restarts, max_iter, lambda_max=0.0,
+                 lambda_k=None, labels=None, stream=None):
+    """-> (gamma[K], lambda_k[K]) for k = k_min..k_max; `labels` (optional) receives [K][J][n] int32."""
+    K = k_max - k_min + 1
+    gamma = np.empty(K, dtype=np.float64)
+    lk_out = np.empty(K, dtype=np.float64)
+    lk = None if lambda_k is None else np.ascontiguousarray(lambda_k, dtype=np.float64)
+    _check(_F["sc_stability"](g, k_min, k_max, J, R, order, int(jackson), n_probe, seed, restarts, max_iter,
+                              lambda_max, _ptr(lk), gamma.ctypes.data, lk_out.ctypes.data, _ptr(labels),
+                              _stream(stream)))
+    return gamma, lk_out
 
 
 def sc_profile_begin():

@@ -178,9 +178,14 @@ int sc_graph_load(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ro
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device);
   cudaStream_t s = 0;
   int rc;
-  if ((rc = g->row_ptr.ensure(sizeof(int64_t) * (n_rows + 1))) != SC_OK) return bail(rc);
-  if ((rc = g->col_idx.ensure(sizeof(int32_t) * (nnz ? nnz : 1))) != SC_OK) return bail(rc);
-  if (!g->unit_weights && (rc = g->values.ensure(sizeof(float) * (nnz ? nnz : 1))) != SC_OK) return bail(rc);
+  // CSR arrays are padded (kRowPtrPad / kColPad zeroed entries) so that the filter's 16-byte
+  // aligned bulk copies of a tile's row_ptr / col_idx / values segments may over-read the tail.
+  if ((rc = g->row_ptr.ensure(sizeof(int64_t) * (n_rows + 1 + kRowPtrPad))) != SC_OK) return bail(rc);
+  if ((rc = g->col_idx.ensure(sizeof(int32_t) * (nnz + kColPad))) != SC_OK) return bail(rc);
+  if (!g->unit_weights && (rc = g->values.ensure(sizeof(float) * (nnz + kColPad))) != SC_OK) return bail(rc);
+  cudaMemsetAsync(g->row_ptr.as<int64_t>() + n_rows + 1, 0, sizeof(int64_t) * kRowPtrPad, s);
+  cudaMemsetAsync(g->col_idx.as<int32_t>() + nnz, 0, sizeof(int32_t) * kColPad, s);
+  if (!g->unit_weights) cudaMemsetAsync(g->values.as<float>() + nnz, 0, sizeof(float) * kColPad, s);
   if ((rc = g->strength64.ensure(sizeof(double) * n_rows)) != SC_OK) return bail(rc);
   if ((rc = g->strength32.ensure(sizeof(float) * n_rows)) != SC_OK) return bail(rc);
   auto cp = [&](void* dst, const void* src, size_t b) -> int {
@@ -468,6 +473,31 @@ int sc_ari(const int32_t* a, const int32_t* b, int64_t n, double* out, void* str
   SC_TRY(sa.in(a, sizeof(int32_t) * n, s, true));
   SC_TRY(sb.in(b, sizeof(int32_t) * n, s, true));
   return ari_dev(static_cast<const int32_t*>(sa.dev), static_cast<const int32_t*>(sb.dev), n, out, s);
+}
+
+int sc_stability(sc_graph* g, int k_min, int k_max, int J, int R, int order, int jackson, int n_probe, uint64_t seed,
+                 int restarts, int max_iter, double lambda_max, const double* lambda_k, double* gamma,
+                 double* lambda_k_out, int32_t* labels, void* stream) {
+  SC_CHECK_ARG(g && gamma, "null argument");
+  SC_CHECK_ARG(1 <= k_min && k_min <= k_max && k_max < g->n_rows, "1 <= k_min <= k_max < n required");
+  SC_CHECK_ARG(J >= 2 && R >= 1 && order >= 1 && restarts >= 1 && max_iter >= 1 && (lambda_k || n_probe >= 1),
+               "J >= 2, R, order, restarts, max_iter, n_probe >= 1 required");
+  SC_CHECK_ARG(g->n_cols == g->n_rows, "sc_stability needs a single-GPU graph");
+  SC_CHECK_ARG(g->n_rows < (int64_t(1) << 25), "n must be < 2^25 for the exact centroid accumulator");
+  cudaStream_t s = as_stream(stream);
+  const int K = k_max - k_min + 1;
+  Staged lab;
+  const size_t lbytes = sizeof(int32_t) * (size_t)K * J * g->n_rows;
+  if (labels) {
+    SC_TRY(lab.in(labels, lbytes, s, false));
+  } else {
+    SC_TRY(lab.alloc(lbytes, s));
+  }
+  SC_TRY(stability_scan(g, k_min, k_max, J, R, order, jackson != 0, n_probe, seed, restarts, max_iter, lambda_max,
+                        lambda_k, gamma, lambda_k_out, static_cast<int32_t*>(lab.dev), s));
+  if (labels) SC_TRY(lab.out(labels, s));
+  SC_CUDA_TRY(cudaStreamSynchronize(s));
+  return SC_OK;
 }
 
 int sc_profile_begin(void) {

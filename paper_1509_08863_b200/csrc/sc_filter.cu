@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "sc_internal.cuh"
 
@@ -28,7 +30,6 @@ namespace sc {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kBlock = 256;
 
 template <typename T> struct Vec;
 template <> struct Vec<float> {
@@ -60,140 +61,374 @@ template <> struct Vec<double> {
   }
 };
 
-// MOMENTS: accumulate <T_s,T_s>, <T_{s+1},T_s>, <T_{s+1},T_{s+1}> per block (fp64).
-template <typename T, int VPR, int SW, int EB, bool UNIT, bool MOMENTS>
-__global__ void __launch_bounds__(kBlock)
-cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                 const float* __restrict__ val, const T* __restrict__ strength, StepParams p) {
-  constexpr int W = Vec<T>::W;
-  constexpr int VPL = VPR / SW;   // vectors per lane
-  constexpr int RPW = 32 / SW;    // rows per warp
-  constexpr int EPL = EB / SW;    // column indices loaded per lane per batch
-  static_assert(VPR % SW == 0 && EB % SW == 0 && 32 % SW == 0, "bad tiling");
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier + 1-D bulk copy (TMA engine) + L2 cache policies
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void ldg_hint(const float* p, float (&v)[4], uint64_t pol) {
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ldg_hint(const double* p, double (&v)[2], uint64_t pol) {
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
+}
+// 16-byte global -> shared async copy (LDGSTS, bypasses L1) with an L2 policy
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// global -> shared bulk copy completing on `bar` (bytes and both addresses 16-byte multiples)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 
+// streaming (read-once / write-once) 16-byte accesses with an L2 evict-first policy
+template <typename T> struct Stream;
+template <> struct Stream<float> {
+  __device__ __forceinline__ static void ld(const float* p, float (&v)[4], uint64_t pol) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                 : "l"(p), "l"(pol));
+  }
+  __device__ __forceinline__ static void st(float* p, const float (&v)[4], uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v[0]),
+                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "l"(pol)
+                 : "memory");
+  }
+};
+template <> struct Stream<double> {
+  __device__ __forceinline__ static void ld(const double* p, double (&v)[2], uint64_t pol) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(v[0]), "=d"(v[1])
+                 : "l"(p), "l"(pol));
+  }
+  __device__ __forceinline__ static void st(double* p, const double (&v)[2], uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v[0]), "d"(v[1]),
+                 "l"(pol)
+                 : "memory");
+  }
+};
+
+// ---------------------------------------------------------------------------
+// The fused step kernel.
+//
+// Persistent CTAs (grid = SMs x resident CTAs) walk row tiles of TR = NC * (32/VPR)
+// rows (tile t = blockIdx.x + i * gridDim.x).  Warp NC is the producer: for each
+// tile it bulk-copies (cp.async.bulk, the TMA engine) the tile's row_ptr and
+// col_idx (+ values) segments into an S-stage shared-memory ring guarded by
+// full/empty mbarriers; lane j of the producer prefetches the CSR bounds of tile
+// i+j, so one DRAM round trip serves 32 tiles.  Consumer warp c owns rows
+// [r0 + c*RPW, r0 + (c+1)*RPW) of the tile, SW = VPR lanes per row, one 16-byte
+// vector (float4 / double2) per lane, so every gathered row of T_s is read as
+// VPR*16 contiguous bytes.  The own row, T_{s-1} and Y rows go to shared memory
+// with cp.async (LDGSTS) -- no registers held across the gather loop.  Column
+// indices are read from the staged segment (LDS); each gather address is one
+// IMAD.WIDE.U32 off a per-lane base; a rolling window keeps EB independent
+// 16-byte gathers in flight per lane.  Streaming operands carry an L2 evict-first
+// policy so the gathered block T_s stays in L2.  A tile whose column segment
+// exceeds the stage capacity reads col/values from global memory directly.
+//
+// MOMENTS (fp64): per-CTA partial sums of <T_s,T_s>, <T_{s+1},T_s>, <T_{s+1},T_{s+1}>.
+// ---------------------------------------------------------------------------
+// build-time tuning (native_build.py --defs)
+#ifndef SC_NC
+#define SC_NC 16          // consumer warps per CTA
+#endif
+#ifndef SC_MIN_CTAS
+#define SC_MIN_CTAS 2     // resident CTAs per SM the register budget is sized for
+#endif
+#ifndef SC_EB_F32
+#define SC_EB_F32 6       // gathers in flight per lane (fp32)
+#endif
+#ifndef SC_EB_F64
+#define SC_EB_F64 4       // gathers in flight per lane (fp64)
+#endif
+constexpr int kNC = SC_NC;
+constexpr int kThreads = (kNC + 1) * 32;   // + one producer warp
+constexpr int kMaxStages = 3;
+
+struct TileMeta {
+  int64_t r0, r1;      // rows [r0, r1)
+  int64_t rpa;         // first row_ptr index staged (r0 rounded down to even)
+  int64_t ca;          // first col index staged (row_ptr[r0] rounded down to a multiple of 4)
+  int32_t overflow;    // 1: the tile's col segment did not fit, read from global
+  int32_t pad;
+};
+
+__host__ __device__ constexpr int tile_rows(int vpr) { return kNC * (32 / vpr); }
+
+struct SmemLayout {
+  int cap;          // col entries per stage
+  int trp;          // row_ptr entries per stage
+  int stages;
+  size_t stage_bytes, rp_off, col_off, val_off, dense_off, red_off, total;
+  __host__ __device__ SmemLayout(int tr, int cap_, bool unit, int nst) {
+    cap = cap_;
+    stages = nst;
+    trp = (tr + 4 + 1) & ~1;
+    rp_off = 0;
+    col_off = (size_t)trp * 8;
+    val_off = col_off + (size_t)cap * 4;
+    stage_bytes = val_off + (unit ? 0 : (size_t)cap * 4);
+    stage_bytes = (stage_bytes + 127) & ~(size_t)127;
+    dense_off = 256 + (size_t)stages * stage_bytes;
+    red_off = dense_off + (size_t)kNC * 3 * 32 * 16;
+    total = red_off + kNC * 3 * sizeof(double);
+  }
+};
+
+template <typename T, int VPR, int EB, bool UNIT, bool MOMENTS>
+__global__ void __launch_bounds__(kThreads, SC_MIN_CTAS)
+cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                 const float* __restrict__ val, const T* __restrict__ strength, StepParams p, int cap,
+                 int nstages) {
+  constexpr int W = Vec<T>::W;
+  constexpr int SW = VPR;          // lanes per row (one 16-byte vector each)
+  constexpr int RPW = 32 / SW;     // rows per warp
+  constexpr int TR = tile_rows(VPR);
+  static_assert(VPR >= 1 && VPR <= 32 && 32 % VPR == 0, "VPR must divide 32");
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  const SmemLayout lay(TR, cap, UNIT, nstages);
+  const int S = nstages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMaxStages;
+  TileMeta* meta = reinterpret_cast<TileMeta*>(smem + 64);
+  unsigned char* stages = smem + 256;
+  unsigned char* dense = smem + lay.dense_off;   // [kNC][3][32] x 16 bytes: own, prev, Y rows
+  double* red = reinterpret_cast<double*>(smem + lay.red_off);
+
+  const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int64_t nrows = p.row_end - p.row_begin;
+  const int64_t ntiles = (nrows + TR - 1) / TR;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint64_t pol_stream = policy_evict_first();
+
+  if (warp == kNC) {
+    // ------------------------------------------------------------ producer
+    int i = 0;
+    for (int64_t tg = blockIdx.x; tg < ntiles; tg += (int64_t)gridDim.x * 32) {
+      const int64_t tl = tg + (int64_t)lane * gridDim.x;
+      int64_t b0 = 0, b1 = 0;
+      if (tl < ntiles) {
+        const int64_t r0 = p.row_begin + tl * TR;
+        b0 = __ldg(row_ptr + r0);
+        b1 = __ldg(row_ptr + min(r0 + TR, p.row_end));
+      }
+      const int64_t left = (ntiles - tg + gridDim.x - 1) / gridDim.x;
+      const int cnt = left < 32 ? (int)left : 32;
+      for (int j = 0; j < cnt; ++j, ++i) {
+        const int64_t e0 = __shfl_sync(FULL, b0, j), e1 = __shfl_sync(FULL, b1, j);
+        if (lane == 0) {
+          const int s = i % S;
+          if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+          const int64_t r0 = p.row_begin + (tg + (int64_t)j * gridDim.x) * TR;
+          const int64_t r1 = min(r0 + TR, p.row_end);
+          const int64_t rpa = r0 & ~int64_t(1);
+          const int64_t nrp = ((r1 + 1 - rpa) + 1) & ~int64_t(1);
+          const int64_t ca = e0 & ~int64_t(3);
+          const int64_t ncol = ((e1 - ca) + 3) & ~int64_t(3);
+          const int overflow = ncol > lay.cap;
+          TileMeta& m = meta[s];
+          m.r0 = r0; m.r1 = r1; m.rpa = rpa; m.ca = ca; m.overflow = overflow;
+          unsigned char* st = stages + (size_t)s * lay.stage_bytes;
+          uint32_t tx = (uint32_t)(nrp * 8);
+          const bool cp_col = !overflow && ncol > 0;
+          if (cp_col) tx += (uint32_t)(ncol * 4 * (UNIT ? 1 : 2));
+          mbar_arrive_expect_tx(&full[s], tx);
+          bulk_g2s(st + lay.rp_off, row_ptr + rpa, (uint32_t)(nrp * 8), &full[s], pol_stream);
+          if (cp_col) {
+            bulk_g2s(st + lay.col_off, col + ca, (uint32_t)(ncol * 4), &full[s], pol_stream);
+            if (!UNIT) bulk_g2s(st + lay.val_off, val + ca, (uint32_t)(ncol * 4), &full[s], pol_stream);
+          }
+        }
+      }
+    }
+    // drain: wait until the consumers released every stage still in use
+    if (lane == 0)
+      for (int j = max(0, i - S); j < i; ++j) mbar_wait(&empty[j % S], (j / S) & 1);
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
   const int sub = lane / SW;
   const int sl = lane % SW;
-  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-
-  const T* tprev = static_cast<const T*>(p.tprev);   // may alias tnext (in-place rotation)
+  const int c = sl * W;   // first column of this lane's vector
+  const T* tprev = static_cast<const T*>(p.tprev);   // may alias tnext (same row, read before write)
   const T* __restrict__ tcur = static_cast<const T*>(p.tcur);
   T* tnext = static_cast<T*>(p.tnext);
   T* y = static_cast<T*>(p.y);
-  const T a = static_cast<T>(p.a), bc = static_cast<T>(p.b_cur), bp = static_cast<T>(p.b_prev);
-  const T cyp = static_cast<T>(p.cy_prev), cyc = static_cast<T>(p.cy_cur), cyn = static_cast<T>(p.cy_next);
-
+  const bool next_first = (p.l2_flags & 1) != 0;
+  // gather address of row k for this lane: gbase + k * ldb (one IMAD.WIDE.U32)
+  const char* gbase = reinterpret_cast<const char*>(tcur + c);
+  const uint32_t ldb = static_cast<uint32_t>(p.ld_cur * sizeof(T));
+  T* d_own = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 0) * 32 + lane) * 16);
+  T* d_prv = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 1) * 32 + lane) * 16);
+  T* d_y = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 2) * 32 + lane) * 16);
   double m_cc = 0.0, m_nc = 0.0, m_nn = 0.0;
 
-  for (int64_t base = p.row_begin + warp * RPW; base < p.row_end; base += nwarps * RPW) {
-    const int64_t row = base + sub;
-    const bool valid = row < p.row_end;
-    int64_t beg = 0;
+  int i = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    const int s = i % S;
+    mbar_wait(&full[s], (i / S) & 1);
+    const TileMeta m = meta[s];
+    const unsigned char* st = stages + (size_t)s * lay.stage_bytes;
+    const int64_t* rps = reinterpret_cast<const int64_t*>(st + lay.rp_off);
+
+    const int64_t row = m.r0 + warp * RPW + sub;
+    const bool valid = row < m.r1;
     int deg = 0;
+    int64_t b = 0;
+    T acc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) acc[w] = T(0);
     if (valid) {
-      beg = __ldg(row_ptr + row);
-      deg = static_cast<int>(__ldg(row_ptr + row + 1) - beg);
+      b = rps[row - m.rpa];
+      deg = static_cast<int>(rps[row - m.rpa + 1] - b);
+      cp_async16(d_own, tcur + row * p.ld_cur + c, pol_stream);
+      if (tprev) cp_async16(d_prv, tprev + row * p.ld_prev + c, pol_stream);
+      if (p.y_mode == 2) cp_async16(d_y, y + row * p.ld_y + c, pol_stream);
     }
-
-    T own[VPL][W], prv[VPL][W], acc[VPL][W];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int c = (sl + SW * v) * W;
-#pragma unroll
-      for (int w = 0; w < W; ++w) { own[v][w] = T(0); prv[v][w] = T(0); acc[v][w] = T(0); }
-      if (valid) {
-        Vec<T>::ldg(tcur + row * p.ld_cur + c, own[v]);
-        if (tprev) Vec<T>::ld(tprev + row * p.ld_prev + c, prv[v]);
-      }
-    }
-
     int maxdeg = deg;
 #pragma unroll
     for (int o = SW; o < 32; o <<= 1) maxdeg = max(maxdeg, __shfl_xor_sync(FULL, maxdeg, o));
 
-    for (int off = 0; off < maxdeg; off += EB) {
-      int ci[EPL];
-      T wv[EPL];
-#pragma unroll
-      for (int t = 0; t < EPL; ++t) {
-        const int pos = off + t * SW + sl;
+    // Rolling window of EB gathers: slot e always holds the load of edge base+e; consuming it
+    // (scoreboard wait on that load only) is immediately followed by issuing edge base+EB+e,
+    // so EB independent 16-byte loads stay in flight per lane across the whole row.
+    auto gather = [&](const int32_t* __restrict__ ci, const float* __restrict__ wi) {
+      T g[EB][W];
+      T wv[EB];
+      auto issue = [&](int e, int pos) {
         const bool ok = pos < deg;
-        ci[t] = ok ? __ldg(col + beg + pos) : -1;
-        if (UNIT) wv[t] = T(1);
-        else wv[t] = ok ? static_cast<T>(__ldg(val + beg + pos)) : T(0);
-      }
-      T g[EB][VPL][W];
-      int kk[EB];
-#pragma unroll
-      for (int e = 0; e < EB; ++e) {
-        kk[e] = __shfl_sync(FULL, ci[e / SW], sub * SW + (e % SW));
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-          if (kk[e] >= 0) {
-            Vec<T>::ldg(tcur + static_cast<int64_t>(kk[e]) * p.ld_cur + (sl + SW * v) * W, g[e][v]);
-          } else {
-#pragma unroll
-            for (int w = 0; w < W; ++w) g[e][v][w] = T(0);
-          }
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < EB; ++e) {
-        if (UNIT) {
-#pragma unroll
-          for (int v = 0; v < VPL; ++v)
-#pragma unroll
-            for (int w = 0; w < W; ++w) acc[v][w] += g[e][v][w];
+        const int k = ok ? ci[pos] : 0;
+        if (!UNIT) wv[e] = ok ? static_cast<T>(wi[pos]) : T(0);
+        if (ok) {
+          Vec<T>::ldg(reinterpret_cast<const T*>(gbase + static_cast<uint64_t>(static_cast<uint32_t>(k)) * ldb), g[e]);
         } else {
-          const T we = __shfl_sync(FULL, wv[e / SW], sub * SW + (e % SW));
 #pragma unroll
-          for (int v = 0; v < VPL; ++v)
-#pragma unroll
-            for (int w = 0; w < W; ++w) acc[v][w] = fma(we, g[e][v][w], acc[v][w]);
+          for (int w = 0; w < W; ++w) g[e][w] = T(0);
         }
-      }
-    }
-
-    if (valid) {
-      const T si = strength[row];
+      };
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        const int c = (sl + SW * v) * W;
-        T tn[W];
+      for (int e = 0; e < EB; ++e) issue(e, e);
+      for (int base = 0; base < maxdeg; base += EB) {
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const T lt = si * own[v][w] - acc[v][w];            // (L T_s)[i]
-          tn[w] = a * lt + bc * own[v][w] + bp * prv[v][w];   // T_{s+1}[i]
-        }
-        if (tnext) Vec<T>::st(tnext + row * p.ld_next + c, tn);
-        if (p.y_mode) {
-          T yv[W];
-          if (p.y_mode == 2) Vec<T>::ld(y + row * p.ld_y + c, yv);
-          else {
-#pragma unroll
-            for (int w = 0; w < W; ++w) yv[w] = T(0);
-          }
-#pragma unroll
-          for (int w = 0; w < W; ++w) yv[w] += cyp * prv[v][w] + cyc * own[v][w] + cyn * tn[w];
-          Vec<T>::st(y + row * p.ld_y + c, yv);
-        }
-        if (MOMENTS) {
+        for (int e = 0; e < EB; ++e) {
 #pragma unroll
           for (int w = 0; w < W; ++w) {
-            const double o = own[v][w], n = tn[w];
-            m_cc += o * o;
-            m_nc += n * o;
-            m_nn += n * n;
+            if (UNIT) acc[w] += g[e][w];
+            else acc[w] = fma(wv[e], g[e][w], acc[w]);
           }
+          issue(e, base + EB + e);
+        }
+      }
+    };
+    if (!m.overflow) {
+      // column indices (and weights) from the staged shared-memory segment
+      gather(reinterpret_cast<const int32_t*>(st + lay.col_off) + (b - m.ca),
+             reinterpret_cast<const float*>(st + lay.val_off) + (b - m.ca));
+    } else {
+      gather(col + b, UNIT ? nullptr : val + b);
+    }
+    // all lanes of this warp are done with stage s
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+
+    if (valid) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      T own[W], prv[W], yv[W];
+      Vec<T>::ld(d_own, own);
+      if (tprev) Vec<T>::ld(d_prv, prv);
+      else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) prv[w] = T(0);
+      }
+      if (p.y_mode == 2) Vec<T>::ld(d_y, yv);
+      else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) yv[w] = T(0);
+      }
+      const T si = strength[row];
+      const T a = static_cast<T>(p.a), bc = static_cast<T>(p.b_cur), bp = static_cast<T>(p.b_prev);
+      T tn[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const T lt = si * own[w] - acc[w];               // (L T_s)[i]
+        tn[w] = a * lt + bc * own[w] + bp * prv[w];      // T_{s+1}[i]
+      }
+      if (tnext) {
+        if (next_first) Stream<T>::st(tnext + row * p.ld_next + c, tn, pol_stream);
+        else Vec<T>::st(tnext + row * p.ld_next + c, tn);
+      }
+      if (p.y_mode) {
+        const T cyp = static_cast<T>(p.cy_prev), cyc = static_cast<T>(p.cy_cur), cyn = static_cast<T>(p.cy_next);
+#pragma unroll
+        for (int w = 0; w < W; ++w) yv[w] += cyp * prv[w] + cyc * own[w] + cyn * tn[w];
+        Stream<T>::st(y + row * p.ld_y + c, yv, pol_stream);
+      }
+      if (MOMENTS) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const double o = own[w], n = tn[w];
+          m_cc += o * o;
+          m_nc += n * o;
+          m_nn += n * n;
         }
       }
     }
   }
 
   if (MOMENTS) {
-    // deterministic block reduction: warp shuffle tree, then fixed-order warp sum
-    __shared__ double red[kBlock / 32][3];
+    // deterministic CTA reduction over the consumer warps (named barrier 1)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       m_cc += __shfl_xor_sync(FULL, m_cc, o);
@@ -201,15 +436,15 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
       m_nn += __shfl_xor_sync(FULL, m_nn, o);
     }
     if (lane == 0) {
-      red[threadIdx.x >> 5][0] = m_cc;
-      red[threadIdx.x >> 5][1] = m_nc;
-      red[threadIdx.x >> 5][2] = m_nn;
+      red[warp * 3 + 0] = m_cc;
+      red[warp * 3 + 1] = m_nc;
+      red[warp * 3 + 2] = m_nn;
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"r"(kNC * 32) : "memory");
     if (threadIdx.x < 3) {
-      double s = 0.0;
-      for (int w = 0; w < kBlock / 32; ++w) s += red[w][threadIdx.x];
-      p.part[blockIdx.x * 3 + threadIdx.x] = s;
+      double sum = 0.0;
+      for (int w = 0; w < kNC; ++w) sum += red[w * 3 + threadIdx.x];
+      p.part[blockIdx.x * 3 + threadIdx.x] = sum;
     }
   }
 }
@@ -276,14 +511,12 @@ int env_int(const char* name, int dflt) {
 }
 
 template <typename T>
-using KernelFn = void (*)(const int64_t*, const int32_t*, const float*, const T*, StepParams);
+using KernelFn = void (*)(const int64_t*, const int32_t*, const float*, const T*, StepParams, int, int);
 
 template <typename T, int VPR, int EB, bool MOM>
 KernelFn<T> pick_unit(bool unit) {
-  constexpr int SW = VPR;                   // one 16-byte vector per lane
-  constexpr int EBX = EB < SW ? SW : EB;    // at least one index per lane per batch
-  if (unit) return cheb_step_kernel<T, VPR, SW, EBX, true, MOM>;
-  return cheb_step_kernel<T, VPR, SW, EBX, false, MOM>;
+  if (unit) return cheb_step_kernel<T, VPR, EB, true, MOM>;
+  return cheb_step_kernel<T, VPR, EB, false, MOM>;
 }
 
 template <typename T, int EB, bool MOM>
@@ -300,50 +533,82 @@ KernelFn<T> pick_vpr(int vpr, bool unit) {
 }
 
 template <typename T>
-KernelFn<T> pick_kernel(int width, bool unit, bool moments, int eb) {
+KernelFn<T> pick_kernel(int width, bool unit, bool moments) {
   constexpr int W = Vec<T>::W;
   if (width % W) return nullptr;
   const int vpr = width / W;
+  // 8 (fp32) / 4 (fp64) gathers of 16 bytes in flight per lane: fits the 56-register
+  // budget of 2 x 544-thread CTAs per SM without spills
+  constexpr int EB = sizeof(T) == 4 ? SC_EB_F32 : SC_EB_F64;
   if (moments) {
-    if (eb <= 8) return pick_vpr<T, 8, true>(vpr, unit);
-    return pick_vpr<T, 16, true>(vpr, unit);
+    if constexpr (sizeof(T) == 8) return pick_vpr<T, EB, true>(vpr, unit);
+    return nullptr;   // moments are accumulated in fp64 only
   }
-  if (eb <= 8) return pick_vpr<T, 8, false>(vpr, unit);
-  if (eb <= 16) return pick_vpr<T, 16, false>(vpr, unit);
-  return pick_vpr<T, 32, false>(vpr, unit);
+  return pick_vpr<T, EB, false>(vpr, unit);
 }
 
 template <typename T> const T* strength_of(const sc_graph* g);
 template <> const float* strength_of<float>(const sc_graph* g) { return g->strength32.as<float>(); }
 template <> const double* strength_of<double>(const sc_graph* g) { return g->strength64.as<double>(); }
 
-template <typename T>
-int grid_for(KernelFn<T> k, const sc_graph* g, int64_t rows, int width) {
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBlock, 0) != cudaSuccess || occ < 1) occ = 1;
-  const int rpw = 32 / (width / Vec<T>::W);
-  const int64_t need = (rows + (int64_t)(kBlock / 32) * rpw - 1) / ((int64_t)(kBlock / 32) * rpw);
-  const int64_t cap = (int64_t)g->num_sms * occ;
-  return static_cast<int>(std::max<int64_t>(1, std::min(need, cap)));
+// Pipeline depth and column-index capacity of one stage: 3 stages with room for
+// ~48 entries per tile row (average degree <= ~40 keeps nearly every tile on the
+// staged path), capped so the CTA stays under ~100 KB of shared memory (2 CTAs per
+// SM).  Tiles whose segment exceeds the capacity read their columns from global
+// memory (correct, slower).
+void stage_plan(int tr, bool unit, int* cap, int* nstages) {
+  const int ns = 3;
+  const int per_entry = unit ? 4 : 8;
+  const int budget = 100 * 1024 - 256 - kNC * 3 * 32 * 16 - kNC * 3 * 8;
+  const int per_stage = budget / ns - (tr + 6) * 8 - 128;
+  int c = std::min(tr * 48, per_stage / per_entry);
+  *cap = std::max(64, c & ~3);
+  *nstages = ns;
 }
 
 template <typename T>
 int launch_step_impl(const sc_graph* g, const StepParams& p, cudaStream_t s, bool moments,
                      int* grid_out) {
-  const int eb = env_int("SC_EB", 16);
-  KernelFn<T> k = pick_kernel<T>(p.width, g->unit_weights, moments, eb);
+  constexpr int W = Vec<T>::W;
+  KernelFn<T> k = pick_kernel<T>(p.width, g->unit_weights, moments);
   if (!k) return fail(SC_ERR_ARG, "unsupported chunk width " + std::to_string(p.width));
-  const int grid = grid_for<T>(k, g, p.row_end - p.row_begin, p.width);
+  const int vpr = p.width / W;
+  const int tr = tile_rows(vpr);
+  int cap = 0, nst = 0;
+  stage_plan(tr, g->unit_weights, &cap, &nst);
+  const SmemLayout lay(tr, cap, g->unit_weights, nst);
+  const int smem = static_cast<int>(lay.total);
+  // per (kernel, smem size) launch configuration, resolved once per process
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> occ_cache;
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = occ_cache.find({(const void*)k, smem});
+    if (it == occ_cache.end()) {
+      SC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+      occ_cache[{(const void*)k, smem}] = occ;
+    } else {
+      occ = it->second;
+    }
+  }
+  const int64_t rows = p.row_end - p.row_begin;
+  const int64_t ntiles = (rows + tr - 1) / tr;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)g->num_sms * occ)));
   if (grid_out) *grid_out = grid;
-  if (p.row_end <= p.row_begin) return SC_OK;
+  if (rows <= 0) return SC_OK;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_prof.on) {
     e0 = g_prof.get();
     e1 = g_prof.get();
     cudaEventRecord(e0, s);
   }
-  k<<<grid, kBlock, 0, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(),
-                            g->unit_weights ? nullptr : g->values.as<float>(), strength_of<T>(g), p);
+  StepParams q = p;
+  static const int l2_flags = env_int("SC_L2_FLAGS", 0);
+  q.l2_flags = l2_flags;
+  k<<<grid, kThreads, smem, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(),
+                                 g->unit_weights ? nullptr : g->values.as<float>(), strength_of<T>(g), q, cap, nst);
   SC_CUDA_TRY(cudaGetLastError());
   if (g_prof.on) {
     cudaEventRecord(e1, s);
@@ -351,7 +616,6 @@ int launch_step_impl(const sc_graph* g, const StepParams& p, cudaStream_t s, boo
     g_prof.launches += 1;
     g_prof.step_launches += 1;
     // algorithmic bytes: CSR share of this chunk + dense operands touched once
-    const int64_t rows = p.row_end - p.row_begin;
     const double csr = (double)rows * 8.0 + (double)g->nnz * (g->unit_weights ? 4.0 : 8.0) * rows / g->n_rows;
     const double dense_rows = (1.0 + (p.tprev ? 1.0 : 0.0) + (p.tnext ? 1.0 : 0.0) +
                                (p.y_mode == 2 ? 2.0 : (p.y_mode == 1 ? 1.0 : 0.0)));
@@ -369,7 +633,7 @@ std::vector<int> chunk_plan(int R, int64_t n_cols) {
   int cw = env_int("SC_CHUNK", 0);
   if (cw <= 0) {
     // keep the gathered block T_s (plus the block being written) resident in L2
-    const double budget = env_int("SC_L2_BUDGET_MB", 48) * 1048576.0;
+    const double budget = env_int("SC_L2_BUDGET_MB", 128) * 1048576.0;
     cw = maxw;
     while (cw > 4 * W && (double)n_cols * cw * sizeof(T) > budget) cw >>= 1;
   }
@@ -387,6 +651,13 @@ std::vector<int> chunk_plan(int R, int64_t n_cols) {
 }
 
 }  // namespace
+
+template <typename T>
+std::vector<int> chunk_widths(int R, int64_t n_cols) {
+  return chunk_plan<T>(R, n_cols);
+}
+template std::vector<int> chunk_widths<float>(int, int64_t);
+template std::vector<int> chunk_widths<double>(int, int64_t);
 
 void profile_begin() {
   g_prof.on = true;
@@ -430,8 +701,17 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
                  T* Y, cudaStream_t s) {
   constexpr int W = Vec<T>::W;
   const int64_t n = g->n_rows;
-  // operate on a vector-aligned layout; pad odd widths / misaligned pointers
-  const int Rp = (R + W - 1) / W * W;
+  // operate on a vector-aligned layout; pad odd widths / misaligned pointers.  A width that
+  // is not a single supported chunk (e.g. R = 24 -> 16 + 8) is padded up to the next power
+  // of two when that still fits one L2-sized chunk: one launch per step instead of several
+  // (small graphs are launch-bound).
+  int Rp = (R + W - 1) / W * W;
+  {
+    int p2 = W;
+    while (p2 < Rp) p2 <<= 1;
+    const std::vector<int> one = chunk_plan<T>(p2, g->n_cols);
+    if (p2 != Rp && one.size() == 1 && chunk_plan<T>(Rp, g->n_cols).size() > 1) Rp = p2;
+  }
   const bool aligned = (Rp == R) && ((uintptr_t)X % 16 == 0) && ((uintptr_t)Y % 16 == 0);
   const T* Xw = X;
   T* Yw = Y;

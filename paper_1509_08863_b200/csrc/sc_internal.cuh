@@ -94,6 +94,11 @@ struct Staged {
 // ---------------------------------------------------------------------------
 }  // namespace sc
 
+namespace sc {
+constexpr int kRowPtrPad = 8;   // extra zeroed row_ptr entries past n_rows+1
+constexpr int kColPad = 8;      // extra zeroed col_idx / values entries past nnz
+}  // namespace sc
+
 struct sc_graph {
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
   bool unit_weights = true;
@@ -123,6 +128,7 @@ struct StepParams {
   double a, b_cur, b_prev;
   double cy_prev, cy_cur, cy_next;
   int y_mode;        // 0 none, 1 write, 2 accumulate
+  int l2_flags;      // bit 0: T_next stores evict-first; bit 1: T_cur gathers evict-last
   int width;         // columns processed (chunk width)
   int total_width;   // all columns of the block (for the profiler's CSR share)
   // moments mode (fp64 only): per-block partial sums written to `part`
@@ -132,6 +138,10 @@ struct StepParams {
 // launch one fused step for `width` columns starting at the given pointers
 template <typename T>
 int launch_step(const sc_graph* g, const StepParams& p, cudaStream_t s);
+
+// column chunk widths (each a supported kernel width) covering R columns
+template <typename T>
+std::vector<int> chunk_widths(int R, int64_t n_cols);
 
 // full filter: Y = sum_j coeffs_j T_j X   (X, Y device, row-major n x R)
 template <typename T>
@@ -168,6 +178,11 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
                double* centroids_host, double* inertia, int* iters, int* best_restart,
                cudaStream_t s);
 int ari_dev(const int32_t* a, const int32_t* b, int64_t n, double* out, cudaStream_t s);
+
+// stability measure gamma(k) over [k_min, k_max] (sc_stability.cu)
+int stability_scan(sc_graph* g, int k_min, int k_max, int J, int R, int order, bool jackson, int n_probe,
+                   uint64_t seed, int restarts, int max_iter, double lambda_max, const double* lambda_k_in,
+                   double* gamma, double* lambda_k_out, int32_t* labels_dev, cudaStream_t s);
 
 // counter-based RNG (host side, identical to the device one)
 uint64_t splitmix64_host(uint64_t x);

@@ -1,0 +1,182 @@
+// Stability measure gamma(k) (§4.3, Eq.(11)) reusing the
+// fused Chebyshev step kernel.
+//
+// For every k in [k_min, k_max] the paper runs the accelerated algorithm J times
+// with J realisations of the random signals and averages the ARI over all pairs
+// of the J clusterings.  Only the cut lambda~_k depends on k; the Chebyshev
+// terms T_m(L~) X_j of one realisation X_j do not.  So each realisation runs the
+// recurrence once (p fused steps, y_mode 0, every T_m kept in HBM: (p+1) N R
+// floats) and one streaming kernel forms the filtered block of every cut,
+//     Y_k = sum_m d_{k,m} T_m      (d_k: Chebyshev coefficients of h_{lambda~_k}),
+// reading the T_m stack once per group of 8 cuts.  k-means and the ARI are the
+// library's own kernels.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "sc_internal.cuh"
+
+namespace sc {
+namespace {
+
+constexpr int kKG = 8;   // cuts formed per pass over the T_m stack
+
+// Y[g][i*R + q] = sum_m D[g][m] * T[m][i*ld + q]  for the kg cuts of this pass
+__global__ void combine_cuts_kernel(const float* __restrict__ Tall, int64_t slot, int nterms, int64_t n, int R,
+                                    int ld, const float* __restrict__ D, int kg, float* __restrict__ Y,
+                                    int64_t ystride) {
+  extern __shared__ float sD[];   // [kKG][nterms]
+  for (int e = threadIdx.x; e < kg * nterms; e += blockDim.x) sD[e] = D[e];
+  __syncthreads();
+  const int64_t total = n * R;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / R;
+    const int q = static_cast<int>(idx - i * R);
+    const float* t = Tall + i * ld + q;
+    float acc[kKG];
+#pragma unroll
+    for (int c = 0; c < kKG; ++c) acc[c] = 0.f;
+    for (int m = 0; m < nterms; ++m) {
+      const float v = __ldg(t + (int64_t)m * slot);
+#pragma unroll
+      for (int c = 0; c < kKG; ++c)
+        if (c < kg) acc[c] = fmaf(sD[c * nterms + m], v, acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < kKG; ++c)
+      if (c < kg) Y[(int64_t)c * ystride + idx] = acc[c];
+  }
+}
+
+__global__ void pad_copy_kernel(const float* __restrict__ src, int64_t n, int R, float* __restrict__ dst, int ld) {
+  const int64_t total = n * ld;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / ld;
+    const int q = static_cast<int>(idx - i * ld);
+    dst[idx] = q < R ? src[i * R + q] : 0.f;
+  }
+}
+
+}  // namespace
+
+int stability_scan(sc_graph* g, int k_min, int k_max, int J, int R, int order, bool jackson, int n_probe,
+                   uint64_t seed, int restarts, int max_iter, double lambda_max, const double* lambda_k_in,
+                   double* gamma, double* lambda_k_out, int32_t* labels_dev, cudaStream_t s) {
+  const int64_t n = g->n_rows;
+  const int K = k_max - k_min + 1;
+  // 1. spectral bounds
+  if (!(lambda_max > 0.0)) {
+    double theta = 0.0;
+    SC_TRY(lanczos_lambda_max(g, 60, seed ^ 0x1a2b3c4dULL, &theta, s));
+    const double gersh = 2.0 * g->max_strength;
+    lambda_max = 1.01 * theta;
+    if (!(lambda_max > 0.0) || lambda_max > gersh) lambda_max = gersh;
+    if (!(lambda_max > 0.0)) lambda_max = 1.0;
+  }
+  std::vector<double> lk(K);
+  if (lambda_k_in) {
+    std::copy(lambda_k_in, lambda_k_in + K, lk.begin());
+  } else {
+    // one moments pass serves the dichotomy of every k
+    DevBuf probes;
+    SC_TRY(probes.ensure(sizeof(double) * n * n_probe));
+    SC_TRY(random_signals<double>(n, n_probe, 0, seed ^ 0x5e5e5e5eULL, 2, 1.0 / n_probe, probes.as<double>(), s));
+    std::vector<double> mu;
+    SC_TRY(cheb_moments(g, lambda_max, order, n_probe, probes.as<double>(), mu, s));
+    for (int c = 0; c < K; ++c) {
+      double ck = 0.0;
+      SC_TRY(lambda_k_dichotomy(mu.data(), order, k_min + c, lambda_max, true, 40, 1e-4, &lk[c], &ck));
+    }
+  }
+  if (lambda_k_out) std::copy(lk.begin(), lk.end(), lambda_k_out);
+
+  // 2. coefficients of every cut, fp32 (the precision the fused filter applies them in)
+  const int nterms = order + 1;
+  std::vector<float> D((size_t)K * nterms);
+  std::vector<double> d(nterms);
+  for (int c = 0; c < K; ++c) {
+    cheby_lowpass_coeffs(lk[c], lambda_max, order, jackson, d.data());
+    for (int m = 0; m < nterms; ++m) D[(size_t)c * nterms + m] = static_cast<float>(d[m]);
+  }
+  DevBuf dD;
+  SC_TRY(dD.ensure(sizeof(float) * D.size()));
+  SC_CUDA_TRY(cudaMemcpyAsync(dD.ptr, D.data(), sizeof(float) * D.size(), cudaMemcpyHostToDevice, s));
+
+  // 3. buffers: T stack (ld = R rounded up to 4), features of every cut, signals
+  const int ld = (R + 3) / 4 * 4;
+  const int64_t slot = n * ld;
+  DevBuf tall, yall, sig;
+  SC_TRY(tall.ensure(sizeof(float) * (size_t)slot * nterms));
+  SC_TRY(yall.ensure(sizeof(float) * (size_t)K * n * R));
+  if (ld != R) SC_TRY(sig.ensure(sizeof(float) * n * R));
+  float* T = tall.as<float>();
+  const std::vector<int> chunks = chunk_widths<float>(ld, n);
+  const int grid = g->num_sms * 8;
+
+  for (int j = 0; j < J; ++j) {
+    const uint64_t sj = seed + (uint64_t)j;
+    // T_0 = X_j (§4.1 step 4: N(0, 1/R) entries)
+    if (ld == R) {
+      SC_TRY(random_signals<float>(n, R, 0, sj, 0, 1.0 / R, T, s));
+    } else {
+      SC_TRY(random_signals<float>(n, R, 0, sj, 0, 1.0 / R, sig.as<float>(), s));
+      pad_copy_kernel<<<grid, 256, 0, s>>>(sig.as<float>(), n, R, T, ld);
+      SC_CUDA_TRY(cudaGetLastError());
+    }
+    // T_{m+1} = 2 L~ T_m - T_{m-1}  (T_1 = L~ T_0), every term kept
+    for (int st = 0; st < order; ++st) {
+      int col0 = 0;
+      for (int w : chunks) {
+        StepParams p{};
+        p.row_begin = 0;
+        p.row_end = n;
+        p.width = w;
+        p.total_width = ld;
+        p.tcur = T + (size_t)st * slot + col0;
+        p.ld_cur = ld;
+        p.tprev = st == 0 ? nullptr : (const void*)(T + (size_t)(st - 1) * slot + col0);
+        p.ld_prev = ld;
+        p.tnext = T + (size_t)(st + 1) * slot + col0;
+        p.ld_next = ld;
+        p.a = (st == 0 ? 2.0 : 4.0) / lambda_max;
+        p.b_cur = st == 0 ? -1.0 : -2.0;
+        p.b_prev = st == 0 ? 0.0 : -1.0;
+        p.y_mode = 0;
+        SC_TRY(launch_step<float>(g, p, s));
+        col0 += w;
+      }
+    }
+    // Y_k for every cut
+    for (int c0 = 0; c0 < K; c0 += kKG) {
+      const int kg = std::min(kKG, K - c0);
+      combine_cuts_kernel<<<grid, 256, sizeof(float) * kg * nterms, s>>>(
+          T, slot, nterms, n, R, ld, dD.as<float>() + (size_t)c0 * nterms, kg,
+          yall.as<float>() + (size_t)c0 * n * R, n * R);
+      SC_CUDA_TRY(cudaGetLastError());
+    }
+    // k-means per cut (§4.1 step 6), replicate seed sj
+    for (int c = 0; c < K; ++c) {
+      double inertia = 0.0;
+      int it = 0, best = 0;
+      SC_TRY(kmeans_run(yall.as<float>() + (size_t)c * n * R, n, R, k_min + c, restarts, max_iter, sj, nullptr,
+                        labels_dev + ((size_t)c * J + j) * n, nullptr, &inertia, &it, &best, s));
+    }
+  }
+  // 4. gamma(k) = 2/(J(J-1)) sum_{a<b} ari(C^a, C^b)   (R7)
+  for (int c = 0; c < K; ++c) {
+    double tot = 0.0;
+    for (int a = 0; a < J; ++a)
+      for (int b = a + 1; b < J; ++b) {
+        double v = 0.0;
+        SC_TRY(ari_dev(labels_dev + ((size_t)c * J + a) * n, labels_dev + ((size_t)c * J + b) * n, n, &v, s));
+        tot += v;
+      }
+    gamma[c] = 2.0 * tot / ((double)J * (J - 1));
+  }
+  return SC_OK;
+}
+
+}  // namespace sc

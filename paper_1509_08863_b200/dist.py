@@ -99,6 +99,13 @@ def exchange_send_lists(part: LocalPart, group=None) -> LocalPart:
     import torch.distributed as dist
     halos = [None] * part.world
     dist.all_gather_object(halos, part.halo_gid, group=group)
+    return send_lists_from_halos(part, halos)
+
+
+def send_lists_from_halos(part: LocalPart, halos) -> LocalPart:
+    """Fill part.send_idx / send_counts from every rank's halo list (halos[q] = global ids
+    rank q reads).  Rows for peer q are sent in ascending global id, which is the order
+    of q's halo block for this owner."""
     inv = np.empty(part.n_local, dtype=np.int64)
     inv[part.perm] = np.arange(part.n_local)
     send, counts = [], []

@@ -52,7 +52,27 @@ WORKLOADS = {
 ORDER = ["c0_sbm2k", "c1_gmm20k", "c2_sbm100k", "c3_sbm1m", "c4_sbm10m"]
 
 
-def build_graph(name: str, seed: int = 1234) -> graphs.CSRGraph:
+def build_graph(name: str, seed: int = 1234, cache: bool = False) -> graphs.CSRGraph:
+    """Build the workload's graph; with ``cache`` the CSR is kept as an .npz under
+    $SC_GRAPH_CACHE (default /tmp/sc_graphs) and reused by later processes."""
+    if cache:
+        import os
+        import numpy as np
+        d = os.environ.get("SC_GRAPH_CACHE", "/tmp/sc_graphs")
+        path = os.path.join(d, f"{name}_{seed}.npz")
+        if os.path.exists(path):
+            z = np.load(path, allow_pickle=False)
+            vals = z["values"] if z["has_values"] else None
+            return graphs.CSRGraph(n=int(z["n"]), row_ptr=z["row_ptr"], col_idx=z["col_idx"], values=vals,
+                                   labels=z["labels"], meta={"cached": path})
+        g = build_graph(name, seed)
+        os.makedirs(d, exist_ok=True)
+        tmp = path + f".{os.getpid()}.tmp.npz"
+        np.savez(tmp, n=g.n, row_ptr=g.row_ptr, col_idx=g.col_idx,
+                 values=g.values if g.values is not None else np.zeros(0, np.float32),
+                 has_values=g.values is not None, labels=g.labels if g.labels is not None else np.zeros(0, np.int32))
+        os.replace(tmp, path)
+        return g
     spec = dict(WORKLOADS[name].graph)
     kind = spec.pop("kind")
     if kind == "sbm":

@@ -338,10 +338,119 @@ def test_ari_matches_oracle(sc):
 # pipeline
 # ---------------------------------------------------------------------------
 
-def test_cluster_pipeline_recovers_c0(sc):
-    g = scinputs.sbm(2000, 5, 10, 0.1, seed=1234)
+def test_cluster_pipeline_recovers_planted_sbm(sc):
+    # configs[0]'s own graph (avg degree 10, eps 0.1) is NOT recoverable by spectral
+    # clustering on the combinatorial Laplacian: its lambda_2..lambda_5 interleave with
+    # modes localised on low-degree nodes, and exact classical SC scores ARI 0.0 there
+    # (reading R11).  A denser SBM of the same size is recovered exactly.
+    g = scinputs.sbm(2000, 5, 20, 0.05, seed=1234)
     G = sc.Graph.from_csr(g)
     lab = np.zeros(g.n, dtype=np.int32)
-    info = sc.sc_cluster(G.handle, 5, 32, 50, True, 32, 2024, 10, 100, False, lab)
-    assert oari.ari(lab, g.labels) > 0.9
-    assert info[2] >= 4.5
+    info = sc.sc_cluster(G.handle, 5, 32, 60, True, 32, 2024, 10, 100, False, lab)
+    assert oari.ari(lab, g.labels) > 0.95
+    assert 4.5 <= info[2] <= 5.5
+    ev = np.linalg.eigvalsh(laplacian.laplacian_dense(g))
+    assert ev[-1] <= info[0] <= 1.02 * ev[-1]
+
+
+# ---------------------------------------------------------------------------
+# stability measure gamma(k) (§4.3 Eq.(11))
+# ---------------------------------------------------------------------------
+
+def _oracle_stability(g, ks, lks, lmax, J, R, order, jackson, seed, restarts, max_iter):
+    from oracle import stability
+    L = laplacian.laplacian(g)
+    out, labs = {}, {}
+    for k, lk in zip(ks, lks):
+        ls = []
+        for j in range(J):
+            X = scinputs.gaussian_block(seed + j, g.n, R).astype(np.float64)
+            F = chebyshev.lowpass_filter(L, X, lk, lmax, order, jackson).astype(np.float32)
+            u = np.stack([scinputs.uniforms(seed + j, k, offset=k * r) for r in range(restarts)])
+            ls.append(kmeans.kmeans(F, k, u, max_iter)[0])
+        out[k] = stability.gamma(ls)
+        labs[k] = ls
+    return out, labs
+
+
+def test_stability_matches_oracle(sc):
+    g = scinputs.sbm(1200, 4, 20, 0.03, seed=21)
+    L = laplacian.laplacian(g)
+    lmax = lambda_max.lambda_max_exact(L) * 1.01
+    ev = np.linalg.eigvalsh(L.toarray())
+    ks = [2, 3, 4, 5, 6]
+    lks = [0.5 * (ev[k - 1] + ev[k]) for k in ks]          # mid-gap cuts from the dense oracle
+    J, R, order, seed, restarts, max_iter = 4, 12, 60, 77, 3, 100
+    G = sc.Graph.from_csr(g)
+    lab = np.zeros((len(ks), J, g.n), dtype=np.int32)
+    gam, lk_used = sc.sc_stability(G.handle, ks[0], ks[-1], J, R, order, True, 0, seed, restarts, max_iter,
+                                   lambda_max=lmax, lambda_k=np.array(lks), labels=lab)
+    assert np.array_equal(lk_used, lks)
+    want, wlabs = _oracle_stability(g, ks, lks, lmax, J, R, order, True, seed, restarts, max_iter)
+    for c, k in enumerate(ks):
+        agree = [oari.ari(lab[c, j], wlabs[k][j]) for j in range(J)]
+        assert min(agree) > 0.99, (k, agree)
+        assert gam[c] == pytest.approx(want[k], abs=2e-3)
+    # the planted k = 4 is the global maximum (§4.3 l.361-362)
+    assert ks[int(np.argmax(gam))] == 4 and gam[ks.index(4)] > 0.99
+
+
+def test_stability_estimated_cuts_and_j2(sc):
+    g = scinputs.sbm(1500, 3, 20, 0.02, seed=5)
+    G = sc.Graph.from_csr(g)
+    gam, lk = sc.sc_stability(G.handle, 2, 4, 2, 8, 60, True, 24, 9, 2, 100)
+    assert np.all(np.diff(lk) >= 0) and np.all(lk > 0)
+    lab = np.zeros((3, 2, g.n), dtype=np.int32)
+    gam2, _ = sc.sc_stability(G.handle, 2, 4, 2, 8, 60, True, 24, 9, 2, 100, labels=lab)
+    assert np.array_equal(gam, gam2)                          # deterministic
+    for c in range(3):                                        # J = 2: gamma is one ARI
+        assert gam[c] == pytest.approx(oari.ari(lab[c, 0], lab[c, 1]), abs=1e-12)
+    assert int(np.argmax(gam)) + 2 == 3
+
+
+def test_row_partitioned_steps_emulated_two_ranks(sc):
+    """The multi-GPU data path on one GPU without inter-rank waiting: both ranks' local CSR
+    (renumbered columns, interior-first rows, halo block), per-step halo fill from the
+    owner's send list, interior then boundary fused steps -- vs the oracle on the whole graph."""
+    from paper_1509_08863_b200 import dist as pdist
+    g = scinputs.sbm(2400, 4, 10, 0.05, seed=31)
+    world, R, order = 2, 16, 30
+    parts = [pdist.local_part(g.row_ptr, g.col_idx, g.values, g.n, r, world) for r in range(world)]
+    halos = [p.halo_gid for p in parts]
+    for p in parts:
+        pdist.send_lists_from_halos(p, halos)
+    Gs = [sc.Graph(p.n_local, p.row_ptr, p.col_idx, p.values, n_cols=p.n_local + p.n_halo) for p in parts]
+    fns = [pdist.cuda_step_fn(G.handle) for G in Gs]
+    lmax = 2.0 * float(g.degrees().max())
+    d = chebyshev.filter_coeffs(0.12 * lmax, lmax, order, True)
+    X = scinputs.gaussian_block(41, g.n, R)
+    T0, bufs, Ys, sends = [], [], [], []
+    for p in parts:
+        t = torch.zeros((p.n_local + p.n_halo, R), dtype=torch.float32, device="cuda")
+        t[: p.n_local] = torch.from_numpy(X[p.r0:p.r1]).cuda()[torch.from_numpy(p.perm).cuda()]
+        T0.append(t)
+        bufs.append([torch.zeros_like(t) for _ in range(2)])
+        Ys.append(torch.empty((p.n_local, R), dtype=torch.float32, device="cuda"))
+        off = np.concatenate([[0], np.cumsum(p.send_counts)])
+        sends.append({q: torch.from_numpy(p.send_idx[off[q]:off[q + 1]]).cuda() for q in range(world)})
+    for st in pdist.step_schedule(order, d, lmax):
+        s = st["s"]
+        cur = [T0[r] if s == 0 else bufs[r][s & 1] for r in range(world)]
+        prev = [None if s == 0 else (T0[r] if s == 1 else bufs[r][(s - 1) & 1]) for r in range(world)]
+        nxt = [bufs[r][(s + 1) & 1] if st["store_next"] else None for r in range(world)]
+        for r, p in enumerate(parts):            # halo exchange (emulated: device copies)
+            blocks = [cur[q][sends[q][r]] for q in range(world) if q != r]
+            if p.n_halo:
+                cur[r][p.n_local:] = torch.cat(blocks)
+        for r, p in enumerate(parts):
+            fns[r](0, p.n_interior, prev[r], cur[r], nxt[r], Ys[r], st)
+            fns[r](p.n_interior, p.n_local, prev[r], cur[r], nxt[r], Ys[r], st)
+    torch.cuda.synchronize()
+    Yfull = np.zeros((g.n, R))
+    for r, p in enumerate(parts):
+        y = np.empty((p.n_local, R))
+        y[p.perm] = Ys[r].cpu().numpy()
+        Yfull[p.r0:p.r1] = y
+    Yo = chebyshev.cheb_filter(laplacian.laplacian(g), X.astype(np.float64), d, lmax)
+    assert all(p.n_halo > 0 and 0 < p.n_interior < p.n_local for p in parts)
+    assert rel(Yfull, Yo) <= F32_TOL
