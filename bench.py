@@ -286,6 +286,9 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "cheb_step_kernel (fused SpMM + 3-term recurrence + Y accumulation)",
                          "avg_launch_us": avg_launch_s * 1e6, "algo_bytes_per_launch": bytes_per_launch,
+                         "l2_gather_GBps": float(g.nnz) * R * 4 * order * args.steps / (kern_ms / 1e3) / 1e9,
+                         "l2_gather_note": "nnz(W)*R*4 bytes of gathered T_s rows per step cross L2->SM; "
+                                           "measured random-gather ceiling in profiles/r01_gather_probe.txt",
                          "kernel_share_of_step": (kern_ms / ms) if ms > 0 else None},
             "gpu_launches": int(launches),
             "clocks": clk,

@@ -19,6 +19,7 @@
 // step already holds in registers), so the fused step streams ~3.67 dense
 // blocks instead of 5.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -199,13 +200,14 @@ struct SmemLayout {
   int cap;          // col entries per stage
   int trp;          // row_ptr entries per stage
   int stages;
-  size_t stage_bytes, rp_off, col_off, val_off, dense_off, red_off, total;
+  size_t stage_bytes, rp_off, ord_off, col_off, val_off, dense_off, red_off, total;
   __host__ __device__ SmemLayout(int tr, int cap_, bool unit, int nst) {
     cap = cap_;
     stages = nst;
     trp = (tr + 4 + 1) & ~1;
     rp_off = 0;
-    col_off = (size_t)trp * 8;
+    ord_off = (size_t)trp * 8;
+    col_off = ord_off + (((size_t)tr * 2 + 15) & ~(size_t)15);
     val_off = col_off + (size_t)cap * 4;
     stage_bytes = val_off + (unit ? 0 : (size_t)cap * 4);
     stage_bytes = (stage_bytes + 127) & ~(size_t)127;
@@ -218,8 +220,8 @@ struct SmemLayout {
 template <typename T, int VPR, int EB, bool UNIT, bool MOMENTS>
 __global__ void __launch_bounds__(kThreads, SC_MIN_CTAS)
 cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                 const float* __restrict__ val, const T* __restrict__ strength, StepParams p, int cap,
-                 int nstages) {
+                 const float* __restrict__ val, const T* __restrict__ strength,
+                 const uint16_t* __restrict__ order, StepParams p, int cap, int nstages) {
   constexpr int W = Vec<T>::W;
   constexpr int SW = VPR;          // lanes per row (one 16-byte vector each)
   constexpr int RPW = 32 / SW;     // rows per warp
@@ -280,11 +282,13 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
           TileMeta& m = meta[s];
           m.r0 = r0; m.r1 = r1; m.rpa = rpa; m.ca = ca; m.overflow = overflow;
           unsigned char* st = stages + (size_t)s * lay.stage_bytes;
-          uint32_t tx = (uint32_t)(nrp * 8);
+          uint32_t tx = (uint32_t)(nrp * 8) + (uint32_t)(TR * 2);
           const bool cp_col = !overflow && ncol > 0;
           if (cp_col) tx += (uint32_t)(ncol * 4 * (UNIT ? 1 : 2));
           mbar_arrive_expect_tx(&full[s], tx);
           bulk_g2s(st + lay.rp_off, row_ptr + rpa, (uint32_t)(nrp * 8), &full[s], pol_stream);
+          bulk_g2s(st + lay.ord_off, order + (tg + (int64_t)j * gridDim.x) * TR, (uint32_t)(TR * 2), &full[s],
+                   pol_stream);
           if (cp_col) {
             bulk_g2s(st + lay.col_off, col + ca, (uint32_t)(ncol * 4), &full[s], pol_stream);
             if (!UNIT) bulk_g2s(st + lay.val_off, val + ca, (uint32_t)(ncol * 4), &full[s], pol_stream);
@@ -323,8 +327,13 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
     const unsigned char* st = stages + (size_t)s * lay.stage_bytes;
     const int64_t* rps = reinterpret_cast<const int64_t*>(st + lay.rp_off);
 
-    const int64_t row = m.r0 + warp * RPW + sub;
-    const bool valid = row < m.r1;
+    // rows of the tile in ascending-degree order; this warp takes one block of RPW
+    // consecutive ranks (similar degrees -> little padding to the warp's longest row),
+    // the block index rotating with the tile so every warp sees every degree class
+    const uint16_t* ord = reinterpret_cast<const uint16_t*>(st + lay.ord_off);
+    const int rank = ((warp + static_cast<int>(t % kNC)) % kNC) * RPW + sub;
+    const bool valid = rank < static_cast<int>(m.r1 - m.r0);
+    const int64_t row = m.r0 + (valid ? ord[rank] : 0);
     int deg = 0;
     int64_t b = 0;
     T acc[W];
@@ -449,6 +458,29 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   }
 }
 
+// Degree-sorted row order inside each tile: order[t*tr + rank] = local row index, ranks by
+// (degree, index).  Built once per (graph, tile rows, row range) and cached on the graph.
+__global__ void tile_order_kernel(const int64_t* __restrict__ row_ptr, int64_t row_begin, int64_t row_end, int tr,
+                                  uint16_t* __restrict__ order) {
+  extern __shared__ int degs[];
+  const int64_t t = blockIdx.x;
+  const int64_t r0 = row_begin + t * tr;
+  const int cnt = static_cast<int>(min((int64_t)tr, row_end - r0));
+  for (int i = threadIdx.x; i < tr; i += blockDim.x)
+    degs[i] = i < cnt ? static_cast<int>(row_ptr[r0 + i + 1] - row_ptr[r0 + i]) : INT_MAX;
+  __syncthreads();
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int d = degs[i];
+    int rank = 0;
+    for (int j = 0; j < cnt; ++j) {
+      const int dj = degs[j];
+      rank += (dj < d) || (dj == d && j < i);
+    }
+    order[t * tr + rank] = static_cast<uint16_t>(i);
+  }
+  for (int i = cnt + threadIdx.x; i < tr; i += blockDim.x) order[t * tr + i] = 0;
+}
+
 // sum per-block moment partials of one launch in a fixed order
 __global__ void reduce_partials_kernel(const double* __restrict__ part, int nblocks,
                                        double* __restrict__ out) {
@@ -511,7 +543,8 @@ int env_int(const char* name, int dflt) {
 }
 
 template <typename T>
-using KernelFn = void (*)(const int64_t*, const int32_t*, const float*, const T*, StepParams, int, int);
+using KernelFn = void (*)(const int64_t*, const int32_t*, const float*, const T*, const uint16_t*, StepParams, int,
+                          int);
 
 template <typename T, int VPR, int EB, bool MOM>
 KernelFn<T> pick_unit(bool unit) {
@@ -560,10 +593,28 @@ void stage_plan(int tr, bool unit, int* cap, int* nstages) {
   const int ns = 3;
   const int per_entry = unit ? 4 : 8;
   const int budget = 100 * 1024 - 256 - kNC * 3 * 32 * 16 - kNC * 3 * 8;
-  const int per_stage = budget / ns - (tr + 6) * 8 - 128;
+  const int per_stage = budget / ns - (tr + 6) * 8 - tr * 2 - 144;
   int c = std::min(tr * 48, per_stage / per_entry);
   *cap = std::max(64, c & ~3);
   *nstages = ns;
+}
+
+const uint16_t* tile_order(const sc_graph* g, int tr, int64_t row_begin, int64_t row_end, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(g->tile_orders_mu);
+  auto key = std::make_tuple(tr, row_begin, row_end);
+  auto it = g->tile_orders.find(key);
+  if (it != g->tile_orders.end()) return it->second->as<uint16_t>();
+  const int64_t ntiles = (row_end - row_begin + tr - 1) / tr;
+  auto buf = std::make_unique<DevBuf>();
+  if (buf->ensure(sizeof(uint16_t) * (size_t)std::max<int64_t>(1, ntiles) * tr) != SC_OK) return nullptr;
+  if (ntiles > 0) {
+    tile_order_kernel<<<(unsigned)ntiles, 256, sizeof(int) * tr, s>>>(g->row_ptr.as<int64_t>(), row_begin, row_end, tr,
+                                                                     buf->as<uint16_t>());
+    if (cudaGetLastError() != cudaSuccess) return nullptr;
+  }
+  const uint16_t* out = buf->as<uint16_t>();
+  g->tile_orders[key] = std::move(buf);
+  return out;
 }
 
 template <typename T>
@@ -604,11 +655,14 @@ int launch_step_impl(const sc_graph* g, const StepParams& p, cudaStream_t s, boo
     e1 = g_prof.get();
     cudaEventRecord(e0, s);
   }
+  const uint16_t* order = tile_order(g, tr, p.row_begin, p.row_end, s);
+  if (!order) return fail(SC_ERR_NOMEM, "tile order allocation failed");
   StepParams q = p;
   static const int l2_flags = env_int("SC_L2_FLAGS", 0);
   q.l2_flags = l2_flags;
   k<<<grid, kThreads, smem, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(),
-                                 g->unit_weights ? nullptr : g->values.as<float>(), strength_of<T>(g), q, cap, nst);
+                                 g->unit_weights ? nullptr : g->values.as<float>(), strength_of<T>(g), order, q, cap,
+                                 nst);
   SC_CUDA_TRY(cudaGetLastError());
   if (g_prof.on) {
     cudaEventRecord(e1, s);

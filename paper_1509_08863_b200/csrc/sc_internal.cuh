@@ -4,7 +4,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "sc_b200.h"
@@ -110,6 +114,9 @@ struct sc_graph {
   sc::DevBuf strength32;  // float  [n_rows]
   // workspace (grow-only)
   sc::DevBuf ws_a, ws_b, ws_sig, ws_part, ws_misc;
+  // per (tile rows, row_begin, row_end): degree-sorted row order inside each tile (uint16)
+  mutable std::map<std::tuple<int, int64_t, int64_t>, std::unique_ptr<sc::DevBuf>> tile_orders;
+  mutable std::mutex tile_orders_mu;
   int num_sms = 148;
   int device = 0;
 };
