@@ -7,10 +7,14 @@
 // scheduling (reading R8):
 //   * distances: fp64, explicit differences, summed in ascending q with
 //     __dsub_rn/__dmul_rn/__dadd_rn (no FMA contraction);
-//   * centroid sums: exact fixed-point accumulation of the fp32 features in
-//     three 38-bit limbs of 64-bit integer atomics (order independent), rounded
-//     once to fp64 (= the correctly rounded sum), then divided by the count.
+//   * centroid sums: members grouped by cluster (counting sort), exact 128-bit
+//     fixed-point accumulation of the fp32 features (x * 2^(100-E), E the exponent
+//     bound of max|x|; integer sums are order independent), rounded once to fp64
+//     (= the correctly rounded sum, as math.fsum), then divided by the count.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -77,65 +81,49 @@ __global__ void range_sums_kernel(const double* __restrict__ v, int64_t n, int64
   if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
 }
 
-// sequential scan of one range: first i with start + cumsum > target
+// first i in [b0, b1) with start + cumsum(v[b0..i]) > target.  One warp: lane j sums a
+// contiguous slice (ascending), lane prefixes locate the slice holding the crossing, whose
+// lane rescans it element by element.  If no prefix exceeds target (rounding at the very
+// end of the range), the last positive entry is taken.
 __global__ void range_select_kernel(const double* __restrict__ v, int64_t b0, int64_t b1, double start,
                                     double target, int64_t* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s = start;
+  const int lane = threadIdx.x;
+  const int64_t len = b1 - b0;
+  const int64_t per = (len + 31) / 32;
+  const int64_t s0 = min(b1, b0 + lane * per), s1 = min(b1, s0 + per);
+  double sum = 0.0;
   int64_t last_pos = -1;
-  for (int64_t i = b0; i < b1; ++i) {
-    s += v[i];
+  for (int64_t i = s0; i < s1; ++i) {
+    sum += v[i];
     if (v[i] > 0.0) last_pos = i;
-    if (s > target) { *out = i; return; }
   }
-  *out = last_pos >= 0 ? last_pos : b1 - 1;
+  // exclusive prefix of the slice sums (fixed order: lanes ascending)
+  double pre = 0.0;
+  for (int j = 0; j < 32; ++j) {
+    const double sj = __shfl_sync(0xffffffffu, sum, j);
+    if (j < lane) pre += sj;
+  }
+  const double hi = start + pre + sum;
+  const unsigned cross = __ballot_sync(0xffffffffu, hi > target && s1 > s0);
+  long long lp = last_pos;
+  for (int o = 16; o > 0; o >>= 1) lp = max(lp, __shfl_xor_sync(0xffffffffu, lp, o));
+  if (cross == 0) {
+    if (lane == 0) *out = lp >= 0 ? lp : b1 - 1;
+    return;
+  }
+  const int L = __ffs(cross) - 1;
+  if (lane == L) {
+    double acc = start + pre;
+    for (int64_t i = s0; i < s1; ++i) {
+      acc += v[i];
+      if (acc > target) { *out = i; return; }
+    }
+    *out = s1 - 1;
+  }
 }
 
 __global__ void row_to_centroid_kernel(const float* __restrict__ F, int64_t idx, int d, double* __restrict__ c) {
   for (int q = threadIdx.x; q < d; q += blockDim.x) c[q] = (double)F[idx * d + q];
-}
-
-// assignment over a tile of centroids [c0, c0+kt); best (dist, label) kept in dmin/lab
-__global__ void assign_kernel(const float* __restrict__ F, int64_t n, int d, const double* __restrict__ C,
-                              int c0, int kt, int first_tile, int last_tile, int32_t* __restrict__ lab,
-                              double* __restrict__ dmin, const int32_t* __restrict__ old_lab,
-                              int* __restrict__ changed, double* __restrict__ part_inertia) {
-  extern __shared__ double sC[];
-  for (int e = threadIdx.x; e < kt * d; e += blockDim.x) sC[e] = C[(int64_t)c0 * d + e];
-  __syncthreads();
-  double inertia = 0.0;
-  int nchg = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float* x = F + i * d;
-    double best = first_tile ? INFINITY : dmin[i];
-    int bl = first_tile ? -1 : lab[i];
-    for (int c = 0; c < kt; ++c) {
-      const double v = dist2_row(x, sC + c * d, d);
-      if (v < best) { best = v; bl = c0 + c; }
-    }
-    if (bl < 0) bl = c0;   // all distances NaN/inf: deterministic fallback
-    dmin[i] = best;
-    lab[i] = bl;
-    if (last_tile) {
-      inertia += best;
-      if (old_lab && old_lab[i] != bl) ++nchg;
-    }
-  }
-  if (last_tile) {
-    __shared__ double sh[kB];
-    __shared__ int shc[kB];
-    sh[threadIdx.x] = inertia;
-    shc[threadIdx.x] = nchg;
-    __syncthreads();
-    for (int o = kB / 2; o > 0; o >>= 1) {
-      if ((int)threadIdx.x < o) { sh[threadIdx.x] += sh[threadIdx.x + o]; shc[threadIdx.x] += shc[threadIdx.x + o]; }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      part_inertia[blockIdx.x] = sh[0];
-      if (shc[0]) atomicAdd(changed, shc[0]);
-    }
-  }
 }
 
 // exact fixed-point image of an fp32 value: x * 2^shift as a signed 128-bit integer
@@ -153,47 +141,6 @@ __device__ __forceinline__ __int128 to_fixed(float xf, int shift) {
   else if (s > -40) v = (__int128)((m + (1ull << (-s - 1))) >> (-s));
   else v = 0;
   return (u >> 31) ? -v : v;
-}
-
-constexpr int kLimb = 38;
-constexpr unsigned long long kLimbMask = (1ull << kLimb) - 1ull;
-
-// accumulate member sums for clusters [c0, c0+kt) into limbs[3][k][d] (global), counts[k]
-__global__ void centroid_accum_kernel(const float* __restrict__ F, const int32_t* __restrict__ lab, int64_t n,
-                                      int d, int c0, int kt, int shift, unsigned long long* __restrict__ limbs,
-                                      int k, unsigned long long* __restrict__ counts, int do_counts) {
-  extern __shared__ unsigned long long sl[];   // [3][kt*d] then counts[kt]
-  const int slots = kt * d;
-  for (int e = threadIdx.x; e < 3 * slots + kt; e += blockDim.x) sl[e] = 0ull;
-  __syncthreads();
-  const int64_t total = n * d;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / d;
-    const int q = static_cast<int>(e - i * d);
-    const int c = lab[i] - c0;
-    if (c < 0 || c >= kt) continue;
-    const __int128 v = to_fixed(F[e], shift);
-    const unsigned long long l0 = (unsigned long long)(v & (__int128)kLimbMask);
-    const __int128 v1 = v >> kLimb;
-    const unsigned long long l1 = (unsigned long long)(v1 & (__int128)kLimbMask);
-    const long long l2 = (long long)(v1 >> kLimb);
-    const int slot = c * d + q;
-    if (l0) atomicAdd(&sl[slot], l0);
-    if (l1) atomicAdd(&sl[slots + slot], l1);
-    if (l2) atomicAdd(&sl[2 * slots + slot], (unsigned long long)l2);
-    if (do_counts && q == 0) atomicAdd(&sl[3 * slots + c], 1ull);
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < 3 * slots; e += blockDim.x) {
-    const unsigned long long v = sl[e];
-    if (v) {
-      const int limb = e / slots, slot = e - limb * slots;
-      atomicAdd(&limbs[(size_t)limb * k * d + (size_t)c0 * d + slot], v);
-    }
-  }
-  if (do_counts)
-    for (int c = threadIdx.x; c < kt; c += blockDim.x)
-      if (sl[3 * slots + c]) atomicAdd(&counts[c0 + c], sl[3 * slots + c]);
 }
 
 // correctly rounded double of S * 2^-shift, S a signed 128-bit integer
@@ -218,20 +165,6 @@ __device__ double fixed_to_double(__int128 S, int shift) {
   return neg ? -r : r;
 }
 
-__global__ void centroid_finalize_kernel(const unsigned long long* __restrict__ limbs,
-                                         const unsigned long long* __restrict__ counts, int k, int d,
-                                         int shift, double* __restrict__ C) {
-  const int slots = k * d;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < slots; e += gridDim.x * blockDim.x) {
-    const int c = e / d;
-    const unsigned long long cnt = counts[c];
-    if (cnt == 0) continue;   // empty cluster keeps its centre
-    const __int128 S = (__int128)limbs[e] + ((__int128)limbs[slots + e] << kLimb) +
-                       ((__int128)(long long)limbs[2 * slots + e] << (2 * kLimb));
-    C[e] = fixed_to_double(S, shift) / (double)cnt;
-  }
-}
-
 __global__ void contingency_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t n,
                                    int ka, int kb, unsigned long long* __restrict__ t) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -249,6 +182,201 @@ __global__ void minmax_kernel(const int32_t* __restrict__ a, int64_t n, int* out
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
   if ((threadIdx.x & 31) == 0) { atomicMin(out, mn); atomicMax(out + 1, mx); }
+}
+
+
+// ---------------------------------------------------------------------------
+// Lloyd assignment, register-tiled like a GEMM: a block of 256 threads computes the
+// distances of 64 points to centroid tiles of 64; thread (ty, tx) owns 4 points x 4
+// centroids (16 fp64 accumulators).  Points and centroids are staged as fp64 [d][64]
+// in shared memory.  Distance = sum_q (x_q - c_q)^2 in ascending q with
+// __dsub_rn/__dmul_rn/__dadd_rn (R8); each thread keeps the first minimum over
+// its centroids, the 16 threads of a point row reduce (dist, index) lexicographically,
+// so the result is the lowest index among equal minima, as np.argmin.
+// ---------------------------------------------------------------------------
+constexpr int kAT = 64;   // points per block and centroids per tile
+
+__global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ F, int64_t n, int d,
+                                                      const double* __restrict__ C, int k,
+                                                      int32_t* __restrict__ lab, const int32_t* __restrict__ old_lab,
+                                                      int* __restrict__ changed, double* __restrict__ part_inertia,
+                                                      unsigned* __restrict__ counts) {
+  extern __shared__ double sm3[];
+  double* sX = sm3;                        // [d][kAT]
+  double* sC = sm3 + (size_t)d * kAT;      // [d][kAT]
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int64_t p0 = (int64_t)blockIdx.x * kAT;
+  for (int e = tid; e < kAT * d; e += 256) {
+    const int row = e / d, q = e - row * d;
+    const int64_t gi = p0 + row;
+    sX[(size_t)q * kAT + row] = gi < n ? (double)F[gi * d + q] : 0.0;
+  }
+  double best[4];
+  int bidx[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { best[i] = INFINITY; bidx[i] = -1; }
+  for (int c0 = 0; c0 < k; c0 += kAT) {
+    const int kt = min(kAT, k - c0);
+    __syncthreads();
+    for (int e = tid; e < kAT * d; e += 256) {
+      const int cc = e / d, q = e - cc * d;
+      sC[(size_t)q * kAT + cc] = cc < kt ? C[(size_t)(c0 + cc) * d + q] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+#pragma unroll 2
+    for (int q = 0; q < d; ++q) {
+      const double2 xa = *reinterpret_cast<const double2*>(sX + (size_t)q * kAT + ty * 4);
+      const double2 xb = *reinterpret_cast<const double2*>(sX + (size_t)q * kAT + ty * 4 + 2);
+      const double2 ca = *reinterpret_cast<const double2*>(sC + (size_t)q * kAT + tx * 4);
+      const double2 cb = *reinterpret_cast<const double2*>(sC + (size_t)q * kAT + tx * 4 + 2);
+      const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+      const double cv[4] = {ca.x, ca.y, cb.x, cb.y};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double diff = __dsub_rn(xv[i], cv[j]);
+          acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(diff, diff));
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cidx = tx * 4 + j;
+      if (cidx < kt) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (acc[i][j] < best[i]) { best[i] = acc[i][j]; bidx[i] = c0 + cidx; }
+      }
+    }
+  }
+  // (dist, index) lexicographic min over the 16 threads of each point row
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best[i], o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx[i], o);
+      const bool take = (oi >= 0) && (bidx[i] < 0 || ob < best[i] || (ob == best[i] && oi < bidx[i]));
+      if (take) { best[i] = ob; bidx[i] = oi; }
+    }
+  }
+  double inertia = 0.0;
+  int nchg = 0;
+  // thread tx < 4 of row ty handles point ty*4 + tx
+  const int i = tx & 3;
+  double bv = best[0];
+  int bl = bidx[0];
+#pragma unroll
+  for (int ii = 1; ii < 4; ++ii) if (ii == i) { bv = best[ii]; bl = bidx[ii]; }
+  const int64_t gi = p0 + ty * 4 + i;
+  const bool mine = tx < 4 && gi < n;
+  if (mine) {
+    if (bl < 0) bl = 0;   // all distances NaN/inf: deterministic fallback
+    lab[gi] = bl;
+    inertia = bv;
+    if (old_lab && old_lab[gi] != bl) nchg = 1;
+  }
+  const unsigned peers = __match_any_sync(0xffffffffu, mine ? bl : -1);
+  if (mine && (tid & 31) == __ffs(peers) - 1) atomicAdd(&counts[bl], (unsigned)__popc(peers));
+  __shared__ double sh[256];
+  __shared__ int shc[256];
+  sh[tid] = inertia;
+  shc[tid] = nchg;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) { sh[tid] += sh[tid + o]; shc[tid] += shc[tid + o]; }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    part_inertia[blockIdx.x] = sh[0];
+    if (shc[0]) atomicAdd(changed, shc[0]);
+  }
+}
+
+// members of cluster c land at perm[off[c] .. off[c+1]) (order inside a cluster is
+// arbitrary; the exact integer sums below do not depend on it).  A block takes a range of
+// points, ranks them per cluster in shared memory and reserves one slice per (block,
+// cluster) with a single global atomic.
+__global__ void scatter_members_kernel(const int32_t* __restrict__ lab, int64_t n, int k, int64_t per_block,
+                                       unsigned* __restrict__ cursor, const int64_t* __restrict__ off,
+                                       int32_t* __restrict__ perm) {
+  extern __shared__ unsigned hist[];   // [k] local counts, then [k] bases
+  unsigned* base = hist + k;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  const int64_t a = blockIdx.x * per_block, b = min(n, a + per_block);
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) atomicAdd(&hist[lab[i]], 1u);
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    base[c] = hist[c] ? atomicAdd(&cursor[c], hist[c]) : 0u;
+    hist[c] = 0;
+  }
+  __syncthreads();
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+    const int c = lab[i];
+    perm[off[c] + base[c] + atomicAdd(&hist[c], 1u)] = static_cast<int32_t>(i);
+  }
+}
+
+__global__ void scatter_members_simple_kernel(const int32_t* __restrict__ lab, int64_t n,
+                                              unsigned* __restrict__ cursor, const int64_t* __restrict__ off,
+                                              int32_t* __restrict__ perm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = lab[i];
+    perm[off[c] + atomicAdd(&cursor[c], 1u)] = static_cast<int32_t>(i);
+  }
+}
+
+// exact member sums: work item w covers members [ws[w], we[w]) of cluster wc[w]; thread
+// (slot j, dim q) accumulates x * 2^shift exactly in a 128-bit integer, the block reduces
+// the slots of each dim and writes one 128-bit partial per (item, dim)
+__global__ void member_sum_kernel(const float* __restrict__ F, int d, const int32_t* __restrict__ perm,
+                                  const int64_t* __restrict__ ws, const int64_t* __restrict__ we, int shift,
+                                  unsigned long long* __restrict__ part /* [items][d][2] */) {
+  extern __shared__ unsigned long long red2[];   // [slots][d][2]
+  const int w = blockIdx.x;
+  const int slots = blockDim.x / d;
+  const int j = threadIdx.x / d, q = threadIdx.x - j * d;
+  __int128 acc = 0;
+  if (j < slots)
+    for (int64_t m = ws[w] + j; m < we[w]; m += slots) acc += to_fixed(F[(int64_t)perm[m] * d + q], shift);
+  if (j < slots) {
+    red2[((size_t)j * d + q) * 2] = (unsigned long long)acc;
+    red2[((size_t)j * d + q) * 2 + 1] = (unsigned long long)(acc >> 64);
+  }
+  __syncthreads();
+  if (threadIdx.x < d) {
+    __int128 sum = 0;
+    for (int jj = 0; jj < slots; ++jj) {
+      const unsigned long long lo = red2[((size_t)jj * d + threadIdx.x) * 2];
+      const unsigned long long hi = red2[((size_t)jj * d + threadIdx.x) * 2 + 1];
+      sum += (__int128)(((unsigned __int128)hi << 64) | lo);
+    }
+    part[((size_t)w * d + threadIdx.x) * 2] = (unsigned long long)sum;
+    part[((size_t)w * d + threadIdx.x) * 2 + 1] = (unsigned long long)(sum >> 64);
+  }
+}
+
+// C[c][q] = correctly rounded (sum of the cluster's partials) / count; empty clusters keep C
+__global__ void member_finalize_kernel(const unsigned long long* __restrict__ part, const int32_t* __restrict__ item0,
+                                       const int32_t* __restrict__ nitems, const unsigned* __restrict__ counts, int k,
+                                       int d, int shift, double* __restrict__ C) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * d; e += gridDim.x * blockDim.x) {
+    const int c = e / d, q = e - c * d;
+    if (counts[c] == 0) continue;
+    __int128 sum = 0;
+    for (int it = 0; it < nitems[c]; ++it) {
+      const size_t o = ((size_t)(item0[c] + it) * d + q) * 2;
+      sum += (__int128)(((unsigned __int128)part[o + 1] << 64) | part[o]);
+    }
+    C[e] = fixed_to_double(sum, shift) / (double)counts[c];
+  }
 }
 
 int num_sms_current() {
@@ -276,15 +404,24 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   const int G = sms * 2;                                  // k-means++ range blocks
   const int64_t chunk = (n + G - 1) / G;
   // workspace
-  DevBuf b_lab, b_new, b_dmin, b_d2, b_C, b_limbs, b_cnt, b_part, b_misc;
+  // assignment: 64 points x 64-centroid tiles per block, fp64 [d][64] tiles of both
+  const int smem_assign = (int)(sizeof(double) * 2 * (size_t)d * kAT);
+  if (smem_assign > 200 * 1024) return fail(SC_ERR_ARG, "sc_kmeans: d must be <= 200");
+  const int64_t nblk = (n + kAT - 1) / kAT;
+  constexpr int64_t kChunk = 512;    // members per exact-sum work item
+  const int64_t max_items = n / kChunk + k + 1;
+  DevBuf b_lab, b_new, b_d2, b_C, b_cnt, b_cur, b_off, b_perm, b_items, b_part, b_psum, b_misc;
   SC_TRY(b_lab.ensure(sizeof(int32_t) * n));
   SC_TRY(b_new.ensure(sizeof(int32_t) * n));
-  SC_TRY(b_dmin.ensure(sizeof(double) * n));
   SC_TRY(b_d2.ensure(sizeof(double) * n));
   SC_TRY(b_C.ensure(sizeof(double) * k * d));
-  SC_TRY(b_limbs.ensure(sizeof(unsigned long long) * 3 * k * d));
-  SC_TRY(b_cnt.ensure(sizeof(unsigned long long) * k));
-  SC_TRY(b_part.ensure(sizeof(double) * std::max(grid, G)));
+  SC_TRY(b_cnt.ensure(sizeof(unsigned) * k));
+  SC_TRY(b_cur.ensure(sizeof(unsigned) * k));
+  SC_TRY(b_off.ensure(sizeof(int64_t) * (k + 1)));
+  SC_TRY(b_perm.ensure(sizeof(int32_t) * n));
+  SC_TRY(b_items.ensure(sizeof(int64_t) * 2 * max_items + sizeof(int32_t) * 2 * k));
+  SC_TRY(b_psum.ensure(sizeof(unsigned long long) * 2 * (size_t)max_items * d));
+  SC_TRY(b_part.ensure(sizeof(double) * std::max<int64_t>(std::max<int64_t>(grid, G), nblk)));
   SC_TRY(b_misc.ensure(64));
   int32_t* lab = b_lab.as<int32_t>();
   int32_t* nw = b_new.as<int32_t>();
@@ -305,33 +442,24 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   if (!std::isfinite(amax)) return fail(SC_ERR_ARG, "features contain inf/nan");
   int E = 0;
   if (amax > 0.0f) { std::frexp((double)amax, &E); }   // amax < 2^E
-  const int shift = 87 - E;
+  const int shift = 100 - E;   // |x| 2^shift < 2^100; sums of < 2^25 members fit 2^125
 
-  // centroid tiles for smem (assign: kt*d doubles; accum: 3*kt*d + kt u64)
-  const size_t smem_cap = 96 * 1024;
-  int kt_assign = std::max(1, std::min(k, (int)(smem_cap / (sizeof(double) * d))));
-  int kt_acc = std::max(1, std::min(k, (int)((smem_cap / sizeof(unsigned long long)) / (3 * (size_t)d + 1))));
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap);
-    cudaFuncSetAttribute(centroid_accum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap);
-    attr_set = true;
-  }
+  SC_CUDA_TRY(cudaFuncSetAttribute(assign3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
+  std::vector<unsigned> cnt_h(k);
 
+  // Lloyd assignment of every point; host receives inertia (fixed-order sum of block
+  // partials), the number of changed labels and the label histogram
   auto assign_all = [&](int32_t* out_lab, const int32_t* old, double* inertia, int* nchanged) -> int {
     SC_CUDA_TRY(cudaMemsetAsync(changed, 0, sizeof(int), s));
-    for (int c0 = 0; c0 < k; c0 += kt_assign) {
-      const int kt = std::min(kt_assign, k - c0);
-      const int last = c0 + kt >= k;
-      assign_kernel<<<grid, kB, sizeof(double) * kt * d, s>>>(F, n, d, C, c0, kt, c0 == 0, last, out_lab,
-                                                               b_dmin.as<double>(), old, changed,
-                                                               b_part.as<double>());
-      SC_CUDA_TRY(cudaGetLastError());
-    }
-    std::vector<double> part(grid);
+    SC_CUDA_TRY(cudaMemsetAsync(b_cnt.ptr, 0, sizeof(unsigned) * k, s));
+    assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, out_lab, old, changed,
+                                                           b_part.as<double>(), b_cnt.as<unsigned>());
+    SC_CUDA_TRY(cudaGetLastError());
+    std::vector<double> part(nblk);
     int h_changed = 0;
-    SC_CUDA_TRY(cudaMemcpyAsync(part.data(), b_part.as<double>(), sizeof(double) * grid, cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaMemcpyAsync(part.data(), b_part.as<double>(), sizeof(double) * nblk, cudaMemcpyDeviceToHost, s));
     SC_CUDA_TRY(cudaMemcpyAsync(&h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaMemcpyAsync(cnt_h.data(), b_cnt.ptr, sizeof(unsigned) * k, cudaMemcpyDeviceToHost, s));
     SC_CUDA_TRY(cudaStreamSynchronize(s));
     double tot = 0.0;
     for (double v : part) tot += v;
@@ -340,19 +468,55 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
     return SC_OK;
   };
 
+  // centroids <- member means of the labels `cur` (histogram in cnt_h): members grouped by
+  // cluster (counting sort), exact 128-bit fixed-point member sums, one rounding
+  std::vector<int64_t> off_h(k + 1), ws_h, we_h;
+  std::vector<int32_t> item0_h(k), nitems_h(k);
   auto update = [&](const int32_t* cur) -> int {
-    SC_CUDA_TRY(cudaMemsetAsync(b_limbs.ptr, 0, sizeof(unsigned long long) * 3 * k * d, s));
-    SC_CUDA_TRY(cudaMemsetAsync(b_cnt.ptr, 0, sizeof(unsigned long long) * k, s));
-    for (int c0 = 0; c0 < k; c0 += kt_acc) {
-      const int kt = std::min(kt_acc, k - c0);
-      const size_t sm = sizeof(unsigned long long) * (3 * (size_t)kt * d + kt);
-      centroid_accum_kernel<<<grid, kB, sm, s>>>(F, cur, n, d, c0, kt, shift, b_limbs.as<unsigned long long>(), k,
-                                                 b_cnt.as<unsigned long long>(), 1);
+    off_h[0] = 0;
+    for (int c = 0; c < k; ++c) off_h[c + 1] = off_h[c] + cnt_h[c];
+    ws_h.clear();
+    we_h.clear();
+    for (int c = 0; c < k; ++c) {
+      item0_h[c] = (int32_t)ws_h.size();
+      for (int64_t a = off_h[c]; a < off_h[c + 1]; a += kChunk) {
+        ws_h.push_back(a);
+        we_h.push_back(std::min(off_h[c + 1], a + kChunk));
+      }
+      nitems_h[c] = (int32_t)ws_h.size() - item0_h[c];
+    }
+    const int64_t items = (int64_t)ws_h.size();
+    int64_t* d_ws = b_items.as<int64_t>();
+    int64_t* d_we = d_ws + max_items;
+    int32_t* d_item0 = reinterpret_cast<int32_t*>(d_we + max_items);
+    int32_t* d_nitems = d_item0 + k;
+    SC_CUDA_TRY(cudaMemcpyAsync(b_off.ptr, off_h.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice, s));
+    if (items) {
+      SC_CUDA_TRY(cudaMemcpyAsync(d_ws, ws_h.data(), sizeof(int64_t) * items, cudaMemcpyHostToDevice, s));
+      SC_CUDA_TRY(cudaMemcpyAsync(d_we, we_h.data(), sizeof(int64_t) * items, cudaMemcpyHostToDevice, s));
+    }
+    SC_CUDA_TRY(cudaMemcpyAsync(d_item0, item0_h.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
+    SC_CUDA_TRY(cudaMemcpyAsync(d_nitems, nitems_h.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
+    SC_CUDA_TRY(cudaMemsetAsync(b_cur.ptr, 0, sizeof(unsigned) * k, s));
+    if (k <= 6144) {
+      const int64_t per_block = std::max<int64_t>(4096, (n + grid - 1) / grid);
+      scatter_members_kernel<<<(unsigned)((n + per_block - 1) / per_block), kB, sizeof(unsigned) * 2 * k, s>>>(
+          cur, n, k, per_block, b_cur.as<unsigned>(), b_off.as<int64_t>(), b_perm.as<int32_t>());
+    } else {
+      scatter_members_simple_kernel<<<grid, kB, 0, s>>>(cur, n, b_cur.as<unsigned>(), b_off.as<int64_t>(),
+                                                        b_perm.as<int32_t>());
+    }
+    SC_CUDA_TRY(cudaGetLastError());
+    if (items) {
+      const int slots = std::max(1, 256 / d);
+      member_sum_kernel<<<(unsigned)items, slots * d, sizeof(unsigned long long) * 2 * slots * d, s>>>(
+          F, d, b_perm.as<int32_t>(), d_ws, d_we, shift, b_psum.as<unsigned long long>());
       SC_CUDA_TRY(cudaGetLastError());
     }
-    centroid_finalize_kernel<<<std::max(1, std::min(grid, (k * d + kB - 1) / kB)), kB, 0, s>>>(
-        b_limbs.as<unsigned long long>(), b_cnt.as<unsigned long long>(), k, d, shift, C);
+    member_finalize_kernel<<<std::max(1, std::min(grid, (k * d + kB - 1) / kB)), kB, 0, s>>>(
+        b_psum.as<unsigned long long>(), d_item0, d_nitems, b_cnt.as<unsigned>(), k, d, shift, C);
     SC_CUDA_TRY(cudaGetLastError());
+    // the histogram buffer is reused by the next assignment only after this finalize (stream order)
     return SC_OK;
   };
 
@@ -361,7 +525,11 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   std::vector<double> best_C((size_t)k * d);
   std::vector<double> u(k);
   std::vector<double> bsum(G), prefix(G + 1);
+  const bool trace = std::getenv("SC_KMEANS_TRACE") != nullptr;
+  auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double t_seed = 0.0, t_lloyd = 0.0, t_mark = now();
   for (int r = 0; r < restarts; ++r) {
+    if (trace) t_mark = now();
     for (int t = 0; t < k; ++t)
       u[t] = uniforms_host ? uniforms_host[(size_t)r * k + t] : uniform_host(seed, 1, (uint64_t)r * k + t);
     // ---- k-means++ seeding
@@ -392,6 +560,7 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
       SC_CUDA_TRY(cudaGetLastError());
     }
     // ---- Lloyd
+    if (trace) { SC_CUDA_TRY(cudaStreamSynchronize(s)); t_seed += now() - t_mark; t_mark = now(); }
     double inertia = 0.0;
     int nchg = 0;
     SC_TRY(assign_all(lab, nullptr, &inertia, &nchg));
@@ -403,6 +572,10 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
       std::swap(lab, nw);
     }
     if (it > max_iter) it = max_iter;
+    if (trace) {
+      t_lloyd += now() - t_mark;
+      std::fprintf(stderr, "[sc_kmeans] restart %d: seeding %.4f s, lloyd %.4f s (%d iters)\n", r, t_seed, t_lloyd, it);
+    }
     if (inertia < best_inertia) {
       best_inertia = inertia;
       best_r = r;
