@@ -686,10 +686,14 @@ std::vector<int> chunk_plan(int R, int64_t n_cols) {
   const int maxw = 32 * W;   // one warp per row
   int cw = env_int("SC_CHUNK", 0);
   if (cw <= 0) {
-    // keep the gathered block T_s (plus the block being written) resident in L2
+    // Keep the gathered chunk of T_s L2-resident: the widest power of two whose N x w block
+    // fits the budget.  If that would take rows narrower than 128 bytes, the block cannot be
+    // L2-resident at a useful row size anyway: use the widest chunk (fewest CSR re-reads,
+    // largest DRAM requests; profiles/r01_gather_probe.txt).
     const double budget = env_int("SC_L2_BUDGET_MB", 128) * 1048576.0;
     cw = maxw;
-    while (cw > 4 * W && (double)n_cols * cw * sizeof(T) > budget) cw >>= 1;
+    while (cw > W && (double)n_cols * cw * sizeof(T) > budget) cw >>= 1;
+    if (cw * (int)sizeof(T) < 128) cw = maxw;
   }
   cw = std::max(W, std::min(cw, maxw));
   std::vector<int> out;
@@ -764,7 +768,8 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
     int p2 = W;
     while (p2 < Rp) p2 <<= 1;
     const std::vector<int> one = chunk_plan<T>(p2, g->n_cols);
-    if (p2 != Rp && one.size() == 1 && chunk_plan<T>(Rp, g->n_cols).size() > 1) Rp = p2;
+    const bool resident = (double)g->n_cols * p2 * sizeof(T) <= env_int("SC_L2_BUDGET_MB", 128) * 1048576.0;
+    if (p2 != Rp && resident && one.size() == 1 && chunk_plan<T>(Rp, g->n_cols).size() > 1) Rp = p2;
   }
   const bool aligned = (Rp == R) && ((uintptr_t)X % 16 == 0) && ((uintptr_t)Y % 16 == 0);
   const T* Xw = X;
