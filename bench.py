@@ -230,11 +230,13 @@ def run_ours(args):
         from paper_1509_08863_b200 import dist as pdist
         Xl = torch.empty((part.n_local, R), dtype=torch.float32, device=dev)
         sc.sc_random_signals_f32(part.n_local, R, part.r0, args.seed, 0, 0.0, Xl)
-        fn = pdist.cuda_step_fn(handle)
+        Xp = Xl[torch.as_tensor(part.perm, device=dev)].contiguous()   # the rank's local row order
+        Yp = torch.empty_like(Xp)
+        nf = pdist.NcclFilter(part, handle)
 
         def step():
             dd = sc.sc_cheby_coeffs(lam_k, lmax, order, w.jackson)
-            pdist.run_filter(part, fn, dd, order, lmax, Xl)
+            nf.filter(dd, order, lmax, Xp, Yp)
 
     def barrier():
         if world > 1:

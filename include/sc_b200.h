@@ -274,6 +274,44 @@ int sc_stability(sc_graph* g, int k_min, int k_max, int J, int R, int order, int
                  double* gamma, double* lambda_k_out, int32_t* labels, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Row-partitioned multi-GPU filter (north_star: halo exchange over NVLink   */
+/* with NCCL, overlapped with the interior SpMM)                             */
+/* ------------------------------------------------------------------------ */
+
+typedef struct sc_comm sc_comm;   /* NCCL communicator + communication stream */
+typedef struct sc_dist sc_dist;   /* one rank's partition plan                */
+
+/* 128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it). */
+int sc_nccl_unique_id(void* id);
+
+/* Communicator of `world` ranks on the current device.  Errors: SC_ERR_CUDA from NCCL. */
+int sc_comm_init(const void* id, int world, int rank, sc_comm** out);
+int sc_comm_free(sc_comm* c);
+
+/*
+ * sc_dist_create -- partition plan of this rank.  g is the rank's local CSR loaded with
+ * sc_graph_load(n_local, n_local + n_halo, ...): rows in local order with the
+ * n_interior rows that have no remote neighbour first; columns [0, n_local) local rows,
+ * [n_local, n_local + n_halo) halo rows grouped by owner rank (ascending).
+ * send_idx (host/device int64, n_send): local row positions to send, grouped by peer;
+ * send_counts / recv_counts (host int64, world): rows sent to / received from each rank
+ * (sum(recv_counts) must equal n_halo).  dist.py builds all of these.
+ */
+int sc_dist_create(sc_graph* g, sc_comm* c, int64_t n_interior, const int64_t* send_idx, int64_t n_send,
+                   const int64_t* send_counts, const int64_t* recv_counts, sc_dist** out);
+int sc_dist_free(sc_dist* d);
+
+/*
+ * sc_dist_filter_f32 -- this rank's rows of Y = sum_j coeffs[j] T_j(L~) X (as
+ * sc_filter_apply_f32), X and Y the n_local x R blocks in the plan's local row order.
+ * Each recurrence step: pack the send rows, exchange halos with NCCL send/recv on the
+ * communicator's stream, run the interior rows' fused step concurrently, then the
+ * boundary rows.  All ranks must call it with the same coeffs/order/lambda_max/R.
+ */
+int sc_dist_filter_f32(sc_dist* d, const double* coeffs, int order, double lambda_max, int R, const float* X,
+                       float* Y, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Instrumentation (bench.py)                                               */
 /* ------------------------------------------------------------------------ */
 

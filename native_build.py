@@ -22,8 +22,22 @@ BUILD = os.path.join(ROOT, "build", "native")
 LIB = os.path.join(PKG, "libsc_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dirs():
+    """NCCL headers/library: the copy bundled with torch (the one torch.distributed loads,
+    so both share one libnccl.so.2 in the process), else the system one."""
+    import sysconfig
+    base = os.path.join(sysconfig.get_paths()["purelib"], "nvidia", "nccl")
+    inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+    if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+        return inc, lib
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+NCCL_INC, NCCL_LIB = _nccl_dirs()
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
-          "-I", CSRC]
+          "-I", CSRC, "-I", NCCL_INC]
 
 
 def _compile(src: str, verbose_ptxas: bool, defs=(), tag="") -> str:
@@ -54,7 +68,9 @@ def build(verbose_ptxas: bool = False, defs=(), out: str = LIB) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose_ptxas, defs, tag), srcs))
     if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(o) for o in objs):
         return out
-    cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    nccl = os.path.join(NCCL_LIB, "libnccl.so.2")
+    cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-Xlinker", nccl, "-Xlinker", f"-rpath={NCCL_LIB}",
+           "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

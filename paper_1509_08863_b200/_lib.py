@@ -73,6 +73,12 @@ _F = {
                        c_vp),
     "sc_stability": _sig("sc_stability", c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_u64, c_i32, c_i32,
                          c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp),
+    "sc_nccl_unique_id": _sig("sc_nccl_unique_id", c_vp),
+    "sc_comm_init": _sig("sc_comm_init", c_vp, c_i32, c_i32, P(c_vp)),
+    "sc_comm_free": _sig("sc_comm_free", c_vp),
+    "sc_dist_create": _sig("sc_dist_create", c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, P(c_vp)),
+    "sc_dist_free": _sig("sc_dist_free", c_vp),
+    "sc_dist_filter_f32": _sig("sc_dist_filter_f32", c_vp, c_vp, c_i32, c_dbl, c_i32, c_vp, c_vp, c_vp),
     "sc_profile_begin": _sig("sc_profile_begin"),
     "sc_profile_end": _sig("sc_profile_end", P(c_i64), P(c_i64), P(c_dbl), P(c_dbl)),
 }
@@ -262,6 +268,42 @@ def sc_stability(g, k_min, k_max, J, R, order, jackson, n_probe, seed, restarts,
                               lambda_max, _ptr(lk), gamma.ctypes.data, lk_out.ctypes.data, _ptr(labels),
                               _stream(stream)))
     return gamma, lk_out
+
+
+def sc_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_F["sc_nccl_unique_id"](ctypes.addressof(buf)))
+    return buf.raw
+
+
+def sc_comm_init(uid: bytes, world, rank):
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    h = c_vp()
+    _check(_F["sc_comm_init"](ctypes.addressof(buf), world, rank, ctypes.byref(h)))
+    return h.value
+
+
+def sc_comm_free(c):
+    _check(_F["sc_comm_free"](c))
+
+
+def sc_dist_create(g, comm, n_interior, send_idx, send_counts, recv_counts):
+    si = np.ascontiguousarray(send_idx, dtype=np.int64)
+    sc_ = np.ascontiguousarray(send_counts, dtype=np.int64)
+    rc = np.ascontiguousarray(recv_counts, dtype=np.int64)
+    h = c_vp()
+    _check(_F["sc_dist_create"](g, comm, n_interior, si.ctypes.data if si.size else None, si.size, sc_.ctypes.data,
+                                rc.ctypes.data, ctypes.byref(h)))
+    return h.value
+
+
+def sc_dist_free(d):
+    _check(_F["sc_dist_free"](d))
+
+
+def sc_dist_filter_f32(d, coeffs, order, lambda_max, R, X, Y, stream=None):
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    _check(_F["sc_dist_filter_f32"](d, coeffs.ctypes.data, order, lambda_max, R, _ptr(X), _ptr(Y), _stream(stream)))
 
 
 def sc_profile_begin():

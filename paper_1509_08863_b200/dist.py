@@ -232,3 +232,34 @@ def filter_local_steps(handle, d, order, lambda_max, X, row_split=None):
         for a, b in zip(split[:-1], split[1:]):
             fn(a, b, T_prev, T_cur, T_next, Y, st)
     return Y
+
+
+class NcclFilter:
+    """The whole row-partitioned filter inside the library (``sc_dist_filter_f32``): per
+    step the halo of T_s is exchanged with NCCL send/recv on the communicator's stream
+    while the interior rows' fused step runs; the boundary rows follow.  Same schedule as
+    ``run_filter`` without any per-step Python.  X and Y are in the plan's local
+    (interior-first) row order: ``X_local[torch.as_tensor(part.perm)]``."""
+
+    def __init__(self, part: LocalPart, graph_handle, group=None):
+        from . import _lib
+        self._lib = _lib
+        uid = [_lib.sc_nccl_unique_id() if part.rank == 0 else None]
+        if part.world > 1:
+            import torch.distributed as dist
+            dist.broadcast_object_list(uid, src=0, group=group)
+        self.comm = _lib.sc_comm_init(uid[0], part.world, part.rank)
+        self.plan = _lib.sc_dist_create(graph_handle, self.comm, part.n_interior, part.send_idx,
+                                        np.asarray(part.send_counts, dtype=np.int64),
+                                        np.asarray(part.recv_counts, dtype=np.int64))
+
+    def filter(self, d, order: int, lambda_max: float, X, Y):
+        self._lib.sc_dist_filter_f32(self.plan, d, order, lambda_max, X.shape[1], X, Y)
+
+    def close(self):
+        if getattr(self, "plan", None):
+            self._lib.sc_dist_free(self.plan)
+            self.plan = None
+        if getattr(self, "comm", None):
+            self._lib.sc_comm_free(self.comm)
+            self.comm = None

@@ -454,3 +454,28 @@ def test_row_partitioned_steps_emulated_two_ranks(sc):
     Yo = chebyshev.cheb_filter(laplacian.laplacian(g), X.astype(np.float64), d, lmax)
     assert all(p.n_halo > 0 and 0 < p.n_interior < p.n_local for p in parts)
     assert rel(Yfull, Yo) <= F32_TOL
+
+
+def test_nccl_dist_filter_single_rank(sc):
+    """sc_dist_filter_f32 end to end on one rank (NCCL communicator of size 1, no halo):
+    the library-side multi-GPU schedule against the oracle, incl. a ragged R."""
+    from paper_1509_08863_b200 import dist as pdist
+    g = scinputs.sbm(3000, 3, 12, 0.05, seed=33)
+    part = pdist.local_part(g.row_ptr, g.col_idx, g.values, g.n, 0, 1)
+    pdist.send_lists_from_halos(part, [part.halo_gid])
+    G = sc.Graph(part.n_local, part.row_ptr, part.col_idx, part.values, n_cols=part.n_local + part.n_halo)
+    nf = pdist.NcclFilter(part, G.handle)
+    lmax = 2.0 * float(g.degrees().max())
+    L = laplacian.laplacian(g)
+    for R, order in [(32, 25), (13, 7)]:
+        d = chebyshev.filter_coeffs(0.1 * lmax, lmax, order, True)
+        X = scinputs.gaussian_block(5, g.n, R)
+        Xp = torch.from_numpy(X[part.perm]).cuda()
+        Yp = torch.empty_like(Xp)
+        nf.filter(d, order, lmax, Xp, Yp)
+        torch.cuda.synchronize()
+        Y = np.empty((g.n, R))
+        Y[part.perm] = Yp.cpu().numpy()
+        Yo = chebyshev.cheb_filter(L, X.astype(np.float64), d, lmax)
+        assert rel(Y, Yo) <= F32_TOL
+    nf.close()
