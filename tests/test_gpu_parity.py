@@ -235,6 +235,71 @@ def test_full_size_c3_sampled_columns(sc):
     assert rel(Y[:, cols], Yo) <= F32_TOL
 
 
+@pytest.mark.slow
+def test_full_size_c1_all_columns(sc):
+    """configs[1] (weighted Gaussian-mixture kNN, N=20k, R=24, p=100) at full size, every column."""
+    from scinputs import configs
+    w = configs.WORKLOADS["c1_gmm20k"]
+    g = configs.build_graph("c1_gmm20k")
+    G = sc.Graph.from_csr(g)
+    L = laplacian.laplacian(g)
+    lmax = lambda_max.lambda_max_bound(L, scinputs.gaussian_block(1, g.n, 1, dtype=np.float64)[:, 0], 300, 0.01)
+    lc = 0.02 * lmax
+    X = scinputs.gaussian_block(78, g.n, w.R)
+    Y = gpu_filter(sc, g, X, lc, lmax, w.order, w.jackson, G=G)
+    Yo = chebyshev.lowpass_filter(L, X.astype(np.float64), lc, lmax, w.order, w.jackson)
+    assert rel(Y, Yo) <= F32_TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, F32_TOL), (torch.float64, F64_TOL)])
+def test_full_size_c2_sampled_columns(sc, dtype, tol):
+    """configs[2] (SBM N=100k, R=48, p=150) at full size in fp32 and fp64; three sampled columns."""
+    from scinputs import configs
+    w = configs.WORKLOADS["c2_sbm100k"]
+    g = configs.build_graph("c2_sbm100k")
+    G = sc.Graph.from_csr(g)
+    lmax = sc.sc_lambda_max(G.handle, 60, 0.01, 3)
+    lc = 0.05 * lmax
+    X = scinputs.gaussian_block(79, g.n, w.R, dtype=np.float64)
+    Y = gpu_filter(sc, g, X, lc, lmax, w.order, w.jackson, dtype=dtype, G=G)
+    cols = [0, 17, 47]
+    Xc = X[:, cols] if dtype == torch.float64 else X[:, cols].astype(np.float32).astype(np.float64)
+    Yo = chebyshev.lowpass_filter(laplacian.laplacian(g), Xc, lc, lmax, w.order, w.jackson)
+    assert rel(Y[:, cols], Yo) <= tol
+
+
+@pytest.mark.slow
+def test_full_size_c4_properties(sc):
+    """configs[4] (SBM N=10M, ~2e8 nonzeros, R=96, p=300) at full size, in bench.py's launch
+    configuration, checked by properties that hold at any size:
+      * the constant vector is the lambda=0 eigenvector: F 1 = p(0) 1 (PAPER.md l.79, l.122);
+      * columns are independent: the filter of 8 sampled columns alone equals those columns of
+        the full 96-column run (different chunking, same per-element arithmetic)."""
+    from scinputs import configs
+    w = configs.WORKLOADS["c4_sbm10m"]
+    g = configs.build_graph("c4_sbm10m")
+    G = sc.Graph.from_csr(g)
+    n, R, p = g.n, w.R, w.order
+    lmax = sc.sc_lambda_max(G.handle, 40, 0.01, 3)
+    lc = 0.05 * lmax
+    X = torch.empty((n, R), dtype=torch.float32, device="cuda")
+    sc.sc_random_signals_f32(n, R, 0, 80, 0, 0.0, X)
+    X[:, 5] = 1.0
+    Y = torch.empty_like(X)
+    sc.sc_filter_lowpass_f32(G.handle, lc, lmax, p, w.jackson, R, 0, X, Y)
+    p0 = float(chebyshev.poly_eval(0.0, chebyshev.filter_coeffs(lc, lmax, p, w.jackson), lmax))
+    c5 = Y[:, 5].double().cpu().numpy()
+    assert np.max(np.abs(c5 - p0)) <= 1e-4 * max(1.0, abs(p0))
+    cols = [0, 5, 31, 32, 63, 64, 90, 95]
+    Xs = X[:, cols].contiguous()
+    Ys = torch.empty_like(Xs)
+    sc.sc_filter_lowpass_f32(G.handle, lc, lmax, p, w.jackson, len(cols), 0, Xs, Ys)
+    torch.cuda.synchronize()
+    a, b = Ys.cpu().numpy(), Y[:, cols].cpu().numpy()
+    assert rel(a, b.astype(np.float64)) <= 1e-6
+
+
 # ---------------------------------------------------------------------------
 # eigencount moments and lambda_k dichotomy
 # ---------------------------------------------------------------------------
