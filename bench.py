@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cluster", action="store_true")
+    ap.add_argument("--no-stability", action="store_true")
     return ap.parse_args()
 
 
@@ -330,6 +331,24 @@ def run_ours(args):
                               "restarts": w.kmeans_restarts, "lambda_max": info[0], "lambda_k": info[1],
                               "count_k": info[2], "kmeans_iters": int(info[4]), "ari_vs_planted": ari,
                               "api": "sc_cluster (device-resident graph)"}
+
+    # ---- stability measure gamma(k) on configs[2] (§4.3 Eq.(11)): k in [10, 30],
+    # J = 10 redraws, R = 48, p = 150, 5 k-means++ restarts per clustering
+    if world == 1 and rank == 0 and not args.no_stability:
+        w2 = configs.WORKLOADS["c2_sbm100k"]
+        g2 = configs.build_graph("c2_sbm100k", seed=args.seed)
+        G2 = sc.Graph.from_csr(g2)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gam, lks = sc.sc_stability(G2.handle, 10, 30, 10, w2.R, w2.order, True, 32, args.seed, 5, 100)
+        torch.cuda.synchronize()
+        ks = list(range(10, 31))
+        out["stability_e2e"] = {"workload": "c2_sbm100k", "seconds": time.perf_counter() - t0, "k_range": [10, 30],
+                                "J": 10, "R": w2.R, "order": w2.order, "kmeans_restarts": 5,
+                                "k_star": ks[int(np.argmax(gam))], "planted_k": w2.k,
+                                "gamma": [round(float(x), 4) for x in gam],
+                                "api": "sc_stability (device-resident graph)"}
+        G2.close()
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt, desc = oracle_sample(g, w, lam_k, lmax, cols=1, budget_s=15.0)

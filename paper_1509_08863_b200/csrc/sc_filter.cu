@@ -599,24 +599,6 @@ void stage_plan(int tr, bool unit, int* cap, int* nstages) {
   *nstages = ns;
 }
 
-const uint16_t* tile_order(const sc_graph* g, int tr, int64_t row_begin, int64_t row_end, cudaStream_t s) {
-  std::lock_guard<std::mutex> lock(g->tile_orders_mu);
-  auto key = std::make_tuple(tr, row_begin, row_end);
-  auto it = g->tile_orders.find(key);
-  if (it != g->tile_orders.end()) return it->second->as<uint16_t>();
-  const int64_t ntiles = (row_end - row_begin + tr - 1) / tr;
-  auto buf = std::make_unique<DevBuf>();
-  if (buf->ensure(sizeof(uint16_t) * (size_t)std::max<int64_t>(1, ntiles) * tr) != SC_OK) return nullptr;
-  if (ntiles > 0) {
-    tile_order_kernel<<<(unsigned)ntiles, 256, sizeof(int) * tr, s>>>(g->row_ptr.as<int64_t>(), row_begin, row_end, tr,
-                                                                     buf->as<uint16_t>());
-    if (cudaGetLastError() != cudaSuccess) return nullptr;
-  }
-  const uint16_t* out = buf->as<uint16_t>();
-  g->tile_orders[key] = std::move(buf);
-  return out;
-}
-
 template <typename T>
 int launch_step_impl(const sc_graph* g, const StepParams& p, cudaStream_t s, bool moments,
                      int* grid_out) {
@@ -710,6 +692,41 @@ std::vector<int> chunk_plan(int R, int64_t n_cols) {
 
 }  // namespace
 
+const uint16_t* tile_order(const sc_graph* g, int tr, int64_t row_begin, int64_t row_end, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(g->tile_orders_mu);
+  auto key = std::make_tuple(tr, row_begin, row_end);
+  auto it = g->tile_orders.find(key);
+  if (it != g->tile_orders.end()) return it->second->as<uint16_t>();
+  const int64_t ntiles = (row_end - row_begin + tr - 1) / tr;
+  auto buf = std::make_unique<DevBuf>();
+  if (buf->ensure(sizeof(uint16_t) * (size_t)std::max<int64_t>(1, ntiles) * tr) != SC_OK) return nullptr;
+  if (ntiles > 0) {
+    tile_order_kernel<<<(unsigned)ntiles, 256, sizeof(int) * tr, s>>>(g->row_ptr.as<int64_t>(), row_begin, row_end, tr,
+                                                                     buf->as<uint16_t>());
+    if (cudaGetLastError() != cudaSuccess) return nullptr;
+  }
+  const uint16_t* out = buf->as<uint16_t>();
+  g->tile_orders[key] = std::move(buf);
+  return out;
+}
+
+void prof_launch_begin(cudaStream_t s, cudaEvent_t* e0) {
+  *e0 = nullptr;
+  if (!g_prof.on) return;
+  *e0 = g_prof.get();
+  cudaEventRecord(*e0, s);
+}
+
+void prof_launch_end(cudaStream_t s, cudaEvent_t e0, double algo_bytes, int steps) {
+  if (!g_prof.on || !e0) return;
+  cudaEvent_t e1 = g_prof.get();
+  cudaEventRecord(e1, s);
+  g_prof.ev.emplace_back(e0, e1);
+  g_prof.launches += 1;
+  g_prof.step_launches += steps;
+  g_prof.algo_bytes += algo_bytes;
+}
+
 template <typename T>
 std::vector<int> chunk_widths(int R, int64_t n_cols) {
   return chunk_plan<T>(R, n_cols);
@@ -796,6 +813,16 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
     T* bufs[2] = {g->ws_b.as<T>(), g->ws_a.as<T>()};   // T_j lives in bufs[j & 1]
     const T* Xc = Xw + col0;
     T* Yc = Yw + col0;
+    // small graphs: one cooperative launch for all steps, CSR resident in shared memory
+    static const int use_resident = env_int("SC_RESIDENT", 1);
+    if (use_resident) {
+      bool ok = false;
+      SC_TRY(resident_filter<T>(g, d, order, lambda_max, w, Xc, Rp, Yc, Rp, bufs[0], bufs[1], s, &ok));
+      if (ok) {
+        col0 += w;
+        continue;
+      }
+    }
     int added = -1;
     for (int st = 0; st < order; ++st) {
       StepParams p{};

@@ -117,6 +117,11 @@ struct sc_graph {
   // per (tile rows, row_begin, row_end): degree-sorted row order inside each tile (uint16)
   mutable std::map<std::tuple<int, int64_t, int64_t>, std::unique_ptr<sc::DevBuf>> tile_orders;
   mutable std::mutex tile_orders_mu;
+  // resident-CSR small-graph plans per (chunk width, element size): host ints
+  // {usable, grid, cap_rows, cap_nnz, smem}, device tile ranges, step coefficients
+  std::map<std::pair<int, int>, std::vector<int64_t>> resident_plans;
+  std::map<std::pair<int, int>, std::unique_ptr<sc::DevBuf>> resident_tiles;
+  sc::DevBuf resident_coef;
   int num_sms = 148;
   int device = 0;
 };
@@ -145,6 +150,19 @@ struct StepParams {
 // launch one fused step for `width` columns starting at the given pointers
 template <typename T>
 int launch_step(const sc_graph* g, const StepParams& p, cudaStream_t s);
+
+// degree-sorted row order of every tile of tr rows over [row_begin, row_end) (cached on g)
+const uint16_t* tile_order(const sc_graph* g, int tr, int64_t row_begin, int64_t row_end, cudaStream_t s);
+
+// launch profiler hooks for kernels launched outside launch_step (one launch = `steps` steps)
+void prof_launch_begin(cudaStream_t s, cudaEvent_t* e0);
+void prof_launch_end(cudaStream_t s, cudaEvent_t e0, double algo_bytes, int steps);
+
+// all `order` steps of one column chunk in one cooperative launch when the CSR fits the
+// aggregate shared memory; *ok = false otherwise (sc_resident.cu)
+template <typename T>
+int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, int w, const T* Xc, int64_t ld_x,
+                    T* Yc, int64_t ld_y, T* buf0, T* buf1, cudaStream_t s, bool* ok);
 
 // column chunk widths (each a supported kernel width) covering R columns
 template <typename T>
