@@ -93,25 +93,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void ldg_hint(const float* p, float (&v)[4], uint64_t pol) {
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
-               : "l"(p), "l"(pol));
-}
-__device__ __forceinline__ void ldg_hint(const double* p, double (&v)[2], uint64_t pol) {
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
-}
 // 16-byte global -> shared async copy (LDGSTS, bypasses L1) with an L2 policy
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // global -> shared bulk copy completing on `bar` (bytes and both addresses 16-byte multiples)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(
@@ -310,7 +296,6 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   const T* __restrict__ tcur = static_cast<const T*>(p.tcur);
   T* tnext = static_cast<T*>(p.tnext);
   T* y = static_cast<T*>(p.y);
-  const bool next_first = (p.l2_flags & 1) != 0;
   // gather address of row k for this lane: gbase + k * ldb (one IMAD.WIDE.U32)
   const char* gbase = reinterpret_cast<const char*>(tcur + c);
   const uint32_t ldb = static_cast<uint32_t>(p.ld_cur * sizeof(T));
@@ -414,10 +399,7 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
         const T lt = si * own[w] - acc[w];               // (L T_s)[i]
         tn[w] = a * lt + bc * own[w] + bp * prv[w];      // T_{s+1}[i]
       }
-      if (tnext) {
-        if (next_first) Stream<T>::st(tnext + row * p.ld_next + c, tn, pol_stream);
-        else Vec<T>::st(tnext + row * p.ld_next + c, tn);
-      }
+      if (tnext) Vec<T>::st(tnext + row * p.ld_next + c, tn);   // T_{s+1} is gathered next step: normal L2 policy
       if (p.y_mode) {
         const T cyp = static_cast<T>(p.cy_prev), cyc = static_cast<T>(p.cy_cur), cyn = static_cast<T>(p.cy_next);
 #pragma unroll
@@ -535,7 +517,7 @@ struct Prof {
 Prof g_prof;
 
 // ---------------------------------------------------------------------------
-// tuning knobs (env SC_CHUNK, SC_EB, SC_L2_BUDGET_MB) -- see DESIGN.md
+// tuning knobs (env SC_CHUNK, SC_L2_BUDGET_MB, SC_RESIDENT) -- see DESIGN.md
 // ---------------------------------------------------------------------------
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
@@ -640,8 +622,6 @@ int launch_step_impl(const sc_graph* g, const StepParams& p, cudaStream_t s, boo
   const uint16_t* order = tile_order(g, tr, p.row_begin, p.row_end, s);
   if (!order) return fail(SC_ERR_NOMEM, "tile order allocation failed");
   StepParams q = p;
-  static const int l2_flags = env_int("SC_L2_FLAGS", 0);
-  q.l2_flags = l2_flags;
   k<<<grid, kThreads, smem, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(),
                                  g->unit_weights ? nullptr : g->values.as<float>(), strength_of<T>(g), order, q, cap,
                                  nst);

@@ -140,7 +140,6 @@ struct StepParams {
   double a, b_cur, b_prev;
   double cy_prev, cy_cur, cy_next;
   int y_mode;        // 0 none, 1 write, 2 accumulate
-  int l2_flags;      // bit 0: T_next stores evict-first; bit 1: T_cur gathers evict-last
   int width;         // columns processed (chunk width)
   int total_width;   // all columns of the block (for the profiler's CSR share)
   // moments mode (fp64 only): per-block partial sums written to `part`

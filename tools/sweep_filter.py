@@ -26,7 +26,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c3_sbm1m")
     ap.add_argument("--chunks", default="16,32")
-    ap.add_argument("--l2flags", default="0,1")
+    ap.add_argument("--l2flags", default="0", help="(removed experiment knob, ignored)")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--tag", default="")
@@ -46,7 +46,6 @@ def main():
     for ch in a.chunks.split(","):
         for fl in a.l2flags.split(","):
             os.environ["SC_CHUNK"] = ch
-            os.environ["SC_L2_FLAGS"] = fl
             f(G.handle, d, order, lmax, R, X, Y)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
