@@ -62,7 +62,8 @@ def build(verbose_ptxas: bool = False, defs=(), out: str = LIB) -> str:
     """Compile every source and link ``out``.  ``defs`` (e.g. ["-DSC_EB_F32=12"]) build a
     tuning variant; its objects get their own names so variants do not clobber each other."""
     os.makedirs(BUILD, exist_ok=True)
-    tag = "" if not defs else "." + "_".join(d.lstrip("-D").replace("=", "") for d in defs)
+    import re
+    tag = "" if not defs else "." + re.sub(r"[^A-Za-z0-9]+", "_", "_".join(d.lstrip("-D") for d in defs))
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose_ptxas, defs, tag), srcs))
