@@ -794,8 +794,7 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
     const T* Xc = Xw + col0;
     T* Yc = Yw + col0;
     // small graphs: one cooperative launch for all steps, CSR resident in shared memory
-    static const int use_resident = env_int("SC_RESIDENT", 1);
-    if (use_resident) {
+    if (env_int("SC_RESIDENT", 1)) {
       bool ok = false;
       SC_TRY(resident_filter<T>(g, d, order, lambda_max, w, Xc, Rp, Yc, Rp, bufs[0], bufs[1], s, &ok));
       if (ok) {

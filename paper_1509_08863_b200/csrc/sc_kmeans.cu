@@ -233,10 +233,11 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
     for (int q = 0; q < d; ++q) {
       const double2 xa = *reinterpret_cast<const double2*>(sX + (size_t)q * kAT + ty * 4);
       const double2 xb = *reinterpret_cast<const double2*>(sX + (size_t)q * kAT + ty * 4 + 2);
-      const double2 ca = *reinterpret_cast<const double2*>(sC + (size_t)q * kAT + tx * 4);
-      const double2 cb = *reinterpret_cast<const double2*>(sC + (size_t)q * kAT + tx * 4 + 2);
+      // thread tx owns centroids tx, tx+16, tx+32, tx+48 of the tile: the 16 lanes of a row
+      // read 16 consecutive doubles per load (one wavefront, no bank conflicts)
+      const double* cq = sC + (size_t)q * kAT + tx;
       const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
-      const double cv[4] = {ca.x, ca.y, cb.x, cb.y};
+      const double cv[4] = {cq[0], cq[16], cq[32], cq[48]};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int cidx = tx * 4 + j;
+      const int cidx = tx + 16 * j;
       if (cidx < kt) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)

@@ -131,8 +131,12 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("path", ["resident", "streaming"])
 @pytest.mark.parametrize("name,maker,R,order,jackson,ratio", CASES, ids=[c[0] for c in CASES])
-def test_filter_f32_parity(sc, name, maker, R, order, jackson, ratio):
+def test_filter_f32_parity(sc, name, maker, R, order, jackson, ratio, path, monkeypatch):
+    # small graphs take the resident-CSR cooperative kernel by default; SC_RESIDENT=0 forces
+    # the streaming per-step kernel on the same inputs
+    monkeypatch.setenv("SC_RESIDENT", "1" if path == "resident" else "0")
     g = maker()
     L = laplacian.laplacian(g)
     lmax = 2.0 * float(laplacian.strengths(laplacian.adjacency(g)).max())
@@ -142,8 +146,10 @@ def test_filter_f32_parity(sc, name, maker, R, order, jackson, ratio):
     assert rel(Y, Yo) <= F32_TOL
 
 
+@pytest.mark.parametrize("path", ["resident", "streaming"])
 @pytest.mark.parametrize("name,maker,R,order,jackson,ratio", CASES[:6], ids=[c[0] for c in CASES[:6]])
-def test_filter_f64_parity(sc, name, maker, R, order, jackson, ratio):
+def test_filter_f64_parity(sc, name, maker, R, order, jackson, ratio, path, monkeypatch):
+    monkeypatch.setenv("SC_RESIDENT", "1" if path == "resident" else "0")
     g = maker()
     L = laplacian.laplacian(g)
     lmax = 2.0 * float(laplacian.strengths(laplacian.adjacency(g)).max())
