@@ -225,7 +225,8 @@ int sc_normalize_rows_f32(float* F, int64_t n, int d, void* stream);
  *  labels    n int32 (host/device);   centroids  k*d doubles or NULL;
  *  inertia   host double or NULL;     iters      host int or NULL;
  *  best_restart host int or NULL.
- * Errors: SC_ERR_ARG for k<1, k>n, d<1, restarts<1, max_iter<1.
+ * Errors: SC_ERR_ARG for k<1, k>n, d<1, d>200 (the assignment kernel stages 64 points and
+ * 64 centroids of d fp64 coordinates in shared memory), restarts<1, max_iter<1, n >= 2^25.
  */
 int sc_kmeans(const float* F, int64_t n, int d, int k, int restarts, int max_iter,
               uint64_t seed, const double* uniforms, int32_t* labels, double* centroids,
