@@ -91,3 +91,23 @@ def test_argument_errors(sc):
         sc.sc_cheby_coeffs(1.0, -1.0, 5, False)
     with pytest.raises(sc.SCError):
         sc.sc_lambda_k_from_moments(np.zeros(11), 5, 0, 4.0, True)
+
+
+def test_argument_errors_new_entry_points(sc):
+    """Argument checks run before any device work (no GPU needed)."""
+    import ctypes
+    lib = sc._lib._lib
+    gamma = np.zeros(3)
+    # null graph / bad k range / J < 2
+    assert lib.sc_stability(None, 2, 4, 3, 8, 10, 1, 4, ctypes.c_uint64(1), 1, 10, ctypes.c_double(0.0), None,
+                            gamma.ctypes.data, None, None, None) == -1
+    assert lib.sc_dist_create(None, None, 0, None, 0, None, None, None) == -1
+    out = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(128)
+    assert lib.sc_comm_init(uid, 0, 0, ctypes.byref(out)) == -1      # world < 1
+    assert lib.sc_comm_init(uid, 2, 2, ctypes.byref(out)) == -1      # rank >= world
+    assert lib.sc_nccl_unique_id(None) == -1
+    assert lib.sc_dist_filter_f32(None, None, 1, ctypes.c_double(1.0), 4, None, None, None) == -1
+    assert "argument" in sc.sc_last_error() or "null" in sc.sc_last_error()
+    with pytest.raises(sc.SCError):
+        sc.sc_kmeans(np.zeros((4, 2), np.float32), 4, 2, 5, 1, 10, 0, None, np.zeros(4, np.int32))   # k > n
