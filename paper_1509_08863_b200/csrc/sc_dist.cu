@@ -173,10 +173,6 @@ int sc_dist_create(sc_graph* g, sc_comm* c, int64_t n_interior, const int64_t* s
     ro += d->recv_counts[q];
   }
   auto bail = [&](int rc) { delete d; return rc; };
-  // The step kernels are persistent (grid = SMs x resident CTAs); leave a few SMs free so
-  // that NCCL's send/recv kernels on the communication stream can run concurrently with
-  // the interior step instead of queueing behind it.
-  if (c->world > 1) g->num_sms = std::max(1, g->num_sms - kNcclReservedSms);
   if (so != n_send || ro != d->n_halo) return bail(fail(SC_ERR_ARG, "send/recv counts do not match n_send / n_halo"));
   if (n_send) {
     int rc = d->send_idx.ensure(sizeof(int64_t) * n_send);
@@ -185,6 +181,10 @@ int sc_dist_create(sc_graph* g, sc_comm* c, int64_t n_interior, const int64_t* s
                    is_device_ptr(send_idx) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(SC_ERR_CUDA, "send_idx upload failed"));
   }
+  // The step kernels are persistent (grid = SMs x resident CTAs); leave a few SMs free so
+  // that NCCL's send/recv kernels on the communication stream can run concurrently with
+  // the interior step instead of queueing behind it.
+  if (c->world > 1) g->num_sms = std::max(1, g->num_sms - kNcclReservedSms);
   *out = d;
   return SC_OK;
 }
