@@ -121,6 +121,31 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def gather_ceiling(row_bytes, table_bytes):
+    """Measured random-gather ceiling (GB/s) for rows of `row_bytes` gathered from a table of
+    `table_bytes`: best EB of the smallest probed table >= table_bytes
+    (profiles/r01_gather_probe.txt, tools/gather_probe.cu on this pool's B200)."""
+    import re
+    p = os.path.join(ROOT, "profiles", "r01_gather_probe.txt")
+    if not os.path.exists(p):
+        return None, None
+    rows = []
+    for ln in open(p):
+        m = re.search(r"row=\s*(\d+)B table=\s*([\d.]+)MB EB=\s*(\d+).*?:\s*([\d.]+) GB/s", ln)
+        if m:
+            rows.append((int(m.group(1)), float(m.group(2)) * 1e6, float(m.group(4))))
+    cands = [r for r in rows if r[0] == row_bytes and r[1] >= table_bytes]
+    if not cands:
+        cands = [r for r in rows if r[0] == row_bytes]
+        if not cands:
+            return None, None
+        tb = max(r[1] for r in cands)
+    else:
+        tb = min(r[1] for r in cands)
+    best = max(r[2] for r in cands if r[1] == tb)
+    return best, f"{row_bytes} B rows from a {tb / 1e6:.0f} MB table"
+
+
 def ncu_traffic(workload):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
@@ -308,6 +333,17 @@ def run_ours(args):
     bytes_per_launch = algo_bytes / max(step_launches, 1)
     achieved = bytes_per_launch / avg_launch_s / 1e9
     traffic = ncu_traffic(args.workload)
+    # gathered bytes: every nonzero of W reads one R-wide row of T_s per step
+    gather_gbps = float(g.nnz) * R * 4 * order * args.steps / (kern_ms / 1e3) / 1e9
+    cw = int(os.environ.get("SC_CHUNK", "0")) or None
+    if cw is None:   # the library's chunk rule: widest power of two with N*w*4 <= 128 MB
+        cw = 128
+        while cw > 4 and n * cw * 4 > 128 * 2 ** 20:
+            cw //= 2
+        if cw * 4 < 128:
+            cw = 128
+    cw = min(cw, R)
+    gceil, gcase = gather_ceiling(cw * 4, n * cw * 4)
 
     out = None
     if rank == 0:
@@ -321,7 +357,9 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "cheb_step_kernel (fused SpMM + 3-term recurrence + Y accumulation)",
                          "avg_launch_us": avg_launch_s * 1e6, "algo_bytes_per_launch": bytes_per_launch,
-                         "l2_gather_GBps": float(g.nnz) * R * 4 * order * args.steps / (kern_ms / 1e3) / 1e9,
+                         "l2_gather_GBps": gather_gbps,
+                         "l2_gather_ceiling_GBps": gceil, "l2_gather_ceiling_case": gcase,
+                         "l2_gather_frac": (gather_gbps / gceil) if gceil else None,
                          "l2_gather_note": "nnz(W)*R*4 bytes of gathered T_s rows per step cross L2->SM; "
                                            "measured random-gather ceiling in profiles/r01_gather_probe.txt",
                          "kernel_share_of_step": (kern_ms / ms) if ms > 0 else None},
