@@ -26,6 +26,9 @@
  *    k-means decisions (argmin, D^2 sampling, best replicate) are taken in fp64.
  *  - There is no CPU fallback: without a CUDA device every compute call
  *    returns SC_ERR_CUDA.
+ *  - A graph handle owns grow-only device workspaces and per-shape launch plans:
+ *    use one handle from one host thread / one stream at a time (distinct handles
+ *    are independent).
  */
 #ifndef SC_B200_H
 #define SC_B200_H
