@@ -196,26 +196,32 @@ __global__ void minmax_kernel(const int32_t* __restrict__ a, int64_t n, int* out
 // ---------------------------------------------------------------------------
 constexpr int kAT = 64;   // points per block and centroids per tile
 
+// Full scan of the points in `list` (or all points when list == nullptr): exact argmin
+// (first minimum) and the second-smallest distance, which becomes the point's lower bound
+// lo_i = sqrt(second) for the pruning test of the next iterations (check_kernel).
 __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ F, int64_t n, int d,
                                                       const double* __restrict__ C, int k,
-                                                      int32_t* __restrict__ lab, const int32_t* __restrict__ old_lab,
-                                                      int* __restrict__ changed, double* __restrict__ part_inertia,
-                                                      unsigned* __restrict__ counts) {
+                                                      const int32_t* __restrict__ list, const int* __restrict__ list_len,
+                                                      int32_t* __restrict__ lab, double* __restrict__ dmin,
+                                                      double* __restrict__ lo) {
   extern __shared__ double sm3[];
   double* sX = sm3;                        // [d][kAT]
   double* sC = sm3 + (size_t)d * kAT;      // [d][kAT]
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
+  const int64_t m = list ? (int64_t)*list_len : n;
   const int64_t p0 = (int64_t)blockIdx.x * kAT;
+  if (p0 >= m) return;
   for (int e = tid; e < kAT * d; e += 256) {
     const int row = e / d, q = e - row * d;
-    const int64_t gi = p0 + row;
-    sX[(size_t)q * kAT + row] = gi < n ? (double)F[gi * d + q] : 0.0;
+    const int64_t pi = p0 + row;
+    const int64_t gi = pi < m ? (list ? (int64_t)list[pi] : pi) : -1;
+    sX[(size_t)q * kAT + row] = gi >= 0 ? (double)F[gi * d + q] : 0.0;
   }
-  double best[4];
+  double best[4], second[4];
   int bidx[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) { best[i] = INFINITY; bidx[i] = -1; }
+  for (int i = 0; i < 4; ++i) { best[i] = INFINITY; second[i] = INFINITY; bidx[i] = -1; }
   for (int c0 = 0; c0 < k; c0 += kAT) {
     const int kt = min(kAT, k - c0);
     __syncthreads();
@@ -251,50 +257,129 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
       const int cidx = tx + 16 * j;
       if (cidx < kt) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (acc[i][j] < best[i]) { best[i] = acc[i][j]; bidx[i] = c0 + cidx; }
+        for (int i = 0; i < 4; ++i) {
+          const double v = acc[i][j];
+          if (v < best[i]) { second[i] = best[i]; best[i] = v; bidx[i] = c0 + cidx; }
+          else if (v < second[i]) second[i] = v;
+        }
       }
     }
   }
-  // (dist, index) lexicographic min over the 16 threads of each point row
+  // (dist, index) lexicographic min over the 16 threads of each point row, second best merged
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best[i], o);
+      const double os = __shfl_xor_sync(0xffffffffu, second[i], o);
       const int oi = __shfl_xor_sync(0xffffffffu, bidx[i], o);
       const bool take = (oi >= 0) && (bidx[i] < 0 || ob < best[i] || (ob == best[i] && oi < bidx[i]));
+      const double loser = take ? best[i] : ob;
+      second[i] = fmin(fmin(second[i], os), loser);
       if (take) { best[i] = ob; bidx[i] = oi; }
     }
   }
-  double inertia = 0.0;
-  int nchg = 0;
   // thread tx < 4 of row ty handles point ty*4 + tx
   const int i = tx & 3;
-  double bv = best[0];
+  double bv = best[0], sv = second[0];
   int bl = bidx[0];
 #pragma unroll
-  for (int ii = 1; ii < 4; ++ii) if (ii == i) { bv = best[ii]; bl = bidx[ii]; }
-  const int64_t gi = p0 + ty * 4 + i;
-  const bool mine = tx < 4 && gi < n;
-  if (mine) {
+  for (int ii = 1; ii < 4; ++ii) if (ii == i) { bv = best[ii]; sv = second[ii]; bl = bidx[ii]; }
+  const int64_t pi = p0 + ty * 4 + i;
+  if (tx < 4 && pi < m) {
+    const int64_t gi = list ? (int64_t)list[pi] : pi;
     if (bl < 0) bl = 0;   // all distances NaN/inf: deterministic fallback
     lab[gi] = bl;
-    inertia = bv;
-    if (old_lab && old_lab[gi] != bl) nchg = 1;
+    dmin[gi] = bv;
+    lo[gi] = sqrt(sv);
   }
-  const unsigned peers = __match_any_sync(0xffffffffu, mine ? bl : -1);
-  if (mine && (tid & 31) == __ffs(peers) - 1) atomicAdd(&counts[bl], (unsigned)__popc(peers));
+}
+
+// Pruning test (Hamerly): the centroids moved by at most dmax since lo_i (a lower bound
+// of the distance to every centroid but the assigned one) was computed.  The exact
+// squared distance to the assigned centroid is computed with the scan's arithmetic; if
+// its root is below the decremented bound (with a 1e-9 relative margin for rounding),
+// the assigned centroid is the unique argmin and the point keeps it -- the labels are the
+// ones a full scan would produce.  Otherwise the point is queued for a full scan.
+__global__ void check_kernel(const float* __restrict__ F, int64_t n, int d, const double* __restrict__ C,
+                             const int32_t* __restrict__ old_lab, const double* __restrict__ dmax,
+                             int32_t* __restrict__ lab, double* __restrict__ dmin, double* __restrict__ lo,
+                             int32_t* __restrict__ list, int* __restrict__ list_len) {
+  const double dm = *dmax;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int a = old_lab[i];
+    const float* x = F + i * d;
+    const double* c = C + (size_t)a * d;
+    double acc = 0.0;
+    for (int q = 0; q < d; ++q) {
+      const double diff = __dsub_rn((double)x[q], c[q]);
+      acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    const double l = lo[i] - dm;
+    lo[i] = l;
+    const bool keep = sqrt(acc) * (1.0 + 1e-9) < l * (1.0 - 1e-9);
+    if (keep) {
+      lab[i] = a;
+      dmin[i] = acc;
+    }
+    const unsigned need = __ballot_sync(__activemask(), !keep);
+    if (!keep) {
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(need) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(list_len, __popc(need));
+      base = __shfl_sync(need, base, leader);
+      list[base + __popc(need & ((1u << lane) - 1))] = static_cast<int32_t>(i);
+    }
+  }
+}
+
+// max_c ||C[c] - C_old[c]|| (inflated by 1e-9 relative for rounding) into *dmax
+__global__ void centroid_shift_kernel(const double* __restrict__ C, const double* __restrict__ Cold, int k, int d,
+                                      double* __restrict__ dmax) {
   __shared__ double sh[256];
-  __shared__ int shc[256];
-  sh[tid] = inertia;
-  shc[tid] = nchg;
+  double m = 0.0;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < d; ++q) {
+      const double t = C[(size_t)c * d + q] - Cold[(size_t)c * d + q];
+      s += t * t;
+    }
+    m = fmax(m, sqrt(s));
+  }
+  sh[threadIdx.x] = m;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (tid < o) { sh[tid] += sh[tid + o]; shc[tid] += shc[tid + o]; }
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
     __syncthreads();
   }
-  if (tid == 0) {
+  if (threadIdx.x == 0) *dmax = sh[0] * (1.0 + 1e-9) + 1e-300;
+}
+
+// per-block inertia partials over fixed index ranges (deterministic whatever path
+// produced each point), changed count, label histogram
+__global__ void __launch_bounds__(256) assign_stats_kernel(const int32_t* __restrict__ lab,
+                                                           const int32_t* __restrict__ old_lab,
+                                                           const double* __restrict__ dmin, int64_t n,
+                                                           double* __restrict__ part_inertia,
+                                                           int* __restrict__ changed, unsigned* __restrict__ counts) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const bool valid = i < n;
+  const int bl = valid ? lab[i] : -1;
+  double inertia = valid ? dmin[i] : 0.0;
+  int nchg = (valid && old_lab && old_lab[i] != bl) ? 1 : 0;
+  const unsigned peers = __match_any_sync(0xffffffffu, bl);
+  if (valid && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[bl], (unsigned)__popc(peers));
+  __shared__ double sh[256];
+  __shared__ int shc[256];
+  sh[threadIdx.x] = inertia;
+  shc[threadIdx.x] = nchg;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) { sh[threadIdx.x] += sh[threadIdx.x + o]; shc[threadIdx.x] += shc[threadIdx.x + o]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     part_inertia[blockIdx.x] = sh[0];
     if (shc[0]) atomicAdd(changed, shc[0]);
   }
@@ -422,7 +507,15 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   SC_TRY(b_perm.ensure(sizeof(int32_t) * n));
   SC_TRY(b_items.ensure(sizeof(int64_t) * 2 * max_items + sizeof(int32_t) * 2 * k));
   SC_TRY(b_psum.ensure(sizeof(unsigned long long) * 2 * (size_t)max_items * d));
-  SC_TRY(b_part.ensure(sizeof(double) * std::max<int64_t>(std::max<int64_t>(grid, G), nblk)));
+  const int64_t nstat = (n + 255) / 256;
+  SC_TRY(b_part.ensure(sizeof(double) * std::max<int64_t>(std::max<int64_t>(grid, G), std::max(nblk, nstat))));
+  DevBuf b_dmin, b_lo, b_list, b_len, b_dmax, b_Cold;
+  SC_TRY(b_dmin.ensure(sizeof(double) * n));
+  SC_TRY(b_lo.ensure(sizeof(double) * n));
+  SC_TRY(b_list.ensure(sizeof(int32_t) * n));
+  SC_TRY(b_len.ensure(16));
+  SC_TRY(b_dmax.ensure(16));
+  SC_TRY(b_Cold.ensure(sizeof(double) * k * d));
   SC_TRY(b_misc.ensure(64));
   int32_t* lab = b_lab.as<int32_t>();
   int32_t* nw = b_new.as<int32_t>();
@@ -450,15 +543,33 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
 
   // Lloyd assignment of every point; host receives inertia (fixed-order sum of block
   // partials), the number of changed labels and the label histogram
+  // Hamerly pruning pays off when a full assignment is expensive; small problems (many of
+  // them in a stability scan) are launch-bound and take the plain full scan
+  const bool prune = (double)n * k * d >= 134217728.0;
   auto assign_all = [&](int32_t* out_lab, const int32_t* old, double* inertia, int* nchanged) -> int {
     SC_CUDA_TRY(cudaMemsetAsync(changed, 0, sizeof(int), s));
     SC_CUDA_TRY(cudaMemsetAsync(b_cnt.ptr, 0, sizeof(unsigned) * k, s));
-    assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, out_lab, old, changed,
-                                                           b_part.as<double>(), b_cnt.as<unsigned>());
+    if (!old || !prune) {
+      // full scan of every point (the first assignment of a restart also sets the bounds lo)
+      assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, nullptr, nullptr, out_lab,
+                                                             b_dmin.as<double>(), b_lo.as<double>());
+    } else {
+      // Hamerly pruning: points whose assigned centroid is provably still the unique
+      // nearest keep it; the rest are queued and fully rescanned
+      SC_CUDA_TRY(cudaMemsetAsync(b_len.ptr, 0, sizeof(int), s));
+      check_kernel<<<grid, kB, 0, s>>>(F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(),
+                                       b_lo.as<double>(), b_list.as<int32_t>(), b_len.as<int>());
+      SC_CUDA_TRY(cudaGetLastError());
+      assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, b_list.as<int32_t>(), b_len.as<int>(),
+                                                             out_lab, b_dmin.as<double>(), b_lo.as<double>());
+    }
     SC_CUDA_TRY(cudaGetLastError());
-    std::vector<double> part(nblk);
+    assign_stats_kernel<<<(unsigned)nstat, 256, 0, s>>>(out_lab, old, b_dmin.as<double>(), n, b_part.as<double>(),
+                                                       changed, b_cnt.as<unsigned>());
+    SC_CUDA_TRY(cudaGetLastError());
+    std::vector<double> part(nstat);
     int h_changed = 0;
-    SC_CUDA_TRY(cudaMemcpyAsync(part.data(), b_part.as<double>(), sizeof(double) * nblk, cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaMemcpyAsync(part.data(), b_part.as<double>(), sizeof(double) * nstat, cudaMemcpyDeviceToHost, s));
     SC_CUDA_TRY(cudaMemcpyAsync(&h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s));
     SC_CUDA_TRY(cudaMemcpyAsync(cnt_h.data(), b_cnt.ptr, sizeof(unsigned) * k, cudaMemcpyDeviceToHost, s));
     SC_CUDA_TRY(cudaStreamSynchronize(s));
@@ -474,6 +585,7 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   std::vector<int64_t> off_h(k + 1), ws_h, we_h;
   std::vector<int32_t> item0_h(k), nitems_h(k);
   auto update = [&](const int32_t* cur) -> int {
+    if (prune) SC_CUDA_TRY(cudaMemcpyAsync(b_Cold.ptr, C, sizeof(double) * k * d, cudaMemcpyDeviceToDevice, s));
     off_h[0] = 0;
     for (int c = 0; c < k; ++c) off_h[c + 1] = off_h[c] + cnt_h[c];
     ws_h.clear();
@@ -518,6 +630,10 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
         b_psum.as<unsigned long long>(), d_item0, d_nitems, b_cnt.as<unsigned>(), k, d, shift, C);
     SC_CUDA_TRY(cudaGetLastError());
     // the histogram buffer is reused by the next assignment only after this finalize (stream order)
+    if (prune) {
+      centroid_shift_kernel<<<1, 256, 0, s>>>(C, b_Cold.as<double>(), k, d, b_dmax.as<double>());
+      SC_CUDA_TRY(cudaGetLastError());
+    }
     return SC_OK;
   };
 
