@@ -70,6 +70,33 @@ struct DevBuf {
   template <typename T> T* as() const { return static_cast<T*>(ptr); }
 };
 
+// Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync on its stream): no
+// device-wide synchronisation, so concurrent streams (sc_stability's k-means workers)
+// stay concurrent.
+struct PoolBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st = 0;
+  PoolBuf() = default;
+  PoolBuf(const PoolBuf&) = delete;
+  PoolBuf& operator=(const PoolBuf&) = delete;
+  ~PoolBuf() {
+    if (ptr) cudaFreeAsync(ptr, st);
+  }
+  int ensure(size_t b, cudaStream_t s) {
+    if (b <= bytes && ptr) return SC_OK;
+    if (ptr) cudaFreeAsync(ptr, st);
+    ptr = nullptr;
+    bytes = 0;
+    st = s;
+    cudaError_t e = cudaMallocAsync(&ptr, b ? b : 1, s);
+    if (e != cudaSuccess) { ptr = nullptr; return fail(SC_ERR_NOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e)); }
+    bytes = b;
+    return SC_OK;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(ptr); }
+};
+
 // Is p a device (or managed) pointer of the current device?
 bool is_device_ptr(const void* p);
 

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "sc_internal.cuh"
@@ -81,45 +82,76 @@ __global__ void range_sums_kernel(const double* __restrict__ v, int64_t n, int64
   if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
 }
 
-// first i in [b0, b1) with start + cumsum(v[b0..i]) > target.  One warp: lane j sums a
-// contiguous slice (ascending), lane prefixes locate the slice holding the crossing, whose
-// lane rescans it element by element.  If no prefix exceeds target (rounding at the very
-// end of the range), the last positive entry is taken.
-__global__ void range_select_kernel(const double* __restrict__ v, int64_t b0, int64_t b1, double start,
-                                    double target, int64_t* out) {
+// Whole k-means++ draw on the device (no host round trip): the block sums are prefixed in
+// ascending order by one thread (the same fp64 sequence the host used to take), the block
+// holding u * total is found, then scanned as in range_select_kernel; the chosen row is
+// copied into centroid slot `c_out`.  total <= 0 (all points coincide with centres):
+// uniform draw floor(u n).
+__global__ void seed_select_kernel(const double* __restrict__ bsum, int G, const double* __restrict__ v, int64_t n,
+                                   int64_t chunk, double u, const float* __restrict__ F, int d,
+                                   double* __restrict__ c_out) {
+  __shared__ double s_start, s_target;
+  __shared__ int s_block;
+  __shared__ long long s_idx;
   const int lane = threadIdx.x;
-  const int64_t len = b1 - b0;
-  const int64_t per = (len + 31) / 32;
-  const int64_t s0 = min(b1, b0 + lane * per), s1 = min(b1, s0 + per);
-  double sum = 0.0;
-  int64_t last_pos = -1;
-  for (int64_t i = s0; i < s1; ++i) {
-    sum += v[i];
-    if (v[i] > 0.0) last_pos = i;
-  }
-  // exclusive prefix of the slice sums (fixed order: lanes ascending)
-  double pre = 0.0;
-  for (int j = 0; j < 32; ++j) {
-    const double sj = __shfl_sync(0xffffffffu, sum, j);
-    if (j < lane) pre += sj;
-  }
-  const double hi = start + pre + sum;
-  const unsigned cross = __ballot_sync(0xffffffffu, hi > target && s1 > s0);
-  long long lp = last_pos;
-  for (int o = 16; o > 0; o >>= 1) lp = max(lp, __shfl_xor_sync(0xffffffffu, lp, o));
-  if (cross == 0) {
-    if (lane == 0) *out = lp >= 0 ? lp : b1 - 1;
-    return;
-  }
-  const int L = __ffs(cross) - 1;
-  if (lane == L) {
-    double acc = start + pre;
-    for (int64_t i = s0; i < s1; ++i) {
-      acc += v[i];
-      if (acc > target) { *out = i; return; }
+  if (lane == 0) {
+    double pre = 0.0;
+    for (int b = 0; b < G; ++b) pre += bsum[b];
+    const double total = pre;
+    if (!(total > 0.0)) {
+      s_block = -1;
+      long long idx = (long long)floor(u * (double)n);
+      s_idx = idx < n - 1 ? idx : n - 1;
+    } else {
+      const double target = u * total;
+      double acc = 0.0;
+      int b = 0;
+      while (b < G - 1 && !(acc + bsum[b] > target)) { acc += bsum[b]; ++b; }
+      s_block = b;
+      s_start = acc;
+      s_target = target;
     }
-    *out = s1 - 1;
   }
+  __syncthreads();
+  if (s_block >= 0) {
+    const int64_t b0 = (int64_t)s_block * chunk, b1 = min(n, b0 + chunk);
+    const int64_t len = b1 - b0;
+    const int64_t per = (len + 31) / 32;
+    const int64_t s0 = min(b1, b0 + lane * per), s1 = min(b1, s0 + per);
+    double sum = 0.0;
+    int64_t last_pos = -1;
+    for (int64_t i = s0; i < s1; ++i) {
+      sum += v[i];
+      if (v[i] > 0.0) last_pos = i;
+    }
+    double pre = 0.0;
+    for (int j = 0; j < 32; ++j) {
+      const double sj = __shfl_sync(0xffffffffu, sum, j);
+      if (j < lane) pre += sj;
+    }
+    const double start = s_start, target = s_target;
+    const double hi = start + pre + sum;
+    const unsigned cross = __ballot_sync(0xffffffffu, hi > target && s1 > s0);
+    long long lp = last_pos;
+    for (int o = 16; o > 0; o >>= 1) lp = max(lp, __shfl_xor_sync(0xffffffffu, lp, o));
+    if (cross == 0) {
+      if (lane == 0) s_idx = lp >= 0 ? lp : b1 - 1;
+    } else {
+      const int L = __ffs(cross) - 1;
+      if (lane == L) {
+        double acc = start + pre;
+        long long pick = s1 - 1;
+        for (int64_t i = s0; i < s1; ++i) {
+          acc += v[i];
+          if (acc > target) { pick = i; break; }
+        }
+        s_idx = pick;
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t idx = s_idx;
+  for (int q = lane; q < d; q += blockDim.x) c_out[q] = (double)F[idx * d + q];
 }
 
 __global__ void row_to_centroid_kernel(const float* __restrict__ F, int64_t idx, int d, double* __restrict__ c) {
@@ -419,14 +451,41 @@ __global__ void scatter_members_simple_kernel(const int32_t* __restrict__ lab, i
   }
 }
 
+// Device-side plan of the member sums (no host round trip): cluster offsets (exclusive scan
+// of the histogram) and work items of <= chunk members, one thread, ascending clusters.
+__global__ void plan_members_kernel(const unsigned* __restrict__ counts, int k, int64_t chunk,
+                                    int64_t* __restrict__ off, int64_t* __restrict__ ws, int64_t* __restrict__ we,
+                                    int32_t* __restrict__ item0, int32_t* __restrict__ nitems,
+                                    int* __restrict__ total_items) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t o = 0;
+  int it = 0;
+  for (int c = 0; c < k; ++c) {
+    off[c] = o;
+    item0[c] = it;
+    const int64_t cnt = counts[c];
+    for (int64_t a = o; a < o + cnt; a += chunk) {
+      ws[it] = a;
+      we[it] = min(o + cnt, a + chunk);
+      ++it;
+    }
+    nitems[c] = it - item0[c];
+    o += cnt;
+  }
+  off[k] = o;
+  *total_items = it;
+}
+
 // exact member sums: work item w covers members [ws[w], we[w]) of cluster wc[w]; thread
 // (slot j, dim q) accumulates x * 2^shift exactly in a 128-bit integer, the block reduces
 // the slots of each dim and writes one 128-bit partial per (item, dim)
 __global__ void member_sum_kernel(const float* __restrict__ F, int d, const int32_t* __restrict__ perm,
-                                  const int64_t* __restrict__ ws, const int64_t* __restrict__ we, int shift,
+                                  const int64_t* __restrict__ ws, const int64_t* __restrict__ we,
+                                  const int* __restrict__ total_items, int shift,
                                   unsigned long long* __restrict__ part /* [items][d][2] */) {
   extern __shared__ unsigned long long red2[];   // [slots][d][2]
   const int w = blockIdx.x;
+  if (w >= *total_items) return;
   const int slots = blockDim.x / d;
   const int j = threadIdx.x / d, q = threadIdx.x - j * d;
   __int128 acc = 0;
@@ -496,32 +555,52 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   const int64_t nblk = (n + kAT - 1) / kAT;
   constexpr int64_t kChunk = 512;    // members per exact-sum work item
   const int64_t max_items = n / kChunk + k + 1;
-  DevBuf b_lab, b_new, b_d2, b_C, b_cnt, b_cur, b_off, b_perm, b_items, b_part, b_psum, b_misc;
-  SC_TRY(b_lab.ensure(sizeof(int32_t) * n));
-  SC_TRY(b_new.ensure(sizeof(int32_t) * n));
-  SC_TRY(b_d2.ensure(sizeof(double) * n));
-  SC_TRY(b_C.ensure(sizeof(double) * k * d));
-  SC_TRY(b_cnt.ensure(sizeof(unsigned) * k));
-  SC_TRY(b_cur.ensure(sizeof(unsigned) * k));
-  SC_TRY(b_off.ensure(sizeof(int64_t) * (k + 1)));
-  SC_TRY(b_perm.ensure(sizeof(int32_t) * n));
-  SC_TRY(b_items.ensure(sizeof(int64_t) * 2 * max_items + sizeof(int32_t) * 2 * k));
-  SC_TRY(b_psum.ensure(sizeof(unsigned long long) * 2 * (size_t)max_items * d));
+  PoolBuf b_lab, b_new, b_d2, b_C, b_cnt, b_cur, b_off, b_perm, b_items, b_part, b_psum, b_misc;
+  SC_TRY(b_lab.ensure(sizeof(int32_t) * n, s));
+  SC_TRY(b_new.ensure(sizeof(int32_t) * n, s));
+  SC_TRY(b_d2.ensure(sizeof(double) * n, s));
+  SC_TRY(b_C.ensure(sizeof(double) * k * d, s));
+  SC_TRY(b_cnt.ensure(sizeof(unsigned) * k, s));
+  SC_TRY(b_cur.ensure(sizeof(unsigned) * k, s));
+  SC_TRY(b_off.ensure(sizeof(int64_t) * (k + 1), s));
+  SC_TRY(b_perm.ensure(sizeof(int32_t) * n, s));
+  SC_TRY(b_items.ensure(sizeof(int64_t) * 2 * max_items + sizeof(int32_t) * 2 * k, s));
+  SC_TRY(b_psum.ensure(sizeof(unsigned long long) * 2 * (size_t)max_items * d, s));
   const int64_t nstat = (n + 255) / 256;
-  SC_TRY(b_part.ensure(sizeof(double) * std::max<int64_t>(std::max<int64_t>(grid, G), std::max(nblk, nstat))));
-  DevBuf b_dmin, b_lo, b_list, b_len, b_dmax, b_Cold;
-  SC_TRY(b_dmin.ensure(sizeof(double) * n));
-  SC_TRY(b_lo.ensure(sizeof(double) * n));
-  SC_TRY(b_list.ensure(sizeof(int32_t) * n));
-  SC_TRY(b_len.ensure(16));
-  SC_TRY(b_dmax.ensure(16));
-  SC_TRY(b_Cold.ensure(sizeof(double) * k * d));
-  SC_TRY(b_misc.ensure(64));
+  SC_TRY(b_part.ensure(sizeof(double) * std::max<int64_t>(std::max<int64_t>(grid, G), std::max(nblk, nstat)), s));
+  PoolBuf b_dmin, b_lo, b_list, b_len, b_dmax, b_Cold;
+  SC_TRY(b_dmin.ensure(sizeof(double) * n, s));
+  SC_TRY(b_lo.ensure(sizeof(double) * n, s));
+  SC_TRY(b_list.ensure(sizeof(int32_t) * n, s));
+  SC_TRY(b_len.ensure(16, s));   // [0] pruning queue length, [1] member work items
+  SC_TRY(b_dmax.ensure(16, s));
+  SC_TRY(b_Cold.ensure(sizeof(double) * k * d, s));
+  PoolBuf b_chg;
+  SC_TRY(b_chg.ensure(sizeof(int) * (max_iter + 2), s));
+  // pinned per-thread landing slots for the changed-label counts (kept across calls)
+  struct PinnedInts {
+    int* p = nullptr;
+    size_t n = 0;
+    ~PinnedInts() { if (p) cudaFreeHost(p); }
+  };
+  static thread_local PinnedInts pin;
+  if (pin.n < (size_t)max_iter + 2) {
+    if (pin.p) cudaFreeHost(pin.p);
+    pin.p = nullptr;
+    pin.n = 0;
+    SC_CUDA_TRY(cudaMallocHost(&pin.p, sizeof(int) * (max_iter + 2)));
+    pin.n = (size_t)max_iter + 2;
+  }
+  int* h_chg = pin.p;
+  cudaEvent_t ev_chg[2];
+  SC_CUDA_TRY(cudaEventCreateWithFlags(&ev_chg[0], cudaEventDisableTiming));
+  SC_CUDA_TRY(cudaEventCreateWithFlags(&ev_chg[1], cudaEventDisableTiming));
+  struct EvGuard { cudaEvent_t* e; ~EvGuard() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); } } ev_guard{ev_chg};
+  SC_TRY(b_misc.ensure(64, s));
   int32_t* lab = b_lab.as<int32_t>();
   int32_t* nw = b_new.as<int32_t>();
   double* C = b_C.as<double>();
   int* changed = b_misc.as<int>();
-  int64_t* sel = reinterpret_cast<int64_t*>(b_misc.as<char>() + 16);
   unsigned* absmax = reinterpret_cast<unsigned*>(b_misc.as<char>() + 32);
 
   // fixed-point scale from the largest |feature|
@@ -539,15 +618,18 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   const int shift = 100 - E;   // |x| 2^shift < 2^100; sums of < 2^25 members fit 2^125
 
   SC_CUDA_TRY(cudaFuncSetAttribute(assign3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
-  std::vector<unsigned> cnt_h(k);
 
   // Lloyd assignment of every point; host receives inertia (fixed-order sum of block
   // partials), the number of changed labels and the label histogram
   // Hamerly pruning pays off when a full assignment is expensive; small problems (many of
   // them in a stability scan) are launch-bound and take the plain full scan
   const bool prune = (double)n * k * d >= 134217728.0;
-  auto assign_all = [&](int32_t* out_lab, const int32_t* old, double* inertia, int* nchanged) -> int {
-    SC_CUDA_TRY(cudaMemsetAsync(changed, 0, sizeof(int), s));
+  // Lloyd assignment of every point, no host synchronisation: labels, exact dmin, the
+  // number of changed labels into changed_dev[slot] and the label histogram (device);
+  // block partials of the inertia in b_part
+  int* changed_dev = b_chg.as<int>();
+  auto assign_all = [&](int32_t* out_lab, const int32_t* old, int slot) -> int {
+    SC_CUDA_TRY(cudaMemsetAsync(changed_dev + slot, 0, sizeof(int), s));
     SC_CUDA_TRY(cudaMemsetAsync(b_cnt.ptr, 0, sizeof(unsigned) * k, s));
     if (!old || !prune) {
       // full scan of every point (the first assignment of a restart also sets the bounds lo)
@@ -565,71 +647,49 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
     }
     SC_CUDA_TRY(cudaGetLastError());
     assign_stats_kernel<<<(unsigned)nstat, 256, 0, s>>>(out_lab, old, b_dmin.as<double>(), n, b_part.as<double>(),
-                                                       changed, b_cnt.as<unsigned>());
+                                                       changed_dev + slot, b_cnt.as<unsigned>());
     SC_CUDA_TRY(cudaGetLastError());
+    return SC_OK;
+  };
+  auto read_inertia = [&](double* inertia) -> int {
     std::vector<double> part(nstat);
-    int h_changed = 0;
     SC_CUDA_TRY(cudaMemcpyAsync(part.data(), b_part.as<double>(), sizeof(double) * nstat, cudaMemcpyDeviceToHost, s));
-    SC_CUDA_TRY(cudaMemcpyAsync(&h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s));
-    SC_CUDA_TRY(cudaMemcpyAsync(cnt_h.data(), b_cnt.ptr, sizeof(unsigned) * k, cudaMemcpyDeviceToHost, s));
     SC_CUDA_TRY(cudaStreamSynchronize(s));
     double tot = 0.0;
-    for (double v : part) tot += v;
+    for (double v : part) tot += v;   // fixed order: deterministic
     *inertia = tot;
-    *nchanged = h_changed;
     return SC_OK;
   };
 
-  // centroids <- member means of the labels `cur` (histogram in cnt_h): members grouped by
-  // cluster (counting sort), exact 128-bit fixed-point member sums, one rounding
-  std::vector<int64_t> off_h(k + 1), ws_h, we_h;
-  std::vector<int32_t> item0_h(k), nitems_h(k);
+  // centroids <- member means of the labels `cur` (histogram on the device): members grouped
+  // by cluster (counting sort), exact 128-bit fixed-point member sums, one rounding
+  int64_t* d_off = b_off.as<int64_t>();
+  int64_t* d_ws = b_items.as<int64_t>();
+  int64_t* d_we = d_ws + max_items;
+  int32_t* d_item0 = reinterpret_cast<int32_t*>(d_we + max_items);
+  int32_t* d_nitems = d_item0 + k;
+  int* d_total = b_len.as<int>() + 1;
   auto update = [&](const int32_t* cur) -> int {
     if (prune) SC_CUDA_TRY(cudaMemcpyAsync(b_Cold.ptr, C, sizeof(double) * k * d, cudaMemcpyDeviceToDevice, s));
-    off_h[0] = 0;
-    for (int c = 0; c < k; ++c) off_h[c + 1] = off_h[c] + cnt_h[c];
-    ws_h.clear();
-    we_h.clear();
-    for (int c = 0; c < k; ++c) {
-      item0_h[c] = (int32_t)ws_h.size();
-      for (int64_t a = off_h[c]; a < off_h[c + 1]; a += kChunk) {
-        ws_h.push_back(a);
-        we_h.push_back(std::min(off_h[c + 1], a + kChunk));
-      }
-      nitems_h[c] = (int32_t)ws_h.size() - item0_h[c];
-    }
-    const int64_t items = (int64_t)ws_h.size();
-    int64_t* d_ws = b_items.as<int64_t>();
-    int64_t* d_we = d_ws + max_items;
-    int32_t* d_item0 = reinterpret_cast<int32_t*>(d_we + max_items);
-    int32_t* d_nitems = d_item0 + k;
-    SC_CUDA_TRY(cudaMemcpyAsync(b_off.ptr, off_h.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice, s));
-    if (items) {
-      SC_CUDA_TRY(cudaMemcpyAsync(d_ws, ws_h.data(), sizeof(int64_t) * items, cudaMemcpyHostToDevice, s));
-      SC_CUDA_TRY(cudaMemcpyAsync(d_we, we_h.data(), sizeof(int64_t) * items, cudaMemcpyHostToDevice, s));
-    }
-    SC_CUDA_TRY(cudaMemcpyAsync(d_item0, item0_h.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
-    SC_CUDA_TRY(cudaMemcpyAsync(d_nitems, nitems_h.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
+    plan_members_kernel<<<1, 32, 0, s>>>(b_cnt.as<unsigned>(), k, kChunk, d_off, d_ws, d_we, d_item0, d_nitems,
+                                         d_total);
+    SC_CUDA_TRY(cudaGetLastError());
     SC_CUDA_TRY(cudaMemsetAsync(b_cur.ptr, 0, sizeof(unsigned) * k, s));
     if (k <= 6144) {
       const int64_t per_block = std::max<int64_t>(4096, (n + grid - 1) / grid);
       scatter_members_kernel<<<(unsigned)((n + per_block - 1) / per_block), kB, sizeof(unsigned) * 2 * k, s>>>(
-          cur, n, k, per_block, b_cur.as<unsigned>(), b_off.as<int64_t>(), b_perm.as<int32_t>());
+          cur, n, k, per_block, b_cur.as<unsigned>(), d_off, b_perm.as<int32_t>());
     } else {
-      scatter_members_simple_kernel<<<grid, kB, 0, s>>>(cur, n, b_cur.as<unsigned>(), b_off.as<int64_t>(),
-                                                        b_perm.as<int32_t>());
+      scatter_members_simple_kernel<<<grid, kB, 0, s>>>(cur, n, b_cur.as<unsigned>(), d_off, b_perm.as<int32_t>());
     }
     SC_CUDA_TRY(cudaGetLastError());
-    if (items) {
-      const int slots = std::max(1, 256 / d);
-      member_sum_kernel<<<(unsigned)items, slots * d, sizeof(unsigned long long) * 2 * slots * d, s>>>(
-          F, d, b_perm.as<int32_t>(), d_ws, d_we, shift, b_psum.as<unsigned long long>());
-      SC_CUDA_TRY(cudaGetLastError());
-    }
+    const int slots = std::max(1, 256 / d);
+    member_sum_kernel<<<(unsigned)max_items, slots * d, sizeof(unsigned long long) * 2 * slots * d, s>>>(
+        F, d, b_perm.as<int32_t>(), d_ws, d_we, d_total, shift, b_psum.as<unsigned long long>());
+    SC_CUDA_TRY(cudaGetLastError());
     member_finalize_kernel<<<std::max(1, std::min(grid, (k * d + kB - 1) / kB)), kB, 0, s>>>(
         b_psum.as<unsigned long long>(), d_item0, d_nitems, b_cnt.as<unsigned>(), k, d, shift, C);
     SC_CUDA_TRY(cudaGetLastError());
-    // the histogram buffer is reused by the next assignment only after this finalize (stream order)
     if (prune) {
       centroid_shift_kernel<<<1, 256, 0, s>>>(C, b_Cold.as<double>(), k, d, b_dmax.as<double>());
       SC_CUDA_TRY(cudaGetLastError());
@@ -641,7 +701,6 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   int best_r = -1, best_it = 0;
   std::vector<double> best_C((size_t)k * d);
   std::vector<double> u(k);
-  std::vector<double> bsum(G), prefix(G + 1);
   const bool trace = std::getenv("SC_KMEANS_TRACE") != nullptr;
   auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   double t_seed = 0.0, t_lloyd = 0.0, t_mark = now();
@@ -649,46 +708,45 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
     if (trace) t_mark = now();
     for (int t = 0; t < k; ++t)
       u[t] = uniforms_host ? uniforms_host[(size_t)r * k + t] : uniform_host(seed, 1, (uint64_t)r * k + t);
-    // ---- k-means++ seeding
+    // ---- k-means++ seeding (device-resident: block sums, then one selection kernel per draw)
     int64_t idx = std::min<int64_t>((int64_t)std::floor(u[0] * n), n - 1);
     row_to_centroid_kernel<<<1, 128, 0, s>>>(F, idx, d, C);
     d2_update_kernel<<<grid, kB, sizeof(double) * d, s>>>(F, n, d, C, b_d2.as<double>(), 1);
     SC_CUDA_TRY(cudaGetLastError());
     for (int t = 1; t < k; ++t) {
       range_sums_kernel<<<G, kB, 0, s>>>(b_d2.as<double>(), n, chunk, b_part.as<double>());
-      SC_CUDA_TRY(cudaMemcpyAsync(bsum.data(), b_part.as<double>(), sizeof(double) * G, cudaMemcpyDeviceToHost, s));
-      SC_CUDA_TRY(cudaStreamSynchronize(s));
-      prefix[0] = 0.0;
-      for (int b = 0; b < G; ++b) prefix[b + 1] = prefix[b] + bsum[b];
-      const double total = prefix[G];
-      if (!(total > 0.0)) {
-        idx = std::min<int64_t>((int64_t)std::floor(u[t] * n), n - 1);
-      } else {
-        const double target = u[t] * total;
-        int b = 0;
-        while (b < G - 1 && !(prefix[b + 1] > target)) ++b;
-        const int64_t b0 = (int64_t)b * chunk, b1 = std::min<int64_t>(n, b0 + chunk);
-        range_select_kernel<<<1, 32, 0, s>>>(b_d2.as<double>(), b0, b1, prefix[b], target, sel);
-        SC_CUDA_TRY(cudaMemcpyAsync(&idx, sel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        SC_CUDA_TRY(cudaStreamSynchronize(s));
-      }
-      row_to_centroid_kernel<<<1, 128, 0, s>>>(F, idx, d, C + (size_t)t * d);
+      seed_select_kernel<<<1, 32, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk, u[t], F, d,
+                                          C + (size_t)t * d);
       d2_update_kernel<<<grid, kB, sizeof(double) * d, s>>>(F, n, d, C + (size_t)t * d, b_d2.as<double>(), 0);
       SC_CUDA_TRY(cudaGetLastError());
     }
-    // ---- Lloyd
+    // ---- Lloyd.  Iterations are issued without waiting; the changed-label count of
+    // iteration it-1 is read (pinned copy + event) while iteration it runs.  Once an
+    // assignment repeats, further iterations are idempotent (same labels -> same exact
+    // means -> same labels), so the one issued speculatively changes nothing but time.
     if (trace) { SC_CUDA_TRY(cudaStreamSynchronize(s)); t_seed += now() - t_mark; t_mark = now(); }
-    double inertia = 0.0;
-    int nchg = 0;
-    SC_TRY(assign_all(lab, nullptr, &inertia, &nchg));
-    int it = 0;
+    SC_TRY(assign_all(lab, nullptr, 0));
+    int it = 0, conv = -1;
     for (it = 1; it <= max_iter; ++it) {
       SC_TRY(update(lab));
-      SC_TRY(assign_all(nw, lab, &inertia, &nchg));
-      if (nchg == 0) break;
+      SC_TRY(assign_all(nw, lab, it));
+      SC_CUDA_TRY(cudaMemcpyAsync(h_chg + it, changed_dev + it, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SC_CUDA_TRY(cudaEventRecord(ev_chg[it & 1], s));
       std::swap(lab, nw);
+      if (it >= 2) {
+        SC_CUDA_TRY(cudaEventSynchronize(ev_chg[(it - 1) & 1]));
+        if (h_chg[it - 1] == 0) { conv = it - 1; break; }
+      }
     }
-    if (it > max_iter) it = max_iter;
+    if (conv < 0) {
+      SC_CUDA_TRY(cudaStreamSynchronize(s));
+      const int last = std::min(it, max_iter);
+      conv = h_chg[last] == 0 ? last : max_iter;
+      // (a run that never converges ends at max_iter, like the oracle)
+    }
+    it = conv;
+    double inertia = 0.0;
+    SC_TRY(read_inertia(&inertia));
     if (trace) {
       t_lloyd += now() - t_mark;
       std::fprintf(stderr, "[sc_kmeans] restart %d: seeding %.4f s, lloyd %.4f s (%d iters)\n", r, t_seed, t_lloyd, it);

@@ -11,8 +11,12 @@
 // reading the T_m stack once per group of 8 cuts.  k-means and the ARI are the
 // library's own kernels.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "sc_internal.cuh"
@@ -105,65 +109,115 @@ int stability_scan(sc_graph* g, int k_min, int k_max, int J, int R, int order, b
   SC_TRY(dD.ensure(sizeof(float) * D.size()));
   SC_CUDA_TRY(cudaMemcpyAsync(dD.ptr, D.data(), sizeof(float) * D.size(), cudaMemcpyHostToDevice, s));
 
-  // 3. buffers: T stack (ld = R rounded up to 4), features of every cut, signals
+  // 3. buffers: T stack (ld = R rounded up to 4), the features of every cut for a group of
+  // replicates (as many as fit half of the free memory), signals
   const int ld = (R + 3) / 4 * 4;
   const int64_t slot = n * ld;
+  const size_t per_rep = sizeof(float) * (size_t)K * n * R;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t tall_bytes = sizeof(float) * (size_t)slot * nterms;
+  const size_t budget = free_b > tall_bytes ? (free_b - tall_bytes) / 2 : 0;
+  const int Jg = (int)std::max<size_t>(1, std::min<size_t>((size_t)J, budget / std::max<size_t>(per_rep, 1)));
   DevBuf tall, yall, sig;
-  SC_TRY(tall.ensure(sizeof(float) * (size_t)slot * nterms));
-  SC_TRY(yall.ensure(sizeof(float) * (size_t)K * n * R));
+  SC_TRY(tall.ensure(tall_bytes));
+  SC_TRY(yall.ensure(per_rep * Jg));
   if (ld != R) SC_TRY(sig.ensure(sizeof(float) * n * R));
   float* T = tall.as<float>();
   const std::vector<int> chunks = chunk_widths<float>(ld, n);
   const int grid = g->num_sms * 8;
+  int dev = 0;
+  cudaGetDevice(&dev);
 
-  for (int j = 0; j < J; ++j) {
-    const uint64_t sj = seed + (uint64_t)j;
-    // T_0 = X_j (§4.1 step 4: N(0, 1/R) entries)
-    if (ld == R) {
-      SC_TRY(random_signals<float>(n, R, 0, sj, 0, 1.0 / R, T, s));
-    } else {
-      SC_TRY(random_signals<float>(n, R, 0, sj, 0, 1.0 / R, sig.as<float>(), s));
-      pad_copy_kernel<<<grid, 256, 0, s>>>(sig.as<float>(), n, R, T, ld);
-      SC_CUDA_TRY(cudaGetLastError());
-    }
-    // T_{m+1} = 2 L~ T_m - T_{m-1}  (T_1 = L~ T_0), every term kept
-    for (int st = 0; st < order; ++st) {
-      int col0 = 0;
-      for (int w : chunks) {
-        StepParams p{};
-        p.row_begin = 0;
-        p.row_end = n;
-        p.width = w;
-        p.total_width = ld;
-        p.tcur = T + (size_t)st * slot + col0;
-        p.ld_cur = ld;
-        p.tprev = st == 0 ? nullptr : (const void*)(T + (size_t)(st - 1) * slot + col0);
-        p.ld_prev = ld;
-        p.tnext = T + (size_t)(st + 1) * slot + col0;
-        p.ld_next = ld;
-        p.a = (st == 0 ? 2.0 : 4.0) / lambda_max;
-        p.b_cur = st == 0 ? -1.0 : -2.0;
-        p.b_prev = st == 0 ? 0.0 : -1.0;
-        p.y_mode = 0;
-        SC_TRY(launch_step<float>(g, p, s));
-        col0 += w;
+  for (int j0 = 0; j0 < J; j0 += Jg) {
+    const int jn = std::min(Jg, J - j0);
+    // 3a. recurrence + every cut's features for replicates j0 .. j0+jn-1 (stream s)
+    for (int jj = 0; jj < jn; ++jj) {
+      const uint64_t sj = seed + (uint64_t)(j0 + jj);
+      // T_0 = X_j (§4.1 step 4: N(0, 1/R) entries)
+      if (ld == R) {
+        SC_TRY(random_signals<float>(n, R, 0, sj, 0, 1.0 / R, T, s));
+      } else {
+        SC_TRY(random_signals<float>(n, R, 0, sj, 0, 1.0 / R, sig.as<float>(), s));
+        pad_copy_kernel<<<grid, 256, 0, s>>>(sig.as<float>(), n, R, T, ld);
+        SC_CUDA_TRY(cudaGetLastError());
+      }
+      // T_{m+1} = 2 L~ T_m - T_{m-1}  (T_1 = L~ T_0), every term kept
+      for (int st = 0; st < order; ++st) {
+        int col0 = 0;
+        for (int w : chunks) {
+          StepParams p{};
+          p.row_begin = 0;
+          p.row_end = n;
+          p.width = w;
+          p.total_width = ld;
+          p.tcur = T + (size_t)st * slot + col0;
+          p.ld_cur = ld;
+          p.tprev = st == 0 ? nullptr : (const void*)(T + (size_t)(st - 1) * slot + col0);
+          p.ld_prev = ld;
+          p.tnext = T + (size_t)(st + 1) * slot + col0;
+          p.ld_next = ld;
+          p.a = (st == 0 ? 2.0 : 4.0) / lambda_max;
+          p.b_cur = st == 0 ? -1.0 : -2.0;
+          p.b_prev = st == 0 ? 0.0 : -1.0;
+          p.y_mode = 0;
+          SC_TRY(launch_step<float>(g, p, s));
+          col0 += w;
+        }
+      }
+      // Y_k for every cut
+      float* yj = yall.as<float>() + (size_t)jj * K * n * R;
+      for (int c0 = 0; c0 < K; c0 += kKG) {
+        const int kg = std::min(kKG, K - c0);
+        combine_cuts_kernel<<<grid, 256, sizeof(float) * kg * nterms, s>>>(
+            T, slot, nterms, n, R, ld, dD.as<float>() + (size_t)c0 * nterms, kg, yj + (size_t)c0 * n * R, n * R);
+        SC_CUDA_TRY(cudaGetLastError());
       }
     }
-    // Y_k for every cut
-    for (int c0 = 0; c0 < K; c0 += kKG) {
-      const int kg = std::min(kKG, K - c0);
-      combine_cuts_kernel<<<grid, 256, sizeof(float) * kg * nterms, s>>>(
-          T, slot, nterms, n, R, ld, dD.as<float>() + (size_t)c0 * nterms, kg,
-          yall.as<float>() + (size_t)c0 * n * R, n * R);
-      SC_CUDA_TRY(cudaGetLastError());
-    }
-    // k-means per cut (§4.1 step 6), replicate seed sj
-    for (int c = 0; c < K; ++c) {
-      double inertia = 0.0;
-      int it = 0, best = 0;
-      SC_TRY(kmeans_run(yall.as<float>() + (size_t)c * n * R, n, R, k_min + c, restarts, max_iter, sj, nullptr,
-                        labels_dev + ((size_t)c * J + j) * n, nullptr, &inertia, &it, &best, s));
-    }
+    cudaEvent_t ready;
+    SC_CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    SC_CUDA_TRY(cudaEventRecord(ready, s));
+    // 3b. the jn*K k-means problems (§4.1 step 6; replicate seed seed+j) are
+    // independent and individually too small to fill the GPU: worker threads, each with its
+    // own stream and stream-ordered workspaces, run them concurrently
+    const int ntask = jn * K;
+    const int nwork = std::min(ntask, 8);
+    std::atomic<int> next{0};
+    std::mutex err_mu;
+    int err_code = SC_OK;
+    std::string err_msg;
+    auto worker = [&]() {
+      cudaSetDevice(dev);
+      cudaStream_t ws = nullptr;
+      if (cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaStreamWaitEvent(ws, ready, 0) != cudaSuccess) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (err_code == SC_OK) { err_code = SC_ERR_CUDA; err_msg = "worker stream creation failed"; }
+        if (ws) cudaStreamDestroy(ws);
+        return;
+      }
+      for (int t = next++; t < ntask; t = next++) {
+        const int jj = t / K, c = t - jj * K;
+        const int j = j0 + jj;
+        double inertia = 0.0;
+        int it = 0, best = 0;
+        const int rc = kmeans_run(yall.as<float>() + ((size_t)jj * K + c) * n * R, n, R, k_min + c, restarts,
+                                  max_iter, seed + (uint64_t)j, nullptr, labels_dev + ((size_t)c * J + j) * n,
+                                  nullptr, &inertia, &it, &best, ws);
+        if (rc != SC_OK) {
+          std::lock_guard<std::mutex> lk(err_mu);
+          if (err_code == SC_OK) { err_code = rc; err_msg = sc_last_error(); }
+          break;
+        }
+      }
+      cudaStreamSynchronize(ws);
+      cudaStreamDestroy(ws);
+    };
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nwork; ++w) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    cudaEventDestroy(ready);
+    if (err_code != SC_OK) return fail(err_code, "sc_stability k-means worker: " + err_msg);
   }
   // 4. gamma(k) = 2/(J(J-1)) sum_{a<b} ari(C^a, C^b)   (R7)
   for (int c = 0; c < K; ++c) {
