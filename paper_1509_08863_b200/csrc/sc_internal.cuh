@@ -80,8 +80,11 @@ struct PoolBuf {
   PoolBuf() = default;
   PoolBuf(const PoolBuf&) = delete;
   PoolBuf& operator=(const PoolBuf&) = delete;
-  ~PoolBuf() {
+  ~PoolBuf() { release(); }
+  void release() {   // before the owning stream is destroyed
     if (ptr) cudaFreeAsync(ptr, st);
+    ptr = nullptr;
+    bytes = 0;
   }
   int ensure(size_t b, cudaStream_t s) {
     if (b <= bytes && ptr) return SC_OK;

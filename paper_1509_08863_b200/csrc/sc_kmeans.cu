@@ -18,6 +18,8 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "sc_internal.cuh"
@@ -541,9 +543,20 @@ int normalize_rows_f32(float* F, int64_t n, int d, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 // k-means driver
 // ---------------------------------------------------------------------------
-int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_iter, uint64_t seed,
-               const double* uniforms_host, int32_t* labels_dev, double* centroids_host, double* inertia_out,
-               int* iters_out, int* best_out, cudaStream_t s) {
+namespace {
+struct KmResult {
+  double inertia = INFINITY;
+  int iters = 0;
+  int r = -1;
+  std::vector<double> C;
+};
+}  // namespace
+
+// Restarts r0, r0 + rstep, ... < restarts on stream s; the best of them (lowest inertia,
+// ties -> lowest r) goes to *res and its labels to labels_dev.
+static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rstep, int restarts, int max_iter,
+                         uint64_t seed, const double* uniforms_host, int32_t* labels_dev, KmResult* res,
+                         cudaStream_t s) {
   const int sms = num_sms_current();
   const int grid = sms * 8;
   const int G = sms * 2;                                  // k-means++ range blocks
@@ -704,7 +717,7 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   const bool trace = std::getenv("SC_KMEANS_TRACE") != nullptr;
   auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   double t_seed = 0.0, t_lloyd = 0.0, t_mark = now();
-  for (int r = 0; r < restarts; ++r) {
+  for (int r = r0; r < restarts; r += rstep) {
     if (trace) t_mark = now();
     for (int t = 0; t < k; ++t)
       u[t] = uniforms_host ? uniforms_host[(size_t)r * k + t] : uniform_host(seed, 1, (uint64_t)r * k + t);
@@ -760,11 +773,85 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
       SC_CUDA_TRY(cudaStreamSynchronize(s));
     }
   }
-  if (best_r < 0) return fail(SC_ERR_ARG, "k-means produced no finite inertia");
-  if (centroids_host) std::memcpy(centroids_host, best_C.data(), sizeof(double) * k * d);
-  if (inertia_out) *inertia_out = best_inertia;
-  if (iters_out) *iters_out = best_it;
-  if (best_out) *best_out = best_r;
+  res->inertia = best_inertia;
+  res->iters = best_it;
+  res->r = best_r;
+  res->C = best_C;
+  return SC_OK;
+}
+
+int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_iter, uint64_t seed,
+               const double* uniforms_host, int32_t* labels_dev, double* centroids_host, double* inertia_out,
+               int* iters_out, int* best_out, cudaStream_t s) {
+  // Restarts are independent: large problems run them on up to 4 worker threads, each with
+  // its own stream and stream-ordered workspace (the pruned Lloyd phase and the k-means++
+  // draws are latency-bound, so concurrent restarts overlap); the winner is the same as in
+  // a sequential loop (lowest inertia, ties -> lowest restart index).
+  const int P = (restarts > 1 && (double)n * d >= 4.0e6) ? std::min(restarts, 4) : 1;
+  std::vector<KmResult> res(P);
+  if (P == 1) {
+    SC_TRY(kmeans_worker(F, n, d, k, 0, 1, restarts, max_iter, seed, uniforms_host, labels_dev, &res[0], s));
+  } else {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaEvent_t ready;
+    SC_CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    SC_CUDA_TRY(cudaEventRecord(ready, s));
+    std::vector<PoolBuf> labs(P);
+    std::vector<cudaStream_t> streams(P, nullptr);
+    std::vector<int> rcs(P, SC_OK);
+    std::vector<std::string> msgs(P);
+    std::vector<std::thread> pool;
+    for (int w = 0; w < P; ++w) {
+      pool.emplace_back([&, w]() {
+        cudaSetDevice(dev);
+        if (cudaStreamCreateWithFlags(&streams[w], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamWaitEvent(streams[w], ready, 0) != cudaSuccess) {
+          rcs[w] = SC_ERR_CUDA;
+          msgs[w] = "worker stream creation failed";
+          return;
+        }
+        int rc = labs[w].ensure(sizeof(int32_t) * n, streams[w]);
+        if (rc == SC_OK)
+          rc = kmeans_worker(F, n, d, k, w, P, restarts, max_iter, seed, uniforms_host, labs[w].as<int32_t>(),
+                             &res[w], streams[w]);
+        if (rc != SC_OK) {
+          rcs[w] = rc;
+          msgs[w] = sc_last_error();
+        }
+        cudaStreamSynchronize(streams[w]);
+      });
+    }
+    for (auto& th : pool) th.join();
+    cudaEventDestroy(ready);
+    int win = -1;
+    for (int w = 0; w < P; ++w) {
+      if (rcs[w] != SC_OK) {
+        for (int v = 0; v < P; ++v) {
+          labs[v].release();
+          if (streams[v]) cudaStreamDestroy(streams[v]);
+        }
+        return fail(rcs[w], "sc_kmeans worker: " + msgs[w]);
+      }
+      if (res[w].r >= 0 && (win < 0 || res[w].inertia < res[win].inertia ||
+                            (res[w].inertia == res[win].inertia && res[w].r < res[win].r)))
+        win = w;
+    }
+    if (win >= 0)
+      SC_CUDA_TRY(cudaMemcpyAsync(labels_dev, labs[win].ptr, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int w = 0; w < P; ++w) {
+      labs[w].release();
+      cudaStreamDestroy(streams[w]);
+    }
+    if (win > 0) std::swap(res[0], res[win]);
+    else if (win < 0) res[0].r = -1;
+  }
+  if (res[0].r < 0) return fail(SC_ERR_ARG, "k-means produced no finite inertia");
+  if (centroids_host) std::memcpy(centroids_host, res[0].C.data(), sizeof(double) * k * d);
+  if (inertia_out) *inertia_out = res[0].inertia;
+  if (iters_out) *iters_out = res[0].iters;
+  if (best_out) *best_out = res[0].r;
   return SC_OK;
 }
 

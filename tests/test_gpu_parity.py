@@ -367,15 +367,18 @@ def _features(seed, n, k, d, spread):
     return (C[lab] + spread * rng.standard_normal((n, d))).astype(np.float32)
 
 
-@pytest.mark.parametrize("n,k,d,spread,restarts", [(2000, 5, 32, 0.3, 10), (20000, 10, 24, 0.8, 3),
-                                                   (5000, 20, 48, 1.5, 2), (3001, 7, 5, 0.5, 4)])
-def test_kmeans_bit_exact(sc, n, k, d, spread, restarts):
+@pytest.mark.parametrize("n,k,d,spread,restarts,max_iter", [
+    (2000, 5, 32, 0.3, 10, 100), (20000, 10, 24, 0.8, 3, 100), (5000, 20, 48, 1.5, 2, 100), (3001, 7, 5, 0.5, 4, 100),
+    # n*d >= 4e6 and n*k*d >= 2^27: concurrent restarts on worker streams + Hamerly pruning
+    # (iterations capped so the fp64 oracle stays within ~a minute)
+    pytest.param(90000, 32, 48, 1.0, 2, 12, marks=pytest.mark.slow)])
+def test_kmeans_bit_exact(sc, n, k, d, spread, restarts, max_iter):
     X = _features(n + k, n, k, d, spread)
     u = np.stack([scinputs.uniforms(7, k, offset=k * r) for r in range(restarts)])
     lab = torch.empty(n, dtype=torch.int32, device="cuda")
     C = np.zeros((k, d), dtype=np.float64)
-    inertia, it, best = sc.sc_kmeans(torch.from_numpy(X).cuda(), n, d, k, restarts, 100, 0, u, lab, C)
-    lo, Co, io, ito, ro, _ = kmeans.kmeans(X, k, u, 100)
+    inertia, it, best = sc.sc_kmeans(torch.from_numpy(X).cuda(), n, d, k, restarts, max_iter, 0, u, lab, C)
+    lo, Co, io, ito, ro, _ = kmeans.kmeans(X, k, u, max_iter)
     assert np.array_equal(lab.cpu().numpy(), lo)
     assert np.array_equal(C, Co)             # exactly rounded member sums -> identical centroids
     assert best == ro and it == ito
