@@ -210,9 +210,9 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
                  const uint16_t* __restrict__ order, StepParams p, int cap, int nstages) {
   constexpr int W = Vec<T>::W;
   constexpr int SW = VPR;          // lanes per row (one 16-byte vector each)
-  constexpr int RPW = 32 / SW;     // rows per warp
+  constexpr int RPW = 32 / SW;     // rows per warp (lanes >= RPW*SW idle when SW does not divide 32)
   constexpr int TR = tile_rows(VPR);
-  static_assert(VPR >= 1 && VPR <= 32 && 32 % VPR == 0, "VPR must divide 32");
+  static_assert(VPR >= 1 && VPR <= 32, "VPR in [1, 32]");
 
   extern __shared__ __align__(128) unsigned char smem[];
   const SmemLayout lay(TR, cap, UNIT, nstages);
@@ -317,7 +317,7 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
     // the block index rotating with the tile so every warp sees every degree class
     const uint16_t* ord = reinterpret_cast<const uint16_t*>(st + lay.ord_off);
     const int rank = ((warp + static_cast<int>(t % kNC)) % kNC) * RPW + sub;
-    const bool valid = rank < static_cast<int>(m.r1 - m.r0);
+    const bool valid = sub < RPW && rank < static_cast<int>(m.r1 - m.r0);
     const int64_t row = m.r0 + (valid ? ord[rank] : 0);
     int deg = 0;
     int64_t b = 0;
@@ -331,9 +331,9 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
       if (tprev) cp_async16(d_prv, tprev + row * p.ld_prev + c, pol_stream);
       if (p.y_mode == 2) cp_async16(d_y, y + row * p.ld_y + c, pol_stream);
     }
-    int maxdeg = deg;
+    int maxdeg = deg;   // over the warp's rows (an upper bound of each row's degree)
 #pragma unroll
-    for (int o = SW; o < 32; o <<= 1) maxdeg = max(maxdeg, __shfl_xor_sync(FULL, maxdeg, o));
+    for (int o = 16; o > 0; o >>= 1) maxdeg = max(maxdeg, __shfl_xor_sync(FULL, maxdeg, o));
 
     // Rolling window of EB gathers: slot e always holds the load of edge base+e; consuming it
     // (scoreboard wait on that load only) is immediately followed by issuing edge base+EB+e,
@@ -539,9 +539,13 @@ KernelFn<T> pick_vpr(int vpr, bool unit) {
   switch (vpr) {
     case 1: return pick_unit<T, 1, EB, MOM>(unit);
     case 2: return pick_unit<T, 2, EB, MOM>(unit);
+    case 3: return pick_unit<T, 3, EB, MOM>(unit);
     case 4: return pick_unit<T, 4, EB, MOM>(unit);
+    case 6: return pick_unit<T, 6, EB, MOM>(unit);
     case 8: return pick_unit<T, 8, EB, MOM>(unit);
+    case 12: return pick_unit<T, 12, EB, MOM>(unit);
     case 16: return pick_unit<T, 16, EB, MOM>(unit);
+    case 24: return pick_unit<T, 24, EB, MOM>(unit);
     case 32: return pick_unit<T, 32, EB, MOM>(unit);
     default: return nullptr;
   }
@@ -642,30 +646,37 @@ int launch_step_impl(const sc_graph* g, const StepParams& p, cudaStream_t s, boo
 }
 
 // Split R columns into chunks of supported widths, each <= cw.
+// Row widths (in 16-byte vectors) the kernels are instantiated for.
+constexpr int kVprSet[] = {32, 24, 16, 12, 8, 6, 4, 3, 2, 1};
+
+// Split R columns (a multiple of the vector width) into chunks of supported widths, each
+// at most cw.
 template <typename T>
 std::vector<int> chunk_plan(int R, int64_t n_cols) {
   constexpr int W = Vec<T>::W;
-  const int maxw = 32 * W;   // one warp per row
-  int cw = env_int("SC_CHUNK", 0);
-  if (cw <= 0) {
-    // Keep the gathered chunk of T_s L2-resident: the widest power of two whose N x w block
+  const int maxv = 32;   // one warp per row
+  int cv = env_int("SC_CHUNK", 0) / W;
+  if (cv <= 0) {
+    // Keep the gathered chunk of T_s L2-resident: the widest supported row whose N x w block
     // fits the budget.  If that would take rows narrower than 128 bytes, the block cannot be
-    // L2-resident at a useful row size anyway: use the widest chunk (fewest CSR re-reads,
-    // largest DRAM requests; profiles/r01_gather_probe.txt).
+    // L2-resident at a useful row size anyway: use 256-byte rows (large DRAM requests, half
+    // the CSR re-reads of 128-byte rows; measured on configs[4]: 64 + 32 columns 3.88 s,
+    // one 96-column chunk 4.09 s, one padded 128-column chunk 5.09 s per pass).
     const double budget = env_int("SC_L2_BUDGET_MB", 128) * 1048576.0;
-    cw = maxw;
-    while (cw > W && (double)n_cols * cw * sizeof(T) > budget) cw >>= 1;
-    if (cw * (int)sizeof(T) < 128) cw = maxw;
+    cv = 1;
+    for (int v : kVprSet)
+      if ((double)n_cols * v * 16 <= budget) { cv = v; break; }
+    if (cv * 16 < 128) cv = 16;
   }
-  cw = std::max(W, std::min(cw, maxw));
+  cv = std::max(1, std::min(cv, maxv));
   std::vector<int> out;
-  int rem = R;
+  int rem = R / W;
   while (rem > 0) {
-    int w = maxw;
-    while (w > W && (w > rem || w > cw)) w >>= 1;
-    if (w > rem) w = rem;   // only when rem < W (caller pads, so never)
-    out.push_back(w);
-    rem -= w;
+    int v = 1;
+    for (int c : kVprSet)
+      if (c <= rem && c <= cv) { v = c; break; }
+    out.push_back(v * W);
+    rem -= v;
   }
   return out;
 }
@@ -762,11 +773,14 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
   // (small graphs are launch-bound).
   int Rp = (R + W - 1) / W * W;
   {
-    int p2 = W;
-    while (p2 < Rp) p2 <<= 1;
+    // smallest supported width >= Rp
+    int pv = 32;
+    for (int v : kVprSet)
+      if (v * W >= Rp) pv = v;
+    const int p2 = pv * W;
     const std::vector<int> one = chunk_plan<T>(p2, g->n_cols);
     const bool resident = (double)g->n_cols * p2 * sizeof(T) <= env_int("SC_L2_BUDGET_MB", 128) * 1048576.0;
-    if (p2 != Rp && resident && one.size() == 1 && chunk_plan<T>(Rp, g->n_cols).size() > 1) Rp = p2;
+    if (p2 > Rp && resident && one.size() == 1 && chunk_plan<T>(Rp, g->n_cols).size() > 1) Rp = p2;
   }
   const bool aligned = (Rp == R) && ((uintptr_t)X % 16 == 0) && ((uintptr_t)Y % 16 == 0);
   const T* Xw = X;

@@ -142,7 +142,7 @@ cheb_resident_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restr
       const int rank = wslot * RPW + sub;
       const int64_t tile_r0 = (t0 + tl) * rp.tr;
       const int rows_in_tile = static_cast<int>(min((int64_t)rp.tr, rp.n - tile_r0));
-      const bool valid = rank < rows_in_tile;
+      const bool valid = sub < RPW && rank < rows_in_tile;
       const int lrow = static_cast<int>(tile_r0 - r0) + (valid ? s_ord[tl * rp.tr + rank] : 0);
       const int64_t row = r0 + lrow;
       int deg = 0, b = 0;
@@ -153,9 +153,9 @@ cheb_resident_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restr
         if (tprev) cp_async16_r(d_prv, tprev + row * ld_prev + c);
         if (cf.y_mode == 2) cp_async16_r(d_y, y + row * rp.ld_y + c);
       }
-      int maxdeg = deg;
+      int maxdeg = deg;   // over the warp's rows
 #pragma unroll
-      for (int o = SW; o < 32; o <<= 1) maxdeg = max(maxdeg, __shfl_xor_sync(FULLM, maxdeg, o));
+      for (int o = 16; o > 0; o >>= 1) maxdeg = max(maxdeg, __shfl_xor_sync(FULLM, maxdeg, o));
       T acc[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) acc[w] = T(0);
@@ -236,9 +236,13 @@ RKernel<T> pick_r(int vpr, bool unit) {
   switch (vpr) {
     case 1: return pick_r2<T, 1>(unit);
     case 2: return pick_r2<T, 2>(unit);
+    case 3: return pick_r2<T, 3>(unit);
     case 4: return pick_r2<T, 4>(unit);
+    case 6: return pick_r2<T, 6>(unit);
     case 8: return pick_r2<T, 8>(unit);
+    case 12: return pick_r2<T, 12>(unit);
     case 16: return pick_r2<T, 16>(unit);
+    case 24: return pick_r2<T, 24>(unit);
     case 32: return pick_r2<T, 32>(unit);
     default: return nullptr;
   }
