@@ -127,6 +127,11 @@ CASES = [
     ("wide_R96", lambda: scinputs.sbm(3000, 6, 12, 0.1, seed=8), 96, 40, False, 0.1),
     ("wide_R200", lambda: scinputs.sbm(1200, 4, 12, 0.1, seed=8), 200, 12, True, 0.1),
     ("star_hub", lambda: scinputs.star(700), 8, 25, False, 0.3),
+    # a 40 000-degree hub: its tile's column segment exceeds the staged capacity (the
+    # streaming kernel reads it from global memory) and the resident plan does not fit
+    ("hub_overflow", lambda: scinputs.from_edges(
+        40001, np.concatenate([np.zeros(40000, np.int64), np.arange(1, 40000)]),
+        np.concatenate([np.arange(1, 40001), np.arange(2, 40001)]), None), 16, 12, False, 0.3),
     ("path_tiny", lambda: scinputs.path(2), 4, 5, False, 0.5),
 ]
 
