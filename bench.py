@@ -336,12 +336,9 @@ def run_ours(args):
     # gathered bytes: every nonzero of W reads one R-wide row of T_s per step
     gather_gbps = float(g.nnz) * R * 4 * order * args.steps / (kern_ms / 1e3) / 1e9
     cw = int(os.environ.get("SC_CHUNK", "0")) or None
-    if cw is None:   # the library's chunk rule: widest power of two with N*w*4 <= 128 MB
-        cw = 128
-        while cw > 4 and n * cw * 4 > 128 * 2 ** 20:
-            cw //= 2
-        if cw * 4 < 128:
-            cw = 128
+    if cw is None:   # the library's chunk rule, in 16-byte vectors
+        cv = next((v for v in (32, 24, 16, 12, 8, 6, 4, 3, 2, 1) if n * v * 16 <= 128 * 2 ** 20), 1)
+        cw = 4 * (cv if cv * 16 >= 128 else 16)
     cw = min(cw, R)
     gceil, gcase = gather_ceiling(cw * 4, n * cw * 4)
 
