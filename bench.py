@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cluster", action="store_true")
     ap.add_argument("--no-stability", action="store_true")
+    ap.add_argument("--dist-path", action="store_true",
+                    help="use the row-partitioned NCCL filter even on one rank (exercises the multi-GPU path)")
     return ap.parse_args()
 
 
@@ -246,7 +248,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     # ---- per-graph setup (single-GPU view for lambda_max / lambda_k)
-    if world == 1:
+    partitioned = world > 1 or args.dist_path
+    if not partitioned:
         G = sc.Graph.from_csr(g)
         lmax = sc.sc_lambda_max(G.handle, 60, 0.01, args.seed)
         lam_k, count_k = sc.sc_estimate_lambda_k(G.handle, w.k, lmax, min(order, 150), True, 32, args.seed + 1,
@@ -258,12 +261,13 @@ def run_ours(args):
         lmax = 2.0 * float(g.degrees().max())
         lam_k, count_k = 0.25 * lmax, float("nan")
         part = pdist.local_part(g.row_ptr, g.col_idx, g.values, n, rank, world)
-        part = pdist.exchange_send_lists(part)
+        part = (pdist.exchange_send_lists(part) if world > 1
+                else pdist.send_lists_from_halos(part, [part.halo_gid]))
         Gl = sc.Graph(part.n_local, part.row_ptr, part.col_idx, part.values, n_cols=part.n_local + part.n_halo)
         handle = Gl.handle
     d = sc.sc_cheby_coeffs(lam_k, lmax, order, w.jackson)
 
-    if world == 1:
+    if not partitioned:
         X = torch.empty((n, R), dtype=torch.float32, device=dev)
         sc.sc_random_signals_f32(n, R, 0, args.seed, 0, 0.0, X)
         Y = torch.empty_like(X)
