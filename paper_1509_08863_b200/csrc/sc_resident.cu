@@ -85,7 +85,7 @@ struct ResidentParams {
 };
 
 template <typename T, int VPR, int EB, bool UNIT>
-__global__ void __launch_bounds__(kRThreads, 1)
+__global__ void __launch_bounds__(kRThreads, 2)
 cheb_resident_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                      const float* __restrict__ val, const T* __restrict__ strength,
                      const uint16_t* __restrict__ order, ResidentParams rp) {
@@ -282,8 +282,11 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
     std::vector<int64_t> plan = {0, 0, 0, 0, 0};
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, g->device);
-    const int grid = (int)std::min<int64_t>(g->num_sms, ntiles);
-    if (coop && grid > 0) {
+    (void)0;
+    // two CTAs per SM when their slices fit (more warps to hide gather latency), else one
+    for (int per_sm = 2; per_sm >= 1 && !plan[0]; --per_sm) {
+      const int grid = (int)std::min<int64_t>((int64_t)g->num_sms * per_sm, ntiles);
+      if (!coop || grid <= 0) break;
       std::vector<int64_t> tb(grid + 1), rpb(grid + 1);
       for (int b = 0; b <= grid; ++b) tb[b] = ntiles * b / grid;
       for (int b = 0; b <= grid; ++b) {
@@ -300,7 +303,8 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
       int occ = 0;
       if (smem <= kRSmemMax &&
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kRThreads, smem) == cudaSuccess && occ >= 1) {
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kRThreads, smem) == cudaSuccess &&
+          occ >= per_sm) {
         auto buf = std::make_unique<DevBuf>();
         SC_TRY(buf->ensure(sizeof(int64_t) * (grid + 1)));
         SC_CUDA_TRY(cudaMemcpy(buf->ptr, tb.data(), sizeof(int64_t) * (grid + 1), cudaMemcpyHostToDevice));
