@@ -558,3 +558,36 @@ def test_nccl_dist_filter_single_rank(sc):
         Yo = chebyshev.cheb_filter(L, X.astype(np.float64), d, lmax)
         assert rel(Y, Yo) <= F32_TOL
     nf.close()
+
+
+# ---------------------------------------------------------------------------
+# randomised filter cases: sizes, degrees, weights, widths, orders, both kernels
+# ---------------------------------------------------------------------------
+
+def _random_case(i):
+    rng = np.random.default_rng(1000 + i)
+    n = int(rng.integers(2, 6000))
+    if rng.random() < 0.5:
+        g = scinputs.random_connected(min(n, 1500), float(rng.uniform(0.0, 0.02)), seed=int(rng.integers(1 << 30)),
+                                      weighted=bool(rng.random() < 0.5))
+    else:
+        k = int(rng.integers(1, 8))
+        n = max(n, 4 * k + 4)
+        g = scinputs.sbm(n, k, float(rng.uniform(2.0, 25.0)), float(rng.uniform(0.0, 0.3)),
+                         seed=int(rng.integers(1 << 30)))
+    R = int(rng.choice([1, 2, 3, 4, 5, 7, 8, 12, 13, 16, 24, 31, 32, 48, 64, 96, 100, 128, 130]))
+    order = int(rng.integers(1, 60))
+    return g, R, order, bool(rng.random() < 0.5), float(rng.uniform(0.01, 1.0))
+
+
+@pytest.mark.parametrize("path", ["resident", "streaming"])
+@pytest.mark.parametrize("i", range(16))
+def test_filter_random_cases(sc, i, path, monkeypatch):
+    monkeypatch.setenv("SC_RESIDENT", "1" if path == "resident" else "0")
+    g, R, order, jackson, ratio = _random_case(i)
+    L = laplacian.laplacian(g)
+    lmax = 2.0 * float(max(laplacian.strengths(laplacian.adjacency(g)).max(), 1e-12))
+    X = scinputs.gaussian_block(50 + i, g.n, R)
+    Y = gpu_filter(sc, g, X, ratio * lmax, lmax, order, jackson)
+    Yo = chebyshev.lowpass_filter(L, X.astype(np.float64), ratio * lmax, lmax, order, jackson)
+    assert rel(Y, Yo) <= F32_TOL, (g.n, g.nnz, R, order)
