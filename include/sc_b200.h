@@ -69,7 +69,8 @@ const char* sc_last_error(void);
  *  row_ptr, col_idx, values   CSR arrays as above (values may be NULL: unit weights).
  *  out      receives the new handle; free it with sc_graph_free.
  * The strengths s_i are computed on device in fp64 from the rows as given.
- * Errors: SC_ERR_ARG for n_rows<1, n_cols<n_rows, nnz<0, null arrays;
+ * Errors: SC_ERR_ARG for n_rows<1, n_cols<n_rows, nnz<0, null arrays, row_ptr[0] != 0,
+ *         row_ptr[n_rows] != nnz, decreasing row_ptr, column index outside [0, n_cols);
  *         SC_ERR_NOMEM / SC_ERR_CUDA on device failures.
  */
 int sc_graph_load(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,

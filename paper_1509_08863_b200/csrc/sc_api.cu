@@ -196,8 +196,10 @@ int sc_graph_load(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ro
   if ((rc = cp(g->row_ptr.ptr, row_ptr, sizeof(int64_t) * (n_rows + 1))) != SC_OK) return bail(rc);
   if ((rc = cp(g->col_idx.ptr, col_idx, sizeof(int32_t) * nnz)) != SC_OK) return bail(rc);
   if (!g->unit_weights && (rc = cp(g->values.ptr, values, sizeof(float) * nnz)) != SC_OK) return bail(rc);
-  int64_t last = 0;
+  int64_t first = 0, last = 0;
+  cudaMemcpy(&first, g->row_ptr.as<int64_t>(), sizeof(int64_t), cudaMemcpyDeviceToHost);
   cudaMemcpy(&last, g->row_ptr.as<int64_t>() + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost);
+  if (first != 0) return bail(fail(SC_ERR_ARG, "row_ptr[0] != 0"));
   if (last != nnz) return bail(fail(SC_ERR_ARG, "row_ptr[n_rows] != nnz"));
   sc::DevBuf flag;
   if ((rc = flag.ensure(16)) != SC_OK) return bail(rc);

@@ -89,6 +89,9 @@ def test_graph_load_rejects_bad_csr(sc):
         sc.sc_graph_load(g.n, g.n, g.nnz, g.row_ptr, bad, None)
     with pytest.raises(sc.SCError):
         sc.sc_graph_load(g.n, g.n, g.nnz + 1, g.row_ptr, g.col_idx, None)
+    shifted = g.row_ptr + 1
+    with pytest.raises(sc.SCError):
+        sc.sc_graph_load(g.n, g.n, g.nnz + 1, shifted, np.concatenate([g.col_idx, [0]]).astype(np.int32), None)
 
 
 @pytest.mark.parametrize("maker", [
