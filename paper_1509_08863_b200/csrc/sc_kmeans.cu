@@ -48,24 +48,52 @@ __global__ void absmax_bits_kernel(const float* __restrict__ F, int64_t total, u
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
-__device__ __forceinline__ double dist2_row(const float* __restrict__ x, const double* __restrict__ c, int d) {
-  double acc = 0.0;
-  for (int q = 0; q < d; ++q) {
-    const double diff = __dsub_rn((double)x[q], c[q]);
-    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+// Stage the rows [p0, p0 + kSP) of F into shared memory as fp32 [kSP][d+1] (padded: the
+// threads of a warp then read their own rows conflict-free); coalesced global loads.
+constexpr int kSP = 128;   // points per block of the per-point kernels
+__device__ __forceinline__ void stage_rows(const float* __restrict__ F, int64_t n, int d, int64_t p0,
+                                           float* __restrict__ sx) {
+  const int rows = (int)min((int64_t)kSP, n - p0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // one warp per row (coalesced, no index division); 8 rows' loads in flight per warp
+  for (int r0 = warp; r0 < rows; r0 += nw * 8) {
+    for (int q0 = 0; q0 < d; q0 += 32) {
+      const int q = q0 + lane;
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + u * nw;
+        v[u] = (r < rows && q < d) ? __ldg(F + (p0 + r) * d + q) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + u * nw;
+        if (r < rows && q < d) sx[r * (d + 1) + q] = v[u];
+      }
+    }
   }
-  return acc;
 }
 
 // d2[i] = (first ? dist : min(d2[i], dist)) to centre c (device fp64 row)
-__global__ void d2_update_kernel(const float* __restrict__ F, int64_t n, int d, const double* __restrict__ c,
-                                 double* __restrict__ d2, int first) {
-  extern __shared__ double sc_[];
+__global__ void __launch_bounds__(kSP) d2_update_kernel(const float* __restrict__ F, int64_t n, int d,
+                                                        const double* __restrict__ c, double* __restrict__ d2,
+                                                        int first) {
+  extern __shared__ unsigned char smd[];
+  double* sc_ = reinterpret_cast<double*>(smd);
+  float* sx = reinterpret_cast<float*>(sc_ + d);
   for (int q = threadIdx.x; q < d; q += blockDim.x) sc_[q] = c[q];
+  const int64_t p0 = (int64_t)blockIdx.x * kSP;
+  stage_rows(F, n, d, p0, sx);
   __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = dist2_row(F + i * d, sc_, d);
-    d2[i] = first ? v : fmin(d2[i], v);
+  const int64_t i = p0 + threadIdx.x;
+  if (i < n) {
+    const float* x = sx + threadIdx.x * (d + 1);
+    double acc = 0.0;
+    for (int q = 0; q < d; ++q) {
+      const double diff = __dsub_rn((double)x[q], sc_[q]);
+      acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    d2[i] = first ? acc : fmin(d2[i], acc);
   }
 }
 
@@ -95,7 +123,14 @@ __global__ void seed_select_kernel(const double* __restrict__ bsum, int G, const
   __shared__ double s_start, s_target;
   __shared__ int s_block;
   __shared__ long long s_idx;
+  __shared__ double s_bs[1024];
   const int lane = threadIdx.x;
+  const bool staged = G <= 1024;
+  if (staged) {
+    for (int b = lane; b < G; b += blockDim.x) s_bs[b] = bsum[b];
+    __syncthreads();
+    bsum = s_bs;   // same values, same summation order below
+  }
   if (lane == 0) {
     double pre = 0.0;
     for (int b = 0; b < G; ++b) pre += bsum[b];
@@ -122,9 +157,11 @@ __global__ void seed_select_kernel(const double* __restrict__ bsum, int G, const
     const int64_t s0 = min(b1, b0 + lane * per), s1 = min(b1, s0 + per);
     double sum = 0.0;
     int64_t last_pos = -1;
-    for (int64_t i = s0; i < s1; ++i) {
-      sum += v[i];
-      if (v[i] > 0.0) last_pos = i;
+#pragma unroll 8
+    for (int64_t i = s0; i < s1; ++i) {   // unrolled: loads in flight, adds in ascending order
+      const double vi = v[i];
+      sum += vi;
+      if (vi > 0.0) last_pos = i;
     }
     double pre = 0.0;
     for (int j = 0; j < 32; ++j) {
@@ -335,14 +372,23 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
 // its root is below the decremented bound (with a 1e-9 relative margin for rounding),
 // the assigned centroid is the unique argmin and the point keeps it -- the labels are the
 // ones a full scan would produce.  Otherwise the point is queued for a full scan.
-__global__ void check_kernel(const float* __restrict__ F, int64_t n, int d, const double* __restrict__ C,
-                             const int32_t* __restrict__ old_lab, const double* __restrict__ dmax,
-                             int32_t* __restrict__ lab, double* __restrict__ dmin, double* __restrict__ lo,
-                             int32_t* __restrict__ list, int* __restrict__ list_len) {
+__global__ void __launch_bounds__(kSP) check_kernel(const float* __restrict__ F, int64_t n, int d,
+                                                    const double* __restrict__ C, const int32_t* __restrict__ old_lab,
+                                                    const double* __restrict__ dmax, int32_t* __restrict__ lab,
+                                                    double* __restrict__ dmin, double* __restrict__ lo,
+                                                    int32_t* __restrict__ list, int* __restrict__ list_len) {
+  extern __shared__ unsigned char smk[];
+  float* sx = reinterpret_cast<float*>(smk);
+  const int64_t p0 = (int64_t)blockIdx.x * kSP;
+  stage_rows(F, n, d, p0, sx);
+  __syncthreads();
   const double dm = *dmax;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t i = p0 + threadIdx.x;
+  const bool in = i < n;
+  bool keep = true;
+  if (in) {
     const int a = old_lab[i];
-    const float* x = F + i * d;
+    const float* x = sx + threadIdx.x * (d + 1);
     const double* c = C + (size_t)a * d;
     double acc = 0.0;
     for (int q = 0; q < d; ++q) {
@@ -351,20 +397,20 @@ __global__ void check_kernel(const float* __restrict__ F, int64_t n, int d, cons
     }
     const double l = lo[i] - dm;
     lo[i] = l;
-    const bool keep = sqrt(acc) * (1.0 + 1e-9) < l * (1.0 - 1e-9);
+    keep = sqrt(acc) * (1.0 + 1e-9) < l * (1.0 - 1e-9);
     if (keep) {
       lab[i] = a;
       dmin[i] = acc;
     }
-    const unsigned need = __ballot_sync(__activemask(), !keep);
-    if (!keep) {
-      const int lane = threadIdx.x & 31;
-      const int leader = __ffs(need) - 1;
-      int base = 0;
-      if (lane == leader) base = atomicAdd(list_len, __popc(need));
-      base = __shfl_sync(need, base, leader);
-      list[base + __popc(need & ((1u << lane) - 1))] = static_cast<int32_t>(i);
-    }
+  }
+  const unsigned need = __ballot_sync(0xffffffffu, !keep);
+  if (!keep) {
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(need) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(list_len, __popc(need));
+    base = __shfl_sync(need, base, leader);
+    list[base + __popc(need & ((1u << lane) - 1))] = static_cast<int32_t>(i);
   }
 }
 
@@ -455,27 +501,51 @@ __global__ void scatter_members_simple_kernel(const int32_t* __restrict__ lab, i
 
 // Device-side plan of the member sums (no host round trip): cluster offsets (exclusive scan
 // of the histogram) and work items of <= chunk members, one thread, ascending clusters.
-__global__ void plan_members_kernel(const unsigned* __restrict__ counts, int k, int64_t chunk,
-                                    int64_t* __restrict__ off, int64_t* __restrict__ ws, int64_t* __restrict__ we,
-                                    int32_t* __restrict__ item0, int32_t* __restrict__ nitems,
-                                    int* __restrict__ total_items) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int64_t o = 0;
-  int it = 0;
-  for (int c = 0; c < k; ++c) {
-    off[c] = o;
-    item0[c] = it;
-    const int64_t cnt = counts[c];
-    for (int64_t a = o; a < o + cnt; a += chunk) {
-      ws[it] = a;
-      we[it] = min(o + cnt, a + chunk);
-      ++it;
+__global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __restrict__ counts, int k, int64_t chunk,
+                                                           int64_t* __restrict__ off, int64_t* __restrict__ ws,
+                                                           int64_t* __restrict__ we, int32_t* __restrict__ item0,
+                                                           int32_t* __restrict__ nitems, int* __restrict__ total_items) {
+  __shared__ long long s_cnt[256];
+  __shared__ int s_ni[256];
+  __shared__ long long carry_off;
+  __shared__ int carry_it;
+  const int tid = threadIdx.x;
+  if (tid == 0) { carry_off = 0; carry_it = 0; }
+  __syncthreads();
+  for (int base = 0; base < k; base += 256) {
+    const int c = base + tid;
+    const long long cnt = c < k ? (long long)counts[c] : 0;
+    const int ni = (int)((cnt + chunk - 1) / chunk);
+    s_cnt[tid] = cnt;
+    s_ni[tid] = ni;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {   // inclusive Hillis-Steele scans
+      const long long a = tid >= o ? s_cnt[tid - o] : 0;
+      const int b = tid >= o ? s_ni[tid - o] : 0;
+      __syncthreads();
+      s_cnt[tid] += a;
+      s_ni[tid] += b;
+      __syncthreads();
     }
-    nitems[c] = it - item0[c];
-    o += cnt;
+    const long long o0 = carry_off + s_cnt[tid] - cnt;   // exclusive
+    const int i0 = carry_it + s_ni[tid] - ni;
+    if (c < k) {
+      off[c] = o0;
+      item0[c] = i0;
+      nitems[c] = ni;
+      for (int j = 0; j < ni; ++j) {
+        ws[i0 + j] = o0 + (int64_t)j * chunk;
+        we[i0 + j] = min(o0 + cnt, o0 + (int64_t)(j + 1) * chunk);
+      }
+    }
+    __syncthreads();
+    if (tid == 255) { carry_off += s_cnt[255]; carry_it += s_ni[255]; }
+    __syncthreads();
   }
-  off[k] = o;
-  *total_items = it;
+  if (tid == 0) {
+    off[k] = carry_off;
+    *total_items = carry_it;
+  }
 }
 
 // exact member sums: work item w covers members [ws[w], we[w]) of cluster wc[w]; thread
@@ -491,8 +561,18 @@ __global__ void member_sum_kernel(const float* __restrict__ F, int d, const int3
   const int slots = blockDim.x / d;
   const int j = threadIdx.x / d, q = threadIdx.x - j * d;
   __int128 acc = 0;
-  if (j < slots)
-    for (int64_t m = ws[w] + j; m < we[w]; m += slots) acc += to_fixed(F[(int64_t)perm[m] * d + q], shift);
+  if (j < slots) {
+    const int64_t e = we[w];
+    int64_t m = ws[w] + j;
+    for (; m + 3 * slots < e; m += 4 * slots) {   // four independent gathers in flight
+      const float x0 = F[(int64_t)perm[m] * d + q];
+      const float x1 = F[(int64_t)perm[m + slots] * d + q];
+      const float x2 = F[(int64_t)perm[m + 2 * slots] * d + q];
+      const float x3 = F[(int64_t)perm[m + 3 * slots] * d + q];
+      acc += to_fixed(x0, shift) + to_fixed(x1, shift) + to_fixed(x2, shift) + to_fixed(x3, shift);
+    }
+    for (; m < e; m += slots) acc += to_fixed(F[(int64_t)perm[m] * d + q], shift);
+  }
   if (j < slots) {
     red2[((size_t)j * d + q) * 2] = (unsigned long long)acc;
     red2[((size_t)j * d + q) * 2 + 1] = (unsigned long long)(acc >> 64);
@@ -511,18 +591,44 @@ __global__ void member_sum_kernel(const float* __restrict__ F, int d, const int3
 }
 
 // C[c][q] = correctly rounded (sum of the cluster's partials) / count; empty clusters keep C
-__global__ void member_finalize_kernel(const unsigned long long* __restrict__ part, const int32_t* __restrict__ item0,
-                                       const int32_t* __restrict__ nitems, const unsigned* __restrict__ counts, int k,
-                                       int d, int shift, double* __restrict__ C) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * d; e += gridDim.x * blockDim.x) {
-    const int c = e / d, q = e - c * d;
-    if (counts[c] == 0) continue;
+// C[c][q] = correctly rounded (sum of the cluster's partials) / count; empty clusters keep C.
+// One block per cluster: thread (j, q) sums items j, j+slots, ... of dim q, then the slots
+// are added in order (integer sums: exact whatever the order).
+__global__ void __launch_bounds__(256) member_finalize_kernel(const unsigned long long* __restrict__ part,
+                                                              const int32_t* __restrict__ item0,
+                                                              const int32_t* __restrict__ nitems,
+                                                              const unsigned* __restrict__ counts, int k, int d,
+                                                              int shift, double* __restrict__ C) {
+  extern __shared__ unsigned long long red3[];   // [slots][d][2]
+  const int c = blockIdx.x;
+  if (c >= k || counts[c] == 0) return;
+  const int slots = max(1, (int)blockDim.x / d);
+  const int nit = nitems[c], i0 = item0[c];
+  for (int q0 = 0; q0 < d; q0 += (int)blockDim.x) {   // d > blockDim: several passes
+    const int j = threadIdx.x / min(d, (int)blockDim.x);
+    const int q = q0 + (int)threadIdx.x % min(d, (int)blockDim.x);
     __int128 sum = 0;
-    for (int it = 0; it < nitems[c]; ++it) {
-      const size_t o = ((size_t)(item0[c] + it) * d + q) * 2;
-      sum += (__int128)(((unsigned __int128)part[o + 1] << 64) | part[o]);
+    if (j < slots && q < d)
+      for (int it = j; it < nit; it += slots) {
+        const size_t o = ((size_t)(i0 + it) * d + q) * 2;
+        sum += (__int128)(((unsigned __int128)part[o + 1] << 64) | part[o]);
+      }
+    __syncthreads();
+    if (j < slots && q < d) {
+      red3[((size_t)j * d + q) * 2] = (unsigned long long)sum;
+      red3[((size_t)j * d + q) * 2 + 1] = (unsigned long long)(sum >> 64);
     }
-    C[e] = fixed_to_double(sum, shift) / (double)counts[c];
+    __syncthreads();
+    if ((int)threadIdx.x < min(d - q0, (int)blockDim.x)) {
+      const int qq = q0 + threadIdx.x;
+      __int128 tot = 0;
+      for (int jj = 0; jj < slots; ++jj) {
+        const unsigned long long lo = red3[((size_t)jj * d + qq) * 2];
+        const unsigned long long hi = red3[((size_t)jj * d + qq) * 2 + 1];
+        tot += (__int128)(((unsigned __int128)hi << 64) | lo);
+      }
+      C[(size_t)c * d + qq] = fixed_to_double(tot, shift) / (double)counts[c];
+    }
   }
 }
 
@@ -631,6 +737,10 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   const int shift = 100 - E;   // |x| 2^shift < 2^100; sums of < 2^25 members fit 2^125
 
   SC_CUDA_TRY(cudaFuncSetAttribute(assign3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
+  const int smem_rows = (int)(sizeof(float) * kSP * (d + 1));
+  const int smem_d2 = smem_rows + (int)(sizeof(double) * d);
+  SC_CUDA_TRY(cudaFuncSetAttribute(check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_rows));
+  SC_CUDA_TRY(cudaFuncSetAttribute(d2_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_d2));
 
   // Lloyd assignment of every point; host receives inertia (fixed-order sum of block
   // partials), the number of changed labels and the label histogram
@@ -652,8 +762,9 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
       // Hamerly pruning: points whose assigned centroid is provably still the unique
       // nearest keep it; the rest are queued and fully rescanned
       SC_CUDA_TRY(cudaMemsetAsync(b_len.ptr, 0, sizeof(int), s));
-      check_kernel<<<grid, kB, 0, s>>>(F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(),
-                                       b_lo.as<double>(), b_list.as<int32_t>(), b_len.as<int>());
+      check_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_rows, s>>>(
+          F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(), b_lo.as<double>(),
+          b_list.as<int32_t>(), b_len.as<int>());
       SC_CUDA_TRY(cudaGetLastError());
       assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, b_list.as<int32_t>(), b_len.as<int>(),
                                                              out_lab, b_dmin.as<double>(), b_lo.as<double>());
@@ -684,8 +795,8 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   int* d_total = b_len.as<int>() + 1;
   auto update = [&](const int32_t* cur) -> int {
     if (prune) SC_CUDA_TRY(cudaMemcpyAsync(b_Cold.ptr, C, sizeof(double) * k * d, cudaMemcpyDeviceToDevice, s));
-    plan_members_kernel<<<1, 32, 0, s>>>(b_cnt.as<unsigned>(), k, kChunk, d_off, d_ws, d_we, d_item0, d_nitems,
-                                         d_total);
+    plan_members_kernel<<<1, 256, 0, s>>>(b_cnt.as<unsigned>(), k, kChunk, d_off, d_ws, d_we, d_item0, d_nitems,
+                                          d_total);
     SC_CUDA_TRY(cudaGetLastError());
     SC_CUDA_TRY(cudaMemsetAsync(b_cur.ptr, 0, sizeof(unsigned) * k, s));
     if (k <= 6144) {
@@ -700,7 +811,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     member_sum_kernel<<<(unsigned)max_items, slots * d, sizeof(unsigned long long) * 2 * slots * d, s>>>(
         F, d, b_perm.as<int32_t>(), d_ws, d_we, d_total, shift, b_psum.as<unsigned long long>());
     SC_CUDA_TRY(cudaGetLastError());
-    member_finalize_kernel<<<std::max(1, std::min(grid, (k * d + kB - 1) / kB)), kB, 0, s>>>(
+    member_finalize_kernel<<<k, 256, sizeof(unsigned long long) * 2 * std::max(1, 256 / d) * d, s>>>(
         b_psum.as<unsigned long long>(), d_item0, d_nitems, b_cnt.as<unsigned>(), k, d, shift, C);
     SC_CUDA_TRY(cudaGetLastError());
     if (prune) {
@@ -724,13 +835,14 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     // ---- k-means++ seeding (device-resident: block sums, then one selection kernel per draw)
     int64_t idx = std::min<int64_t>((int64_t)std::floor(u[0] * n), n - 1);
     row_to_centroid_kernel<<<1, 128, 0, s>>>(F, idx, d, C);
-    d2_update_kernel<<<grid, kB, sizeof(double) * d, s>>>(F, n, d, C, b_d2.as<double>(), 1);
+    d2_update_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_d2, s>>>(F, n, d, C, b_d2.as<double>(), 1);
     SC_CUDA_TRY(cudaGetLastError());
     for (int t = 1; t < k; ++t) {
       range_sums_kernel<<<G, kB, 0, s>>>(b_d2.as<double>(), n, chunk, b_part.as<double>());
       seed_select_kernel<<<1, 32, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk, u[t], F, d,
                                           C + (size_t)t * d);
-      d2_update_kernel<<<grid, kB, sizeof(double) * d, s>>>(F, n, d, C + (size_t)t * d, b_d2.as<double>(), 0);
+      d2_update_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_d2, s>>>(F, n, d, C + (size_t)t * d,
+                                                                            b_d2.as<double>(), 0);
       SC_CUDA_TRY(cudaGetLastError());
     }
     // ---- Lloyd.  Iterations are issued without waiting; the changed-label count of
