@@ -49,29 +49,23 @@ __global__ void absmax_bits_kernel(const float* __restrict__ F, int64_t total, u
 }
 
 // Stage the rows [p0, p0 + kSP) of F into shared memory as fp32 [kSP][d+1] (padded: the
-// threads of a warp then read their own rows conflict-free); coalesced global loads.
+// threads of a warp then read their own rows conflict-free).  4-byte cp.async (LDGSTS):
+// a warp copies 32 consecutive floats of a row per instruction (coalesced), every copy of
+// the tile is in flight at once and no register holds the data.
 constexpr int kSP = 128;   // points per block of the per-point kernels
 __device__ __forceinline__ void stage_rows(const float* __restrict__ F, int64_t n, int d, int64_t p0,
                                            float* __restrict__ sx) {
   const int rows = (int)min((int64_t)kSP, n - p0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  // one warp per row (coalesced, no index division); 8 rows' loads in flight per warp
-  for (int r0 = warp; r0 < rows; r0 += nw * 8) {
-    for (int q0 = 0; q0 < d; q0 += 32) {
-      const int q = q0 + lane;
-      float v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int r = r0 + u * nw;
-        v[u] = (r < rows && q < d) ? __ldg(F + (p0 + r) * d + q) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int r = r0 + u * nw;
-        if (r < rows && q < d) sx[r * (d + 1) + q] = v[u];
-      }
+  for (int r = warp; r < rows; r += nw) {
+    const float* src = F + (p0 + r) * d;
+    float* dst = sx + r * (d + 1);
+    for (int q = lane; q < d; q += 32) {
+      const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + q));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src + q) : "memory");
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // d2[i] = (first ? dist : min(d2[i], dist)) to centre c (device fp64 row)
@@ -112,85 +106,100 @@ __global__ void range_sums_kernel(const double* __restrict__ v, int64_t n, int64
   if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
 }
 
-// Whole k-means++ draw on the device (no host round trip): the block sums are prefixed in
-// ascending order by one thread (the same fp64 sequence the host used to take), the block
-// holding u * total is found, then scanned as in range_select_kernel; the chosen row is
-// copied into centroid slot `c_out`.  total <= 0 (all points coincide with centres):
-// uniform draw floor(u n).
-__global__ void seed_select_kernel(const double* __restrict__ bsum, int G, const double* __restrict__ v, int64_t n,
-                                   int64_t chunk, double u, const float* __restrict__ F, int d,
-                                   double* __restrict__ c_out) {
-  __shared__ double s_start, s_target;
-  __shared__ int s_block;
-  __shared__ long long s_idx;
-  __shared__ double s_bs[1024];
-  const int lane = threadIdx.x;
-  const bool staged = G <= 1024;
-  if (staged) {
-    for (int b = lane; b < G; b += blockDim.x) s_bs[b] = bsum[b];
-    __syncthreads();
-    bsum = s_bs;   // same values, same summation order below
+// Whole k-means++ draw on the device (no host round trip), one 1024-thread block: the G
+// block sums are prefixed (fixed-order block scan), the block holding u * total is found,
+// its range is split into 1024 contiguous slices whose sums are prefixed the same way, and
+// the slice crossing the target is scanned sequentially for the first i with
+// prefix_i > u * total (R13: a fixed summation order of the GPU's own).  The
+// chosen row is copied into centroid slot `c_out`.  total <= 0 (all points coincide with
+// centres): uniform draw floor(u n).
+constexpr int kSel = 1024;
+// inclusive block scan in a fixed order (warp shuffle scans, then the warp totals); every
+// thread's inclusive value lands in s_inc[threadIdx.x]
+__device__ __forceinline__ void block_inclusive_scan(double v, double* s_w, double* s_inc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
-  if (lane == 0) {
-    double pre = 0.0;
-    for (int b = 0; b < G; ++b) pre += bsum[b];
-    const double total = pre;
-    if (!(total > 0.0)) {
-      s_block = -1;
-      long long idx = (long long)floor(u * (double)n);
-      s_idx = idx < n - 1 ? idx : n - 1;
-    } else {
-      const double target = u * total;
-      double acc = 0.0;
-      int b = 0;
-      while (b < G - 1 && !(acc + bsum[b] > target)) { acc += bsum[b]; ++b; }
-      s_block = b;
-      s_start = acc;
-      s_target = target;
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    double t = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
     }
+    s_w[32 + lane] = t;
   }
   __syncthreads();
-  if (s_block >= 0) {
-    const int64_t b0 = (int64_t)s_block * chunk, b1 = min(n, b0 + chunk);
-    const int64_t len = b1 - b0;
-    const int64_t per = (len + 31) / 32;
-    const int64_t s0 = min(b1, b0 + lane * per), s1 = min(b1, s0 + per);
+  s_inc[threadIdx.x] = (warp ? s_w[32 + warp - 1] : 0.0) + x;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSel) seed_select_kernel(const double* __restrict__ bsum, int G,
+                                                           const double* __restrict__ v, int64_t n, int64_t chunk,
+                                                           double u, const float* __restrict__ F, int d,
+                                                           double* __restrict__ c_out) {
+  __shared__ double s_w[64];
+  __shared__ double s_inc[kSel];
+  __shared__ int s_first;
+  __shared__ long long s_idx, s_last;
+  const int t = threadIdx.x;
+  // 1. prefix of the G <= kSel block sums; the chosen block is the first whose inclusive
+  // prefix exceeds u * total (atomicMin: unique even if rounding made the prefix non-monotone)
+  block_inclusive_scan(t < G ? bsum[t] : 0.0, s_w, s_inc);
+  const double total = s_inc[kSel - 1];
+  if (t == 0) { s_first = INT_MAX; s_last = -1; }
+  __syncthreads();
+  if (!(total > 0.0)) {
+    if (t == 0) {
+      const long long idx = (long long)floor(u * (double)n);
+      s_idx = idx < n - 1 ? idx : n - 1;
+    }
+    __syncthreads();
+  } else {
+    const double target = u * total;
+    if (t < G && s_inc[t] > target) atomicMin(&s_first, t);
+    __syncthreads();
+    const int blk = s_first == INT_MAX ? G - 1 : s_first;
+    const double start = blk ? s_inc[blk - 1] : 0.0;
+    __syncthreads();
+    // 2. kSel contiguous slices of the chosen block, prefixed the same way
+    const int64_t b0 = (int64_t)blk * chunk, b1 = min(n, b0 + chunk);
+    const int64_t len = b1 - b0 > 0 ? b1 - b0 : 0;
+    const int64_t per = (len + kSel - 1) / kSel;
+    const int64_t s0 = min(b1, b0 + t * per), s1 = min(b1, s0 + per);
     double sum = 0.0;
-    int64_t last_pos = -1;
-#pragma unroll 8
-    for (int64_t i = s0; i < s1; ++i) {   // unrolled: loads in flight, adds in ascending order
+    long long last_pos = -1;
+    for (int64_t i = s0; i < s1; ++i) {
       const double vi = v[i];
       sum += vi;
       if (vi > 0.0) last_pos = i;
     }
-    double pre = 0.0;
-    for (int j = 0; j < 32; ++j) {
-      const double sj = __shfl_sync(0xffffffffu, sum, j);
-      if (j < lane) pre += sj;
-    }
-    const double start = s_start, target = s_target;
-    const double hi = start + pre + sum;
-    const unsigned cross = __ballot_sync(0xffffffffu, hi > target && s1 > s0);
-    long long lp = last_pos;
-    for (int o = 16; o > 0; o >>= 1) lp = max(lp, __shfl_xor_sync(0xffffffffu, lp, o));
-    if (cross == 0) {
-      if (lane == 0) s_idx = lp >= 0 ? lp : b1 - 1;
-    } else {
-      const int L = __ffs(cross) - 1;
-      if (lane == L) {
-        double acc = start + pre;
-        long long pick = s1 - 1;
-        for (int64_t i = s0; i < s1; ++i) {
-          acc += v[i];
-          if (acc > target) { pick = i; break; }
-        }
-        s_idx = pick;
+    if (last_pos >= 0) atomicMax(&s_last, last_pos);
+    if (t == 0) s_first = INT_MAX;
+    block_inclusive_scan(sum, s_w, s_inc);
+    if (s1 > s0 && start + s_inc[t] > target) atomicMin(&s_first, t);
+    __syncthreads();
+    if (s_first == INT_MAX) {
+      if (t == 0) s_idx = s_last >= 0 ? s_last : b1 - 1;
+    } else if (t == s_first) {
+      double acc = start + (t ? s_inc[t - 1] : 0.0);
+      long long pick = s1 - 1;
+      for (int64_t i = s0; i < s1; ++i) {
+        acc += v[i];
+        if (acc > target) { pick = i; break; }
       }
+      s_idx = pick;
     }
+    __syncthreads();
   }
-  __syncthreads();
   const int64_t idx = s_idx;
-  for (int q = lane; q < d; q += blockDim.x) c_out[q] = (double)F[idx * d + q];
+  for (int q = t; q < d; q += blockDim.x) c_out[q] = (double)F[idx * d + q];
 }
 
 __global__ void row_to_centroid_kernel(const float* __restrict__ F, int64_t idx, int d, double* __restrict__ c) {
@@ -366,6 +375,194 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Screened assignment: an fp32 pass finds, for every point, the nearest and second-nearest
+// centroid under approximate distances R~ = fl32(sum_q fma((x_q - c~_q)^2)) (c~ = fp32(c)),
+// together with a rigorous bound |R~ - rho^2| <= eps(R~) on the rounding error (rho the exact
+// real distance).  When R~_2 - eps(R~_2) > R~_1 + eps(R~_1) (with 1e-12 relative slack for the
+// fp64 evaluation), the fp32 nearest is provably the unique exact argmin of the fp64 scan
+// (R8) -- its exact fp64 distance is computed and the point is done; lo =
+// sqrt(R~_2 - eps(R~_2)) is a valid lower bound of the distance to every other centroid.
+// Ambiguous points are queued for the exact scan (assign3_kernel).  Bound (u = 2^-24,
+// eta = 2^-149 for subnormal results, C_m = max_c ||c||):
+//   ||e|| <= u rho + theta,  theta = u (1+u) C_m + 3 eta sqrt(d)   (e = computed - exact diffs)
+//   |sum diff~^2 - rho^2| <= (2u + u^2) rho^2 + 2 theta (1+u) rho + theta^2
+//   |R~ - sum diff~^2| <= gamma_d sum diff~^2,  gamma_d = d u / (1 - d u)
+//   => |R~ - rho^2| <= A rho^2 + B rho + C, solved for rho <= rho_max(R~).
+// (The expanded form ||x||^2 + ||c||^2 - 2 x.c halves the arithmetic but its error scales
+// with ||x|| ||c|| instead of rho^2: measured on configs[3] features it left up to 44 % of
+// the points undecided, against < 0.003 % here.)
+// ---------------------------------------------------------------------------
+struct ScreenBound {
+  double A, B, C;
+  __device__ ScreenBound(double cm, int d) {
+    const double u = 0x1p-24, eta = 0x1p-149;
+    const double g = d * u / (1.0 - d * u);
+    const double theta = u * (1.0 + u) * cm * 1.0001 + 4.0 * eta * sqrt((double)d);
+    A = g + (1.0 + g) * (2.0 * u + u * u);
+    B = 2.0 * (1.0 + g) * (1.0 + u) * theta;
+    C = (1.0 + g) * theta * theta + (d + 1) * eta;
+  }
+  __device__ double eps(double R) const {
+    const double rho = (B + sqrt(B * B + 4.0 * (1.0 - A) * (R + C))) / (2.0 * (1.0 - A));
+    return (A * rho * rho + B * rho + C) * (1.0 + 1e-6) + 1e-300;
+  }
+};
+
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+
+// fp32 copy of the centroids and C_m = max_c ||c|| (rounded up)
+__global__ void centroid_prep_kernel(const double* __restrict__ C, int k, int d, float* __restrict__ Cf,
+                                     double* __restrict__ cm) {
+  __shared__ double sh[256];
+  double m = 0.0;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    double s2 = 0.0;
+    for (int q = 0; q < d; ++q) {
+      const double v = C[(size_t)c * d + q];
+      Cf[(size_t)c * d + q] = (float)v;
+      s2 += v * v;
+    }
+    m = fmax(m, sqrt(s2));
+  }
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *cm = sh[0] * (1.0 + 1e-9);
+}
+
+constexpr int kSPT = 128;              // points per block of the screen
+constexpr int kSLX = kSPT + 4;         // padded leading dimensions (16-byte aligned rows)
+constexpr int kSLC = kAT + 4;
+
+__global__ void __launch_bounds__(256) assign_screen_kernel(const float* __restrict__ F, int64_t n, int d,
+                                                            const double* __restrict__ C,
+                                                            const float* __restrict__ Cf,
+                                                            const double* __restrict__ cm, int k,
+                                                            const int32_t* __restrict__ list,
+                                                            const int* __restrict__ list_len,
+                                                            int32_t* __restrict__ lab, double* __restrict__ dmin,
+                                                            double* __restrict__ lo, int32_t* __restrict__ amb,
+                                                            int* __restrict__ amb_len) {
+  // 128 points x 64-centroid tiles per block; thread (ty, tx) owns points ty*8 .. ty*8+7 and
+  // the centroid pairs (2tx, 2tx+1), (2tx+32, 2tx+33) of a tile: 16 packed accumulators.
+  // Packed fp32x2 arithmetic (FADD2/FFMA2: two IEEE round-to-nearest lanes per instruction,
+  // the same rounding as scalar code, so the bound above holds lane by lane).
+  extern __shared__ float smf[];
+  float* sX = smf;                                    // [d][kSLX]
+  float* sC = smf + (size_t)d * kSLX;                 // [d][kSLC]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int64_t m = list ? (int64_t)*list_len : n;
+  const int64_t p0 = (int64_t)blockIdx.x * kSPT;
+  if (p0 >= m) return;
+  // staging: a warp reads one row (coalesced), lanes store down the column
+  for (int row = warp; row < kSPT; row += 8) {
+    const int64_t pi = p0 + row;
+    const int64_t gi = pi < m ? (list ? (int64_t)list[pi] : pi) : -1;
+    for (int q = lane; q < d; q += 32) sX[(size_t)q * kSLX + row] = gi >= 0 ? F[gi * d + q] : 0.f;
+  }
+  float best[8], second[8];
+  int bidx[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { best[i] = INFINITY; second[i] = INFINITY; bidx[i] = -1; }
+  for (int c0 = 0; c0 < k; c0 += kAT) {
+    const int kt = min(kAT, k - c0);
+    __syncthreads();
+    for (int cc = warp; cc < kAT; cc += 8)
+      for (int q = lane; q < d; q += 32) sC[(size_t)q * kSLC + cc] = cc < kt ? Cf[(size_t)(c0 + cc) * d + q] : 0.f;
+    __syncthreads();
+    uint64_t acc[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { acc[i][0] = 0ull; acc[i][1] = 0ull; }
+#pragma unroll 4
+    for (int q = 0; q < d; ++q) {
+      const float4 xa = *reinterpret_cast<const float4*>(sX + (size_t)q * kSLX + ty * 8);
+      const float4 xb = *reinterpret_cast<const float4*>(sX + (size_t)q * kSLX + ty * 8 + 4);
+      const uint64_t c01 = *reinterpret_cast<const uint64_t*>(sC + (size_t)q * kSLC + 2 * tx);
+      const uint64_t c23 = *reinterpret_cast<const uint64_t*>(sC + (size_t)q * kSLC + 2 * tx + 32);
+      const float xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint64_t xv = pack2(xs[i], xs[i]);
+        uint64_t d0, d1;
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d0) : "l"(xv), "l"(c01));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d1) : "l"(xv), "l"(c23));
+        asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc[i][0]) : "l"(d0));
+        asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc[i][1]) : "l"(d1));
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        const int cidx = 2 * tx + 32 * h + l;   // ascending per thread
+        if (cidx < kt) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float v = __uint_as_float((unsigned)(acc[i][h] >> (32 * l)));
+            if (v < best[i]) { second[i] = best[i]; best[i] = v; bidx[i] = c0 + cidx; }
+            else if (v < second[i]) second[i] = v;
+          }
+        }
+      }
+  }
+  // (R~, index) lexicographic min over the 16 threads of each point row, second best merged
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best[i], o);
+      const float os = __shfl_xor_sync(0xffffffffu, second[i], o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx[i], o);
+      const bool take = (oi >= 0) && (bidx[i] < 0 || ob < best[i] || (ob == best[i] && oi < bidx[i]));
+      const float loser = take ? best[i] : ob;
+      second[i] = fminf(fminf(second[i], os), loser);
+      if (take) { best[i] = ob; bidx[i] = oi; }
+    }
+  }
+  // thread tx < 8 of row ty handles point ty*8 + tx
+  const int i = tx & 7;
+  float bv = best[0], sv = second[0];
+  int bl = bidx[0];
+#pragma unroll
+  for (int ii = 1; ii < 8; ++ii) if (ii == i) { bv = best[ii]; sv = second[ii]; bl = bidx[ii]; }
+  const int col = ty * 8 + i;
+  const int64_t pi = p0 + col;
+  if (tx < 8 && pi < m) {
+    const int64_t gi = list ? (int64_t)list[pi] : pi;
+    const ScreenBound sb(*cm, d);
+    bool unique = false;
+    double low = 0.0;
+    if (bl >= 0 && isfinite(bv)) {
+      const double r1 = bv, r2 = sv;
+      const double up = (r1 + sb.eps(r1)) * (1.0 + 1e-12);
+      low = isinf(r2) ? (double)INFINITY : (r2 - sb.eps(r2)) * (1.0 - 1e-12);
+      unique = low > up;
+    }
+    if (unique) {
+      const double* c = C + (size_t)bl * d;
+      double acc = 0.0;
+      for (int q = 0; q < d; ++q) {
+        const double diff = __dsub_rn((double)sX[(size_t)q * kSLX + col], c[q]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+      }
+      lab[gi] = bl;
+      dmin[gi] = acc;
+      lo[gi] = sqrt(low);
+    } else {
+      amb[atomicAdd(amb_len, 1)] = static_cast<int32_t>(gi);
+    }
+  }
+}
+
 // Pruning test (Hamerly): the centroids moved by at most dmax since lo_i (a lower bound
 // of the distance to every centroid but the assigned one) was computed.  The exact
 // squared distance to the assigned centroid is computed with the scan's arithmetic; if
@@ -499,12 +696,12 @@ __global__ void scatter_members_simple_kernel(const int32_t* __restrict__ lab, i
   }
 }
 
-// Device-side plan of the member sums (no host round trip): cluster offsets (exclusive scan
-// of the histogram) and work items of <= chunk members, one thread, ascending clusters.
+// Device-side plan of the member sums (no host round trip): cluster offsets off[0..k]
+// (exclusive scan of the histogram) and the first work item item0[0..k] of each cluster
+// (work items of <= chunk members, ascending clusters); item0[k] = number of items.
 __global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __restrict__ counts, int k, int64_t chunk,
-                                                           int64_t* __restrict__ off, int64_t* __restrict__ ws,
-                                                           int64_t* __restrict__ we, int32_t* __restrict__ item0,
-                                                           int32_t* __restrict__ nitems, int* __restrict__ total_items) {
+                                                           int64_t* __restrict__ off, int32_t* __restrict__ item0,
+                                                           int* __restrict__ total_items) {
   __shared__ long long s_cnt[256];
   __shared__ int s_ni[256];
   __shared__ long long carry_off;
@@ -527,16 +724,9 @@ __global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __res
       s_ni[tid] += b;
       __syncthreads();
     }
-    const long long o0 = carry_off + s_cnt[tid] - cnt;   // exclusive
-    const int i0 = carry_it + s_ni[tid] - ni;
     if (c < k) {
-      off[c] = o0;
-      item0[c] = i0;
-      nitems[c] = ni;
-      for (int j = 0; j < ni; ++j) {
-        ws[i0 + j] = o0 + (int64_t)j * chunk;
-        we[i0 + j] = min(o0 + cnt, o0 + (int64_t)(j + 1) * chunk);
-      }
+      off[c] = carry_off + s_cnt[tid] - cnt;   // exclusive
+      item0[c] = carry_it + s_ni[tid] - ni;
     }
     __syncthreads();
     if (tid == 255) { carry_off += s_cnt[255]; carry_it += s_ni[255]; }
@@ -544,34 +734,50 @@ __global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __res
   }
   if (tid == 0) {
     off[k] = carry_off;
+    item0[k] = carry_it;
     *total_items = carry_it;
   }
 }
 
-// exact member sums: work item w covers members [ws[w], we[w]) of cluster wc[w]; thread
-// (slot j, dim q) accumulates x * 2^shift exactly in a 128-bit integer, the block reduces
-// the slots of each dim and writes one 128-bit partial per (item, dim)
+// Exact member sums: block w takes work item w -- cluster c (item0[c] <= w < item0[c+1],
+// binary search), members [off[c] + j chunk, min(off[c+1], off[c] + (j+1) chunk)) with
+// j = w - item0[c].  Thread (slot, dim q) accumulates x * 2^shift exactly in a 128-bit integer,
+// the block reduces its slots, and the block sum of each dim is added, as four 32-bit limbs,
+// to the cluster's 64-bit limb accumulators acc[c][q][0..3] (integer atomics: exact and order
+// independent; < 2^32 items keep every limb sum below 2^64).
 __global__ void member_sum_kernel(const float* __restrict__ F, int d, const int32_t* __restrict__ perm,
-                                  const int64_t* __restrict__ ws, const int64_t* __restrict__ we,
-                                  const int* __restrict__ total_items, int shift,
-                                  unsigned long long* __restrict__ part /* [items][d][2] */) {
+                                  const int64_t* __restrict__ off, const int32_t* __restrict__ item0, int k,
+                                  int64_t chunk, const int* __restrict__ total_items, int shift,
+                                  unsigned long long* __restrict__ acc4 /* [k][d][4] */) {
   extern __shared__ unsigned long long red2[];   // [slots][d][2]
+  __shared__ int s_c;
   const int w = blockIdx.x;
   if (w >= *total_items) return;
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = k;   // largest c with item0[c] <= w
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (item0[mid] <= w) lo = mid; else hi = mid;
+    }
+    s_c = lo;
+  }
+  __syncthreads();
+  const int c = s_c;
+  const int64_t wsb = off[c] + (int64_t)(w - item0[c]) * chunk;
+  const int64_t web = min(off[c + 1], wsb + chunk);
   const int slots = blockDim.x / d;
   const int j = threadIdx.x / d, q = threadIdx.x - j * d;
   __int128 acc = 0;
   if (j < slots) {
-    const int64_t e = we[w];
-    int64_t m = ws[w] + j;
-    for (; m + 3 * slots < e; m += 4 * slots) {   // four independent gathers in flight
-      const float x0 = F[(int64_t)perm[m] * d + q];
-      const float x1 = F[(int64_t)perm[m + slots] * d + q];
-      const float x2 = F[(int64_t)perm[m + 2 * slots] * d + q];
-      const float x3 = F[(int64_t)perm[m + 3 * slots] * d + q];
-      acc += to_fixed(x0, shift) + to_fixed(x1, shift) + to_fixed(x2, shift) + to_fixed(x3, shift);
+    int64_t m = wsb + j;
+    for (; m + 7 * slots < web; m += 8 * slots) {   // eight independent gathers in flight
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = F[(int64_t)perm[m + u * slots] * d + q];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += to_fixed(x[u], shift);
     }
-    for (; m < e; m += slots) acc += to_fixed(F[(int64_t)perm[m] * d + q], shift);
+    for (; m < web; m += slots) acc += to_fixed(F[(int64_t)perm[m] * d + q], shift);
   }
   if (j < slots) {
     red2[((size_t)j * d + q) * 2] = (unsigned long long)acc;
@@ -585,51 +791,29 @@ __global__ void member_sum_kernel(const float* __restrict__ F, int d, const int3
       const unsigned long long hi = red2[((size_t)jj * d + threadIdx.x) * 2 + 1];
       sum += (__int128)(((unsigned __int128)hi << 64) | lo);
     }
-    part[((size_t)w * d + threadIdx.x) * 2] = (unsigned long long)sum;
-    part[((size_t)w * d + threadIdx.x) * 2 + 1] = (unsigned long long)(sum >> 64);
+    const unsigned __int128 us = (unsigned __int128)sum;
+    unsigned long long* a = acc4 + ((size_t)c * d + threadIdx.x) * 4;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const unsigned long long limb = (unsigned long long)(us >> (32 * l)) & 0xffffffffull;
+      if (limb) atomicAdd(a + l, limb);
+    }
   }
 }
 
-// C[c][q] = correctly rounded (sum of the cluster's partials) / count; empty clusters keep C
-// C[c][q] = correctly rounded (sum of the cluster's partials) / count; empty clusters keep C.
-// One block per cluster: thread (j, q) sums items j, j+slots, ... of dim q, then the slots
-// are added in order (integer sums: exact whatever the order).
-__global__ void __launch_bounds__(256) member_finalize_kernel(const unsigned long long* __restrict__ part,
-                                                              const int32_t* __restrict__ item0,
-                                                              const int32_t* __restrict__ nitems,
-                                                              const unsigned* __restrict__ counts, int k, int d,
-                                                              int shift, double* __restrict__ C) {
-  extern __shared__ unsigned long long red3[];   // [slots][d][2]
-  const int c = blockIdx.x;
-  if (c >= k || counts[c] == 0) return;
-  const int slots = max(1, (int)blockDim.x / d);
-  const int nit = nitems[c], i0 = item0[c];
-  for (int q0 = 0; q0 < d; q0 += (int)blockDim.x) {   // d > blockDim: several passes
-    const int j = threadIdx.x / min(d, (int)blockDim.x);
-    const int q = q0 + (int)threadIdx.x % min(d, (int)blockDim.x);
-    __int128 sum = 0;
-    if (j < slots && q < d)
-      for (int it = j; it < nit; it += slots) {
-        const size_t o = ((size_t)(i0 + it) * d + q) * 2;
-        sum += (__int128)(((unsigned __int128)part[o + 1] << 64) | part[o]);
-      }
-    __syncthreads();
-    if (j < slots && q < d) {
-      red3[((size_t)j * d + q) * 2] = (unsigned long long)sum;
-      red3[((size_t)j * d + q) * 2 + 1] = (unsigned long long)(sum >> 64);
-    }
-    __syncthreads();
-    if ((int)threadIdx.x < min(d - q0, (int)blockDim.x)) {
-      const int qq = q0 + threadIdx.x;
-      __int128 tot = 0;
-      for (int jj = 0; jj < slots; ++jj) {
-        const unsigned long long lo = red3[((size_t)jj * d + qq) * 2];
-        const unsigned long long hi = red3[((size_t)jj * d + qq) * 2 + 1];
-        tot += (__int128)(((unsigned __int128)hi << 64) | lo);
-      }
-      C[(size_t)c * d + qq] = fixed_to_double(tot, shift) / (double)counts[c];
-    }
-  }
+// C[c][q] = correctly rounded (cluster sum) / count; empty clusters keep C.  The sum is
+// sum_l acc[c][q][l] 2^(32 l) mod 2^128, read as a signed 128-bit integer.
+__global__ void member_finalize_kernel(const unsigned long long* __restrict__ acc4, const unsigned* __restrict__ counts,
+                                       int k, int d, int shift, double* __restrict__ C) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)k * d) return;
+  const int c = (int)(e / d);
+  if (counts[c] == 0) return;
+  const unsigned long long* a = acc4 + e * 4;
+  unsigned __int128 u = 0;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) u += (unsigned __int128)a[l] << (32 * l);
+  C[e] = fixed_to_double((__int128)u, shift) / (double)counts[c];
 }
 
 int num_sms_current() {
@@ -665,7 +849,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
                          cudaStream_t s) {
   const int sms = num_sms_current();
   const int grid = sms * 8;
-  const int G = sms * 2;                                  // k-means++ range blocks
+  const int G = std::min(sms * 2, 1024);                  // k-means++ range blocks (<= kSel)
   const int64_t chunk = (n + G - 1) / G;
   // workspace
   // assignment: 64 points x 64-centroid tiles per block, fp64 [d][64] tiles of both
@@ -683,19 +867,25 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_TRY(b_cur.ensure(sizeof(unsigned) * k, s));
   SC_TRY(b_off.ensure(sizeof(int64_t) * (k + 1), s));
   SC_TRY(b_perm.ensure(sizeof(int32_t) * n, s));
-  SC_TRY(b_items.ensure(sizeof(int64_t) * 2 * max_items + sizeof(int32_t) * 2 * k, s));
-  SC_TRY(b_psum.ensure(sizeof(unsigned long long) * 2 * (size_t)max_items * d, s));
+  SC_TRY(b_items.ensure(sizeof(int32_t) * (k + 1), s));
+  SC_TRY(b_psum.ensure(sizeof(unsigned long long) * 4 * (size_t)k * d, s));
   const int64_t nstat = (n + 255) / 256;
   SC_TRY(b_part.ensure(sizeof(double) * std::max<int64_t>(std::max<int64_t>(grid, G), std::max(nblk, nstat)), s));
   PoolBuf b_dmin, b_lo, b_list, b_len, b_dmax, b_Cold;
   SC_TRY(b_dmin.ensure(sizeof(double) * n, s));
   SC_TRY(b_lo.ensure(sizeof(double) * n, s));
   SC_TRY(b_list.ensure(sizeof(int32_t) * n, s));
-  SC_TRY(b_len.ensure(16, s));   // [0] pruning queue length, [1] member work items
+  SC_TRY(b_len.ensure(16, s));   // [0] pruning queue length, [1] member work items, [2] ambiguous
   SC_TRY(b_dmax.ensure(16, s));
   SC_TRY(b_Cold.ensure(sizeof(double) * k * d, s));
   PoolBuf b_chg;
   SC_TRY(b_chg.ensure(sizeof(int) * (max_iter + 2), s));
+  // screened assignment: fp32 centroids, C_m, queue of the points the screen cannot decide
+  PoolBuf b_Cf, b_amb;
+  SC_TRY(b_Cf.ensure(sizeof(float) * (size_t)k * d + 64, s));
+  SC_TRY(b_amb.ensure(sizeof(int32_t) * n, s));
+  float* d_Cf = b_Cf.as<float>();
+  double* d_cm = reinterpret_cast<double*>(b_Cf.as<char>() + ((sizeof(float) * (size_t)k * d + 15) / 16) * 16);
   // pinned per-thread landing slots for the changed-label counts (kept across calls)
   struct PinnedInts {
     int* p = nullptr;
@@ -703,14 +893,15 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     ~PinnedInts() { if (p) cudaFreeHost(p); }
   };
   static thread_local PinnedInts pin;
-  if (pin.n < (size_t)max_iter + 2) {
+  if (pin.n < 2 * ((size_t)max_iter + 2)) {
     if (pin.p) cudaFreeHost(pin.p);
     pin.p = nullptr;
     pin.n = 0;
-    SC_CUDA_TRY(cudaMallocHost(&pin.p, sizeof(int) * (max_iter + 2)));
-    pin.n = (size_t)max_iter + 2;
+    SC_CUDA_TRY(cudaMallocHost(&pin.p, sizeof(int) * 2 * (max_iter + 2)));
+    pin.n = 2 * ((size_t)max_iter + 2);
   }
   int* h_chg = pin.p;
+  int* h_rescan = pin.p + max_iter + 2;   // pruning-queue length per iteration (-1: no check run)
   cudaEvent_t ev_chg[2];
   SC_CUDA_TRY(cudaEventCreateWithFlags(&ev_chg[0], cudaEventDisableTiming));
   SC_CUDA_TRY(cudaEventCreateWithFlags(&ev_chg[1], cudaEventDisableTiming));
@@ -737,6 +928,10 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   const int shift = 100 - E;   // |x| 2^shift < 2^100; sums of < 2^25 members fit 2^125
 
   SC_CUDA_TRY(cudaFuncSetAttribute(assign3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
+  const int smem_screen = (int)(sizeof(float) * (size_t)d * (kSLX + kSLC));
+  SC_CUDA_TRY(cudaFuncSetAttribute(assign_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_screen));
+  // the screen pays off when the exact scan is expensive (env SC_KMEANS_SCREEN=0 disables it)
+  const bool screen = (double)n * k * d >= 134217728.0 && !(std::getenv("SC_KMEANS_SCREEN") && std::atoi(std::getenv("SC_KMEANS_SCREEN")) == 0);
   const int smem_rows = (int)(sizeof(float) * kSP * (d + 1));
   const int smem_d2 = smem_rows + (int)(sizeof(double) * d);
   SC_CUDA_TRY(cudaFuncSetAttribute(check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_rows));
@@ -751,10 +946,38 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   // number of changed labels into changed_dev[slot] and the label histogram (device);
   // block partials of the inertia in b_part
   int* changed_dev = b_chg.as<int>();
-  auto assign_all = [&](int32_t* out_lab, const int32_t* old, int slot) -> int {
+  const bool trace_len = std::getenv("SC_KMEANS_TRACE") != nullptr;
+  auto assign_all = [&](int32_t* out_lab, const int32_t* old, int slot, bool try_check) -> int {
     SC_CUDA_TRY(cudaMemsetAsync(changed_dev + slot, 0, sizeof(int), s));
     SC_CUDA_TRY(cudaMemsetAsync(b_cnt.ptr, 0, sizeof(unsigned) * k, s));
-    if (!old || !prune) {
+    if (screen) {
+      // fp32 screen + exact verification of every point (or of the pruning queue), exact
+      // fp64 scan of the points it cannot decide
+      const bool pruned = old && prune && try_check;
+      int* amb_len = b_len.as<int>() + 2;
+      SC_CUDA_TRY(cudaMemsetAsync(b_len.ptr, 0, 3 * sizeof(int), s));
+      if (pruned) {
+        check_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_rows, s>>>(
+            F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(), b_lo.as<double>(),
+            b_list.as<int32_t>(), b_len.as<int>());
+        SC_CUDA_TRY(cudaGetLastError());
+      }
+      centroid_prep_kernel<<<1, 256, 0, s>>>(C, k, d, d_Cf, d_cm);
+      SC_CUDA_TRY(cudaGetLastError());
+      assign_screen_kernel<<<(unsigned)((n + kSPT - 1) / kSPT), 256, smem_screen, s>>>(
+          F, n, d, C, d_Cf, d_cm, k, pruned ? b_list.as<int32_t>() : nullptr, pruned ? b_len.as<int>() : nullptr,
+          out_lab, b_dmin.as<double>(), b_lo.as<double>(), b_amb.as<int32_t>(), amb_len);
+      SC_CUDA_TRY(cudaGetLastError());
+      assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, b_amb.as<int32_t>(), amb_len, out_lab,
+                                                             b_dmin.as<double>(), b_lo.as<double>());
+      if (trace_len) {
+        int h_len[3] = {0, 0, 0};
+        SC_CUDA_TRY(cudaMemcpyAsync(h_len, b_len.ptr, sizeof(h_len), cudaMemcpyDeviceToHost, s));
+        SC_CUDA_TRY(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[sc_kmeans] iteration %d: %d rescanned, %d ambiguous of %lld\n", slot,
+                     pruned ? h_len[0] : (int)n, h_len[2], (long long)n);
+      }
+    } else if (!old || !prune) {
       // full scan of every point (the first assignment of a restart also sets the bounds lo)
       assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, nullptr, nullptr, out_lab,
                                                              b_dmin.as<double>(), b_lo.as<double>());
@@ -768,6 +991,12 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
       SC_CUDA_TRY(cudaGetLastError());
       assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, b_list.as<int32_t>(), b_len.as<int>(),
                                                              out_lab, b_dmin.as<double>(), b_lo.as<double>());
+      if (trace_len) {
+        int h_len = 0;
+        SC_CUDA_TRY(cudaMemcpyAsync(&h_len, b_len.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SC_CUDA_TRY(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[sc_kmeans] iteration %d: %d of %lld points rescanned\n", slot, h_len, (long long)n);
+      }
     }
     SC_CUDA_TRY(cudaGetLastError());
     assign_stats_kernel<<<(unsigned)nstat, 256, 0, s>>>(out_lab, old, b_dmin.as<double>(), n, b_part.as<double>(),
@@ -788,17 +1017,14 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   // centroids <- member means of the labels `cur` (histogram on the device): members grouped
   // by cluster (counting sort), exact 128-bit fixed-point member sums, one rounding
   int64_t* d_off = b_off.as<int64_t>();
-  int64_t* d_ws = b_items.as<int64_t>();
-  int64_t* d_we = d_ws + max_items;
-  int32_t* d_item0 = reinterpret_cast<int32_t*>(d_we + max_items);
-  int32_t* d_nitems = d_item0 + k;
+  int32_t* d_item0 = b_items.as<int32_t>();
   int* d_total = b_len.as<int>() + 1;
   auto update = [&](const int32_t* cur) -> int {
     if (prune) SC_CUDA_TRY(cudaMemcpyAsync(b_Cold.ptr, C, sizeof(double) * k * d, cudaMemcpyDeviceToDevice, s));
-    plan_members_kernel<<<1, 256, 0, s>>>(b_cnt.as<unsigned>(), k, kChunk, d_off, d_ws, d_we, d_item0, d_nitems,
-                                          d_total);
+    plan_members_kernel<<<1, 256, 0, s>>>(b_cnt.as<unsigned>(), k, kChunk, d_off, d_item0, d_total);
     SC_CUDA_TRY(cudaGetLastError());
     SC_CUDA_TRY(cudaMemsetAsync(b_cur.ptr, 0, sizeof(unsigned) * k, s));
+    SC_CUDA_TRY(cudaMemsetAsync(b_psum.ptr, 0, sizeof(unsigned long long) * 4 * (size_t)k * d, s));
     if (k <= 6144) {
       const int64_t per_block = std::max<int64_t>(4096, (n + grid - 1) / grid);
       scatter_members_kernel<<<(unsigned)((n + per_block - 1) / per_block), kB, sizeof(unsigned) * 2 * k, s>>>(
@@ -809,10 +1035,10 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     SC_CUDA_TRY(cudaGetLastError());
     const int slots = std::max(1, 256 / d);
     member_sum_kernel<<<(unsigned)max_items, slots * d, sizeof(unsigned long long) * 2 * slots * d, s>>>(
-        F, d, b_perm.as<int32_t>(), d_ws, d_we, d_total, shift, b_psum.as<unsigned long long>());
+        F, d, b_perm.as<int32_t>(), d_off, d_item0, k, kChunk, d_total, shift, b_psum.as<unsigned long long>());
     SC_CUDA_TRY(cudaGetLastError());
-    member_finalize_kernel<<<k, 256, sizeof(unsigned long long) * 2 * std::max(1, 256 / d) * d, s>>>(
-        b_psum.as<unsigned long long>(), d_item0, d_nitems, b_cnt.as<unsigned>(), k, d, shift, C);
+    member_finalize_kernel<<<(unsigned)(((int64_t)k * d + 255) / 256), 256, 0, s>>>(
+        b_psum.as<unsigned long long>(), b_cnt.as<unsigned>(), k, d, shift, C);
     SC_CUDA_TRY(cudaGetLastError());
     if (prune) {
       centroid_shift_kernel<<<1, 256, 0, s>>>(C, b_Cold.as<double>(), k, d, b_dmax.as<double>());
@@ -839,7 +1065,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     SC_CUDA_TRY(cudaGetLastError());
     for (int t = 1; t < k; ++t) {
       range_sums_kernel<<<G, kB, 0, s>>>(b_d2.as<double>(), n, chunk, b_part.as<double>());
-      seed_select_kernel<<<1, 32, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk, u[t], F, d,
+      seed_select_kernel<<<1, kSel, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk, u[t], F, d,
                                           C + (size_t)t * d);
       d2_update_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_d2, s>>>(F, n, d, C + (size_t)t * d,
                                                                             b_d2.as<double>(), 0);
@@ -850,17 +1076,29 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     // assignment repeats, further iterations are idempotent (same labels -> same exact
     // means -> same labels), so the one issued speculatively changes nothing but time.
     if (trace) { SC_CUDA_TRY(cudaStreamSynchronize(s)); t_seed += now() - t_mark; t_mark = now(); }
-    SC_TRY(assign_all(lab, nullptr, 0));
+    SC_TRY(assign_all(lab, nullptr, 0, false));
     int it = 0, conv = -1;
+    // With the screen on, the Hamerly check is only worth its extra pass over the features
+    // while it keeps most points: it is skipped once it queued >= 60 % of them (known with
+    // one iteration of lag) and re-tried every 8th iteration.
+    bool use_check = true;
+    int last_check = 0;
     for (it = 1; it <= max_iter; ++it) {
+      const bool try_check = !screen || use_check || it - last_check >= 8;
+      if (try_check) last_check = it;
       SC_TRY(update(lab));
-      SC_TRY(assign_all(nw, lab, it));
+      SC_TRY(assign_all(nw, lab, it, try_check));
       SC_CUDA_TRY(cudaMemcpyAsync(h_chg + it, changed_dev + it, sizeof(int), cudaMemcpyDeviceToHost, s));
+      if (screen && try_check)
+        SC_CUDA_TRY(cudaMemcpyAsync(h_rescan + it, b_len.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+      else
+        h_rescan[it] = -1;
       SC_CUDA_TRY(cudaEventRecord(ev_chg[it & 1], s));
       std::swap(lab, nw);
       if (it >= 2) {
         SC_CUDA_TRY(cudaEventSynchronize(ev_chg[(it - 1) & 1]));
         if (h_chg[it - 1] == 0) { conv = it - 1; break; }
+        if (h_rescan[it - 1] >= 0) use_check = (double)h_rescan[it - 1] < 0.6 * (double)n;
       }
     }
     if (conv < 0) {

@@ -370,6 +370,8 @@ def test_normalize_rows(sc):
 
 def _features(seed, n, k, d, spread):
     rng = np.random.default_rng(seed)
+    if spread < 0:   # integer grid: duplicate points, duplicate seeds, exactly tied distances
+        return rng.integers(0, 3, (n, d)).astype(np.float32)
     C = rng.standard_normal((k, d))
     lab = rng.integers(0, k, n)
     return (C[lab] + spread * rng.standard_normal((n, d))).astype(np.float32)
@@ -379,7 +381,10 @@ def _features(seed, n, k, d, spread):
     (2000, 5, 32, 0.3, 10, 100), (20000, 10, 24, 0.8, 3, 100), (5000, 20, 48, 1.5, 2, 100), (3001, 7, 5, 0.5, 4, 100),
     # n*d >= 4e6 and n*k*d >= 2^27: concurrent restarts on worker streams + Hamerly pruning
     # (iterations capped so the fp64 oracle stays within ~a minute)
-    pytest.param(90000, 32, 48, 1.0, 2, 12, marks=pytest.mark.slow)])
+    pytest.param(90000, 32, 48, 1.0, 2, 12, marks=pytest.mark.slow),
+    # same regime on integer-grid features: exact ties defeat the fp32 screen, so the
+    # exact fp64 rescan of the ambiguous points decides them
+    pytest.param(40000, 64, 56, -1.0, 1, 6, marks=pytest.mark.slow)])
 def test_kmeans_bit_exact(sc, n, k, d, spread, restarts, max_iter):
     X = _features(n + k, n, k, d, spread)
     u = np.stack([scinputs.uniforms(7, k, offset=k * r) for r in range(restarts)])
