@@ -634,32 +634,51 @@ __global__ void centroid_shift_kernel(const double* __restrict__ C, const double
 }
 
 // per-block inertia partials over fixed index ranges (deterministic whatever path
-// produced each point), changed count, label histogram
+// produced each point), changed count, label histogram; with old labels also the list of
+// the changed points and the histogram of their old and new labels (incremental update)
 __global__ void __launch_bounds__(256) assign_stats_kernel(const int32_t* __restrict__ lab,
                                                            const int32_t* __restrict__ old_lab,
                                                            const double* __restrict__ dmin, int64_t n,
                                                            double* __restrict__ part_inertia,
-                                                           int* __restrict__ changed, unsigned* __restrict__ counts) {
+                                                           int* __restrict__ changed, unsigned* __restrict__ counts,
+                                                           int32_t* __restrict__ chg_list,
+                                                           unsigned* __restrict__ dcount) {
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
   const bool valid = i < n;
   const int bl = valid ? lab[i] : -1;
   double inertia = valid ? dmin[i] : 0.0;
-  int nchg = (valid && old_lab && old_lab[i] != bl) ? 1 : 0;
+  const int ol = (valid && old_lab) ? old_lab[i] : bl;
+  const bool chg = valid && ol != bl;
   const unsigned peers = __match_any_sync(0xffffffffu, bl);
   if (valid && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[bl], (unsigned)__popc(peers));
+  const unsigned cm = __ballot_sync(0xffffffffu, chg);
+  if (cm) {
+    const int lane = threadIdx.x & 31, leader = __ffs(cm) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(changed, __popc(cm));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (chg) {
+      chg_list[base + __popc(cm & ((1u << lane) - 1))] = static_cast<int32_t>(i);
+      atomicAdd(&dcount[bl], 1u);
+      atomicAdd(&dcount[ol], 1u);
+    }
+  }
   __shared__ double sh[256];
-  __shared__ int shc[256];
   sh[threadIdx.x] = inertia;
-  shc[threadIdx.x] = nchg;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) { sh[threadIdx.x] += sh[threadIdx.x + o]; shc[threadIdx.x] += shc[threadIdx.x + o]; }
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    part_inertia[blockIdx.x] = sh[0];
-    if (shc[0]) atomicAdd(changed, shc[0]);
-  }
+  if (threadIdx.x == 0) part_inertia[blockIdx.x] = sh[0];
+}
+
+// Centroid sums are kept as exact integers, so they can also be updated incrementally: the
+// full recompute (plan, scatter, member sums) runs iff full_gate(); otherwise
+// member_delta_kernel moves the changed points' contributions between clusters.  The
+// decision reads the device-side changed-label count (no host round trip).
+__device__ __forceinline__ bool full_gate(const int* chg, int64_t thresh) {
+  return chg == nullptr || (int64_t)*chg > thresh;
 }
 
 // members of cluster c land at perm[off[c] .. off[c+1]) (order inside a cluster is
@@ -668,7 +687,8 @@ __global__ void __launch_bounds__(256) assign_stats_kernel(const int32_t* __rest
 // cluster) with a single global atomic.
 __global__ void scatter_members_kernel(const int32_t* __restrict__ lab, int64_t n, int k, int64_t per_block,
                                        unsigned* __restrict__ cursor, const int64_t* __restrict__ off,
-                                       int32_t* __restrict__ perm) {
+                                       int32_t* __restrict__ perm, const int* __restrict__ chg, int64_t thresh) {
+  if (!full_gate(chg, thresh)) return;
   extern __shared__ unsigned hist[];   // [k] local counts, then [k] bases
   unsigned* base = hist + k;
   for (int c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
@@ -689,7 +709,9 @@ __global__ void scatter_members_kernel(const int32_t* __restrict__ lab, int64_t 
 
 __global__ void scatter_members_simple_kernel(const int32_t* __restrict__ lab, int64_t n,
                                               unsigned* __restrict__ cursor, const int64_t* __restrict__ off,
-                                              int32_t* __restrict__ perm) {
+                                              int32_t* __restrict__ perm, const int* __restrict__ chg,
+                                              int64_t thresh) {
+  if (!full_gate(chg, thresh)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = lab[i];
     perm[off[c] + atomicAdd(&cursor[c], 1u)] = static_cast<int32_t>(i);
@@ -699,9 +721,21 @@ __global__ void scatter_members_simple_kernel(const int32_t* __restrict__ lab, i
 // Device-side plan of the member sums (no host round trip): cluster offsets off[0..k]
 // (exclusive scan of the histogram) and the first work item item0[0..k] of each cluster
 // (work items of <= chunk members, ascending clusters); item0[k] = number of items.
-__global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __restrict__ counts, int k, int64_t chunk,
-                                                           int64_t* __restrict__ off, int32_t* __restrict__ item0,
-                                                           int* __restrict__ total_items) {
+__global__ void zero_acc_kernel(unsigned long long* __restrict__ acc4, int64_t cnt, const int* __restrict__ chg,
+                                int64_t thresh) {
+  if (!full_gate(chg, thresh)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    acc4[i] = 0ull;
+}
+
+// (full recompute: histogram of the labels; incremental: histogram of the changed points'
+// old and new labels)
+__global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __restrict__ counts_full,
+                                                           const unsigned* __restrict__ counts_delta, int k,
+                                                           int64_t chunk, int64_t* __restrict__ off,
+                                                           int32_t* __restrict__ item0, int* __restrict__ total_items,
+                                                           const int* __restrict__ chg, int64_t thresh) {
+  const unsigned* __restrict__ counts = full_gate(chg, thresh) ? counts_full : counts_delta;
   __shared__ long long s_cnt[256];
   __shared__ int s_ni[256];
   __shared__ long long carry_off;
@@ -739,6 +773,14 @@ __global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __res
   }
 }
 
+__device__ __forceinline__ void add_limbs(unsigned long long* a, unsigned __int128 u) {
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const unsigned long long limb = (unsigned long long)(u >> (32 * l)) & 0xffffffffull;
+    if (limb) atomicAdd(a + l, limb);
+  }
+}
+
 // Exact member sums: block w takes work item w -- cluster c (item0[c] <= w < item0[c+1],
 // binary search), members [off[c] + j chunk, min(off[c+1], off[c] + (j+1) chunk)) with
 // j = w - item0[c].  Thread (slot, dim q) accumulates x * 2^shift exactly in a 128-bit integer,
@@ -770,14 +812,26 @@ __global__ void member_sum_kernel(const float* __restrict__ F, int d, const int3
   __int128 acc = 0;
   if (j < slots) {
     int64_t m = wsb + j;
-    for (; m + 7 * slots < web; m += 8 * slots) {   // eight independent gathers in flight
+    // entry bit 31: subtract (incremental update); eight independent gathers in flight
+    for (; m + 7 * slots < web; m += 8 * slots) {
       float x[8];
+      uint32_t e[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = F[(int64_t)perm[m + u * slots] * d + q];
+      for (int u = 0; u < 8; ++u) {
+        e[u] = static_cast<uint32_t>(perm[m + u * slots]);
+        x[u] = F[(int64_t)(e[u] & 0x7fffffffu) * d + q];
+      }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc += to_fixed(x[u], shift);
+      for (int u = 0; u < 8; ++u) {
+        const __int128 v = to_fixed(x[u], shift);
+        acc += (e[u] >> 31) ? -v : v;
+      }
     }
-    for (; m < web; m += slots) acc += to_fixed(F[(int64_t)perm[m] * d + q], shift);
+    for (; m < web; m += slots) {
+      const uint32_t e = static_cast<uint32_t>(perm[m]);
+      const __int128 v = to_fixed(F[(int64_t)(e & 0x7fffffffu) * d + q], shift);
+      acc += (e >> 31) ? -v : v;
+    }
   }
   if (j < slots) {
     red2[((size_t)j * d + q) * 2] = (unsigned long long)acc;
@@ -791,28 +845,42 @@ __global__ void member_sum_kernel(const float* __restrict__ F, int d, const int3
       const unsigned long long hi = red2[((size_t)jj * d + threadIdx.x) * 2 + 1];
       sum += (__int128)(((unsigned __int128)hi << 64) | lo);
     }
-    const unsigned __int128 us = (unsigned __int128)sum;
-    unsigned long long* a = acc4 + ((size_t)c * d + threadIdx.x) * 4;
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      const unsigned long long limb = (unsigned long long)(us >> (32 * l)) & 0xffffffffull;
-      if (limb) atomicAdd(a + l, limb);
-    }
+    add_limbs(acc4 + ((size_t)c * d + threadIdx.x) * 4, (unsigned __int128)sum);
+  }
+}
+
+// Incremental exact update: every changed point (old label a -> new label b) is listed
+// under cluster b with sign + and under cluster a with sign - (bit 31 of the entry); the
+// member sums then move its fixed-point image between the clusters exactly.
+__global__ void scatter_delta_kernel(const int32_t* __restrict__ chg_list, const int* __restrict__ chg,
+                                     const int32_t* __restrict__ prev, const int32_t* __restrict__ cur,
+                                     unsigned* __restrict__ cursor, const int64_t* __restrict__ off,
+                                     int32_t* __restrict__ perm, int64_t thresh) {
+  if (full_gate(chg, thresh)) return;
+  const int m = *chg;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    const int32_t i = chg_list[j];
+    const int b = cur[i], a = prev[i];
+    perm[off[b] + atomicAdd(&cursor[b], 1u)] = i;
+    perm[off[a] + atomicAdd(&cursor[a], 1u)] = static_cast<int32_t>(static_cast<uint32_t>(i) | 0x80000000u);
   }
 }
 
 // C[c][q] = correctly rounded (cluster sum) / count; empty clusters keep C.  The sum is
-// sum_l acc[c][q][l] 2^(32 l) mod 2^128, read as a signed 128-bit integer.
-__global__ void member_finalize_kernel(const unsigned long long* __restrict__ acc4, const unsigned* __restrict__ counts,
+// sum_l acc[c][q][l] 2^(32 l) mod 2^128, read as a signed 128-bit integer; the limbs are
+// rewritten in canonical form (each < 2^32), so the next update starts from one add per limb.
+__global__ void member_finalize_kernel(unsigned long long* __restrict__ acc4, const unsigned* __restrict__ counts,
                                        int k, int d, int shift, double* __restrict__ C) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)k * d) return;
   const int c = (int)(e / d);
-  if (counts[c] == 0) return;
-  const unsigned long long* a = acc4 + e * 4;
+  unsigned long long* a = acc4 + e * 4;
   unsigned __int128 u = 0;
 #pragma unroll
   for (int l = 0; l < 4; ++l) u += (unsigned __int128)a[l] << (32 * l);
+#pragma unroll
+  for (int l = 0; l < 4; ++l) a[l] = (unsigned long long)(u >> (32 * l)) & 0xffffffffull;
+  if (counts[c] == 0) return;
   C[e] = fixed_to_double((__int128)u, shift) / (double)counts[c];
 }
 
@@ -857,7 +925,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   if (smem_assign > 200 * 1024) return fail(SC_ERR_ARG, "sc_kmeans: d must be <= 200");
   const int64_t nblk = (n + kAT - 1) / kAT;
   constexpr int64_t kChunk = 512;    // members per exact-sum work item
-  const int64_t max_items = n / kChunk + k + 1;
+  const int64_t max_items = 2 * n / kChunk + k + 1;   // (incremental lists: 2 entries per changed point)
   PoolBuf b_lab, b_new, b_d2, b_C, b_cnt, b_cur, b_off, b_perm, b_items, b_part, b_psum, b_misc;
   SC_TRY(b_lab.ensure(sizeof(int32_t) * n, s));
   SC_TRY(b_new.ensure(sizeof(int32_t) * n, s));
@@ -866,7 +934,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_TRY(b_cnt.ensure(sizeof(unsigned) * k, s));
   SC_TRY(b_cur.ensure(sizeof(unsigned) * k, s));
   SC_TRY(b_off.ensure(sizeof(int64_t) * (k + 1), s));
-  SC_TRY(b_perm.ensure(sizeof(int32_t) * n, s));
+  SC_TRY(b_perm.ensure(sizeof(int32_t) * 2 * n, s));
   SC_TRY(b_items.ensure(sizeof(int32_t) * (k + 1), s));
   SC_TRY(b_psum.ensure(sizeof(unsigned long long) * 4 * (size_t)k * d, s));
   const int64_t nstat = (n + 255) / 256;
@@ -881,7 +949,9 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   PoolBuf b_chg;
   SC_TRY(b_chg.ensure(sizeof(int) * (max_iter + 2), s));
   // screened assignment: fp32 centroids, C_m, queue of the points the screen cannot decide
-  PoolBuf b_Cf, b_amb;
+  PoolBuf b_Cf, b_amb, b_chgl, b_dcnt;
+  SC_TRY(b_chgl.ensure(sizeof(int32_t) * n, s));
+  SC_TRY(b_dcnt.ensure(sizeof(unsigned) * k, s));
   SC_TRY(b_Cf.ensure(sizeof(float) * (size_t)k * d + 64, s));
   SC_TRY(b_amb.ensure(sizeof(int32_t) * n, s));
   float* d_Cf = b_Cf.as<float>();
@@ -950,6 +1020,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   auto assign_all = [&](int32_t* out_lab, const int32_t* old, int slot, bool try_check) -> int {
     SC_CUDA_TRY(cudaMemsetAsync(changed_dev + slot, 0, sizeof(int), s));
     SC_CUDA_TRY(cudaMemsetAsync(b_cnt.ptr, 0, sizeof(unsigned) * k, s));
+    SC_CUDA_TRY(cudaMemsetAsync(b_dcnt.ptr, 0, sizeof(unsigned) * k, s));
     if (screen) {
       // fp32 screen + exact verification of every point (or of the pruning queue), exact
       // fp64 scan of the points it cannot decide
@@ -1000,7 +1071,8 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     }
     SC_CUDA_TRY(cudaGetLastError());
     assign_stats_kernel<<<(unsigned)nstat, 256, 0, s>>>(out_lab, old, b_dmin.as<double>(), n, b_part.as<double>(),
-                                                       changed_dev + slot, b_cnt.as<unsigned>());
+                                                       changed_dev + slot, b_cnt.as<unsigned>(),
+                                                       b_chgl.as<int32_t>(), b_dcnt.as<unsigned>());
     SC_CUDA_TRY(cudaGetLastError());
     return SC_OK;
   };
@@ -1019,20 +1091,32 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   int64_t* d_off = b_off.as<int64_t>();
   int32_t* d_item0 = b_items.as<int32_t>();
   int* d_total = b_len.as<int>() + 1;
-  auto update = [&](const int32_t* cur) -> int {
+  // full recompute when more than n/4 labels changed (or no previous sums), else incremental
+  // (2 gathered rows per changed point against n)
+  const int64_t delta_thresh = n / 4;
+  auto update = [&](const int32_t* cur, const int32_t* prev, const int* chg) -> int {
+    if (!prev) chg = nullptr;
     if (prune) SC_CUDA_TRY(cudaMemcpyAsync(b_Cold.ptr, C, sizeof(double) * k * d, cudaMemcpyDeviceToDevice, s));
-    plan_members_kernel<<<1, 256, 0, s>>>(b_cnt.as<unsigned>(), k, kChunk, d_off, d_item0, d_total);
+    zero_acc_kernel<<<std::max(1, std::min(grid, (int)((4 * (int64_t)k * d + kB - 1) / kB))), kB, 0, s>>>(
+        b_psum.as<unsigned long long>(), 4 * (int64_t)k * d, chg, delta_thresh);
+    plan_members_kernel<<<1, 256, 0, s>>>(b_cnt.as<unsigned>(), b_dcnt.as<unsigned>(), k, kChunk, d_off, d_item0,
+                                          d_total, chg, delta_thresh);
     SC_CUDA_TRY(cudaGetLastError());
     SC_CUDA_TRY(cudaMemsetAsync(b_cur.ptr, 0, sizeof(unsigned) * k, s));
-    SC_CUDA_TRY(cudaMemsetAsync(b_psum.ptr, 0, sizeof(unsigned long long) * 4 * (size_t)k * d, s));
     if (k <= 6144) {
       const int64_t per_block = std::max<int64_t>(4096, (n + grid - 1) / grid);
       scatter_members_kernel<<<(unsigned)((n + per_block - 1) / per_block), kB, sizeof(unsigned) * 2 * k, s>>>(
-          cur, n, k, per_block, b_cur.as<unsigned>(), d_off, b_perm.as<int32_t>());
+          cur, n, k, per_block, b_cur.as<unsigned>(), d_off, b_perm.as<int32_t>(), chg, delta_thresh);
     } else {
-      scatter_members_simple_kernel<<<grid, kB, 0, s>>>(cur, n, b_cur.as<unsigned>(), d_off, b_perm.as<int32_t>());
+      scatter_members_simple_kernel<<<grid, kB, 0, s>>>(cur, n, b_cur.as<unsigned>(), d_off, b_perm.as<int32_t>(),
+                                                        chg, delta_thresh);
     }
     SC_CUDA_TRY(cudaGetLastError());
+    if (prev) {
+      scatter_delta_kernel<<<grid, kB, 0, s>>>(b_chgl.as<int32_t>(), chg, prev, cur, b_cur.as<unsigned>(), d_off,
+                                               b_perm.as<int32_t>(), delta_thresh);
+      SC_CUDA_TRY(cudaGetLastError());
+    }
     const int slots = std::max(1, 256 / d);
     member_sum_kernel<<<(unsigned)max_items, slots * d, sizeof(unsigned long long) * 2 * slots * d, s>>>(
         F, d, b_perm.as<int32_t>(), d_off, d_item0, k, kChunk, d_total, shift, b_psum.as<unsigned long long>());
@@ -1086,7 +1170,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     for (it = 1; it <= max_iter; ++it) {
       const bool try_check = !screen || use_check || it - last_check >= 8;
       if (try_check) last_check = it;
-      SC_TRY(update(lab));
+      SC_TRY(update(lab, it >= 2 ? nw : nullptr, changed_dev + (it - 1)));
       SC_TRY(assign_all(nw, lab, it, try_check));
       SC_CUDA_TRY(cudaMemcpyAsync(h_chg + it, changed_dev + it, sizeof(int), cudaMemcpyDeviceToHost, s));
       if (screen && try_check)
@@ -1099,6 +1183,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
         SC_CUDA_TRY(cudaEventSynchronize(ev_chg[(it - 1) & 1]));
         if (h_chg[it - 1] == 0) { conv = it - 1; break; }
         if (h_rescan[it - 1] >= 0) use_check = (double)h_rescan[it - 1] < 0.6 * (double)n;
+        if (trace_len) std::fprintf(stderr, "[sc_kmeans] iteration %d: %d labels changed\n", it - 1, h_chg[it - 1]);
       }
     }
     if (conv < 0) {
