@@ -31,6 +31,7 @@ bool is_device_ptr(const void* p) {
 
 int Staged::alloc(size_t b, cudaStream_t s) {
   st = s;
+  keep_pool_reserved();
   cudaError_t e = cudaMallocAsync(&owned, b ? b : 1, s);
   if (e != cudaSuccess) {
     owned = nullptr;
