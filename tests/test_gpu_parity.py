@@ -384,7 +384,9 @@ def _features(seed, n, k, d, spread):
     pytest.param(90000, 32, 48, 1.0, 2, 12, marks=pytest.mark.slow),
     # same regime on integer-grid features: exact ties defeat the fp32 screen, so the
     # exact fp64 rescan of the ambiguous points decides them
-    pytest.param(40000, 64, 56, -1.0, 1, 6, marks=pytest.mark.slow)])
+    pytest.param(40000, 64, 56, -1.0, 1, 6, marks=pytest.mark.slow),
+    # screened path with d and k off every tile multiple (29 dims, 70 centroids)
+    pytest.param(70000, 70, 29, 0.7, 1, 6, marks=pytest.mark.slow)])
 def test_kmeans_bit_exact(sc, n, k, d, spread, restarts, max_iter):
     X = _features(n + k, n, k, d, spread)
     u = np.stack([scinputs.uniforms(7, k, offset=k * r) for r in range(restarts)])
@@ -396,6 +398,33 @@ def test_kmeans_bit_exact(sc, n, k, d, spread, restarts, max_iter):
     assert np.array_equal(C, Co)             # exactly rounded member sums -> identical centroids
     assert best == ro and it == ito
     assert inertia == pytest.approx(io, rel=1e-12)
+
+
+@pytest.mark.parametrize("case", ["k1", "k_eq_n", "d1", "three_distinct_rows"])
+def test_kmeans_edge_cases(sc, case):
+    """Degenerate k-means inputs: one cluster, one point per cluster, one dimension, and
+    fewer distinct points than clusters (D^2 total reaches 0 -> uniform draws, duplicate
+    centres, empty clusters keep their centre, tied distances -> lowest index)."""
+    rng = np.random.default_rng(11)
+    if case == "k1":
+        X, k = rng.standard_normal((50, 3)).astype(np.float32), 1
+    elif case == "k_eq_n":
+        X, k = rng.standard_normal((40, 2)).astype(np.float32), 40
+    elif case == "d1":
+        X, k = rng.standard_normal((300, 1)).astype(np.float32), 5
+    else:
+        base = rng.standard_normal((3, 4)).astype(np.float32)
+        X, k = base[rng.integers(0, 3, 200)], 5
+    n, d = X.shape
+    u = np.stack([scinputs.uniforms(5, k, offset=k * r) for r in range(3)])
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    C = np.zeros((k, d), dtype=np.float64)
+    inertia, it, best = sc.sc_kmeans(torch.from_numpy(X).cuda(), n, d, k, 3, 100, 0, u, lab, C)
+    lo, Co, io, ito, ro, _ = kmeans.kmeans(X, k, u, 100)
+    assert np.array_equal(lab.cpu().numpy(), lo)
+    assert np.array_equal(C, Co)
+    assert best == ro and it == ito
+    assert inertia == pytest.approx(io, rel=1e-12, abs=1e-300)
 
 
 def test_kmeans_on_filtered_features_and_default_uniforms(sc):
