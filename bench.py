@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cluster", action="store_true")
     ap.add_argument("--no-stability", action="store_true")
+    ap.add_argument("--no-prof", action="store_true", help="diagnostics: time without per-launch events")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="row-partitioned runs: halo rows stored by the step kernel into the peers (p2p, CUDA IPC "
+                         "over NVLink) or exchanged with NCCL send/recv")
     ap.add_argument("--dist-path", action="store_true",
                     help="use the row-partitioned NCCL filter even on one rank (exercises the multi-GPU path)")
     return ap.parse_args()
@@ -281,7 +285,16 @@ def run_ours(args):
         sc.sc_random_signals_f32(part.n_local, R, part.r0, args.seed, 0, 0.0, Xl)
         Xp = Xl[torch.as_tensor(part.perm, device=dev)].contiguous()   # the rank's local row order
         Yp = torch.empty_like(Xp)
-        nf = pdist.NcclFilter(part, handle)
+        exchange = args.exchange
+        if exchange == "p2p":
+            try:
+                nf = pdist.P2PFilter(part, handle, n, R)
+            except Exception as e:   # IPC mapping unavailable: the NCCL schedule instead
+                print(f"[bench] p2p exchange setup failed ({e}); using NCCL", file=sys.stderr)
+                exchange = f"nccl (p2p setup failed: {str(e)[:80]})"
+                nf = pdist.NcclFilter(part, handle)
+        else:
+            nf = pdist.NcclFilter(part, handle)
 
         def step():
             dd = sc.sc_cheby_coeffs(lam_k, lmax, order, w.jackson)
@@ -299,7 +312,8 @@ def run_ours(args):
     barrier()
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
-    sc.sc_profile_begin()
+    if not args.no_prof:
+        sc.sc_profile_begin()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if l2_resident:
@@ -324,6 +338,10 @@ def run_ours(args):
         ms = e0.elapsed_time(e1)
     launches, step_launches, kern_ms, algo_bytes = sc.sc_profile_end()
     clk = clocks.stop()
+    if args.no_prof:
+        if rank == 0:
+            print(json.dumps({"diagnostic": "no per-launch events", "ms_per_step": ms / args.steps}))
+        return
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -353,7 +371,7 @@ def run_ours(args):
             "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(base_config(args, g, w, world), lambda_max=lmax, lambda_cut=lam_k,
-                           lambda_cut_count=count_k),
+                           lambda_cut_count=count_k, **({"exchange": exchange} if partitioned else {})),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "cheb_step_kernel (fused SpMM + 3-term recurrence + Y accumulation)",
@@ -368,8 +386,32 @@ def run_ours(args):
             "clocks": clk,
         }
 
+    # ---- e2e through the C ABI with pinned host buffers, row-partitioned: every rank copies
+    # its local rows in and out; bytes are the whole job's, time the max over ranks
+    if partitioned and not args.no_e2e:
+        Xh = torch.empty((part.n_local, R), dtype=torch.float32, pin_memory=True)
+        Xh.copy_(Xp)
+        Yh = torch.empty((part.n_local, R), dtype=torch.float32, pin_memory=True)
+        for _ in range(2):
+            nf.filter(d, order, lmax, Xh, Yh)
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            nf.filter(d, order, lmax, Xh, Yh)
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        if rank == 0:
+            out["e2e"] = {"value": work / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(n * R * 4),
+                          "d2h_bytes_per_step": int(n * R * 4), "ms_per_step": ems / args.steps,
+                          "api": f"row-partitioned filter ({exchange}) with host X, Y on every rank"}
+
     # ---- e2e through the C ABI with pinned host buffers (single GPU)
-    if world == 1 and not args.no_e2e and rank == 0:
+    if world == 1 and not partitioned and not args.no_e2e and rank == 0:
         Xh = torch.empty((n, R), dtype=torch.float32, pin_memory=True)
         Xh.copy_(X)
         Yh = torch.empty((n, R), dtype=torch.float32, pin_memory=True)
@@ -439,6 +481,11 @@ def run_ours(args):
                                "seconds": dt}
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+    if partitioned:
+        torch.cuda.synchronize()
+        nf.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -317,6 +317,59 @@ int sc_dist_filter_f32(sc_dist* d, const double* coeffs, int order, double lambd
                        float* Y, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Row-partitioned filter with the halo exchange fused into the step kernel */
+/* (north_star: "exchanges the needed rows of T_j over NVLink ... overlapped */
+/* with the interior SpMM")                                */
+/* ------------------------------------------------------------------------ */
+
+typedef struct sc_p2p sc_p2p;     /* one rank's partition + peer-mapped T buffers */
+
+/*
+ * sc_p2p_create -- one rank of a row partition whose halo rows are delivered by the
+ * producing rank's step kernel (NVLink peer stores from its epilogue), not by a
+ * separate exchange.  g: the rank's local CSR (n_rows = n_local; columns >= n_local
+ * are the halo, grouped by owner rank, ascending).  Send descriptors, CSR by local
+ * row: row i is needed by peers sd_peer[e] at their halo slot sd_slot[e], e in
+ * [sd_ptr[i], sd_ptr[i+1]) (sd_ptr: n_local+1 entries; sd_row[e] = i repeats the row
+ * of entry e).  peer_n_local[q]: n_local of rank q.  n_global: rows of the whole
+ * graph (all ranks must agree; it fixes the common column-chunk plan).  max_R:
+ * widest block the partition will filter.  Arrays are copied (host or device).
+ * Allocates three (n_local + n_halo) x ceil4(max_R) fp32 buffers (cudaMalloc, CUDA
+ * IPC exportable) and a flag array.  world <= 8.
+ */
+int sc_p2p_create(sc_graph* g, int world, int rank, int64_t n_global, const int64_t* sd_ptr, const int64_t* sd_row,
+                  const int32_t* sd_peer, const int64_t* sd_slot, int64_t n_desc, const int64_t* peer_n_local,
+                  int max_R, sc_p2p** out);
+int sc_p2p_free(sc_p2p* p);
+
+/* sc_p2p_export -- CUDA IPC handles of the rank's three T buffers and its flag array:
+ * 4 x 64 bytes written to `handles`.  sc_p2p_import -- map peer `peer`'s buffers
+ * (the 256 bytes its export produced; cudaIpcOpenMemHandle, peer access enabled
+ * lazily).  sc_p2p_link_local -- same for a peer created in this process (single-GPU
+ * emulation and tests). */
+int sc_p2p_export(sc_p2p* p, void* handles);
+int sc_p2p_import(sc_p2p* p, int peer, const void* handles);
+int sc_p2p_link_local(sc_p2p* p, sc_p2p* peer);
+
+/*
+ * sc_p2p_filter_f32 -- this rank's rows of Y = sum_j coeffs[j] T_j(L~) X (as
+ * sc_dist_filter_f32; X, Y n_local x R in the local row order, host or device).
+ * One process per GPU; every rank must make the same sequence of calls.  Before each
+ * step the stream waits (one-warp kernel, acquire loads of the flags the peers
+ * publish when their previous step's stores have landed; traps after ~20 s without
+ * progress rather than hang).  R <= max_R.
+ *
+ * sc_p2p_filter_group_f32 -- all `world` ranks of a partition held by this process
+ * (ps[q] has rank q, peers linked with sc_p2p_link_local), device X[q] / Y[q]: the
+ * same kernels launched in a dependency order on one stream (step s of every rank,
+ * then step s+1), so nothing waits: the single-GPU emulation of the fused exchange.
+ */
+int sc_p2p_filter_f32(sc_p2p* p, const double* coeffs, int order, double lambda_max, int R, const float* X, float* Y,
+                      void* stream);
+int sc_p2p_filter_group_f32(sc_p2p* const* ps, int world, const double* coeffs, int order, double lambda_max, int R,
+                            const float* const* X, float* const* Y, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Instrumentation (bench.py)                                               */
 /* ------------------------------------------------------------------------ */
 

@@ -79,6 +79,15 @@ _F = {
     "sc_dist_create": _sig("sc_dist_create", c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, P(c_vp)),
     "sc_dist_free": _sig("sc_dist_free", c_vp),
     "sc_dist_filter_f32": _sig("sc_dist_filter_f32", c_vp, c_vp, c_i32, c_dbl, c_i32, c_vp, c_vp, c_vp),
+    "sc_p2p_create": _sig("sc_p2p_create", c_vp, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i32,
+                          P(c_vp)),
+    "sc_p2p_free": _sig("sc_p2p_free", c_vp),
+    "sc_p2p_export": _sig("sc_p2p_export", c_vp, c_vp),
+    "sc_p2p_import": _sig("sc_p2p_import", c_vp, c_i32, c_vp),
+    "sc_p2p_link_local": _sig("sc_p2p_link_local", c_vp, c_vp),
+    "sc_p2p_filter_f32": _sig("sc_p2p_filter_f32", c_vp, c_vp, c_i32, c_dbl, c_i32, c_vp, c_vp, c_vp),
+    "sc_p2p_filter_group_f32": _sig("sc_p2p_filter_group_f32", c_vp, c_i32, c_vp, c_i32, c_dbl, c_i32, c_vp, c_vp,
+                                    c_vp),
     "sc_profile_begin": _sig("sc_profile_begin"),
     "sc_profile_end": _sig("sc_profile_end", P(c_i64), P(c_i64), P(c_dbl), P(c_dbl)),
 }
@@ -304,6 +313,54 @@ def sc_dist_free(d):
 def sc_dist_filter_f32(d, coeffs, order, lambda_max, R, X, Y, stream=None):
     coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
     _check(_F["sc_dist_filter_f32"](d, coeffs.ctypes.data, order, lambda_max, R, _ptr(X), _ptr(Y), _stream(stream)))
+
+
+def sc_p2p_create(g, world, rank, n_global, sd_ptr, sd_row, sd_peer, sd_slot, peer_n_local, max_R):
+    sp = np.ascontiguousarray(sd_ptr, dtype=np.int64)
+    sr = np.ascontiguousarray(sd_row, dtype=np.int64)
+    pe = np.ascontiguousarray(sd_peer, dtype=np.int32)
+    sl = np.ascontiguousarray(sd_slot, dtype=np.int64)
+    nl = np.ascontiguousarray(peer_n_local, dtype=np.int64)
+    h = c_vp()
+    nd = int(sr.size)
+    _check(_F["sc_p2p_create"](g, world, rank, n_global, sp.ctypes.data, sr.ctypes.data if nd else None,
+                               pe.ctypes.data if nd else None, sl.ctypes.data if nd else None, nd, nl.ctypes.data,
+                               max_R, ctypes.byref(h)))
+    return h.value
+
+
+def sc_p2p_free(p):
+    _check(_F["sc_p2p_free"](p))
+
+
+def sc_p2p_export(p) -> bytes:
+    buf = ctypes.create_string_buffer(256)
+    _check(_F["sc_p2p_export"](p, ctypes.addressof(buf)))
+    return buf.raw
+
+
+def sc_p2p_import(p, peer, handles: bytes):
+    buf = ctypes.create_string_buffer(bytes(handles), 256)
+    _check(_F["sc_p2p_import"](p, peer, ctypes.addressof(buf)))
+
+
+def sc_p2p_link_local(p, peer):
+    _check(_F["sc_p2p_link_local"](p, peer))
+
+
+def sc_p2p_filter_f32(p, coeffs, order, lambda_max, R, X, Y, stream=None):
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    _check(_F["sc_p2p_filter_f32"](p, coeffs.ctypes.data, order, lambda_max, R, _ptr(X), _ptr(Y), _stream(stream)))
+
+
+def sc_p2p_filter_group_f32(ps, coeffs, order, lambda_max, R, Xs, Ys, stream=None):
+    world = len(ps)
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    pa = (c_vp * world)(*ps)
+    xa = (c_vp * world)(*[_ptr(x) for x in Xs])
+    ya = (c_vp * world)(*[_ptr(y) for y in Ys])
+    _check(_F["sc_p2p_filter_group_f32"](ctypes.addressof(pa), world, coeffs.ctypes.data, order, lambda_max, R,
+                                         ctypes.addressof(xa), ctypes.addressof(ya), _stream(stream)))
 
 
 def sc_profile_begin():

@@ -400,6 +400,17 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
         tn[w] = a * lt + bc * own[w] + bp * prv[w];      // T_{s+1}[i]
       }
       if (tnext) Vec<T>::st(tnext + row * p.ld_next + c, tn);   // T_{s+1} is gathered next step: normal L2 policy
+      if (p.p2p && tnext && row >= p.p2p->row0) {
+        // fused halo exchange: the peers that read this row get it straight into their halo
+        // (NVLink stores from the epilogue, no pack / send / receive)
+        const P2PDev* x = p.p2p;
+        const int64_t e1 = x->sd_ptr[row + 1];
+        for (int64_t e = x->sd_ptr[row]; e < e1; ++e) {
+          const int q = x->sd_peer[e];
+          T* dst = static_cast<T*>(x->peer_buf[p.p2p_next][q]) + (x->peer_nl[q] + x->sd_slot[e]) * p.ld_next + c;
+          Vec<T>::st(dst, tn);
+        }
+      }
       if (p.y_mode) {
         const T cyp = static_cast<T>(p.cy_prev), cyc = static_cast<T>(p.cy_cur), cyn = static_cast<T>(p.cy_next);
 #pragma unroll
@@ -414,6 +425,24 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
           m_nc += n * o;
           m_nn += n * n;
         }
+      }
+    }
+  }
+
+  if (p.p2p) {
+    // publish completion to the peers: every consumer thread fences its (remote) stores,
+    // the last CTA to finish writes p2p_signal into each peer's flag array (release)
+    __threadfence_system();
+    asm volatile("bar.sync 2, %0;" ::"r"(kNC * 32) : "memory");
+    if (threadIdx.x == 0) {
+      const P2PDev* x = p.p2p;
+      if (atomicAdd(x->done_ctr, 1u) == gridDim.x - 1) {
+        *x->done_ctr = 0u;
+        __threadfence_system();
+        for (int q = 0; q < x->world; ++q)
+          if (q != x->rank)
+            asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(x->peer_flags[q] + x->rank), "l"(p.p2p_signal)
+                         : "memory");
       }
     }
   }

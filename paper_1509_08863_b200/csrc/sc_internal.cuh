@@ -177,6 +177,26 @@ namespace sc {
 // ---------------------------------------------------------------------------
 // kernels / drivers (defined in the .cu files)
 // ---------------------------------------------------------------------------
+// Fused peer-to-peer halo exchange (sc_p2p.cu): device-side description of where a rank's
+// boundary rows go.  Row i of this rank is needed by the peers listed in
+// [sd_ptr[i], sd_ptr[i+1]): peer sd_peer[e] keeps it at halo slot sd_slot[e], i.e. row
+// peer_nl[q] + sd_slot[e] of its buffers.  peer_buf[b][q] is peer q's T buffer b (b = 0, 1, 2)
+// mapped into this process (NVLink peer memory via CUDA IPC, or local memory in the
+// single-GPU emulation); peer_flags[q] is peer q's flag array ([world] int64, written by
+// rank r at index r).
+struct P2PDev {
+  const int64_t* sd_ptr;
+  const int32_t* sd_peer;
+  const int64_t* sd_slot;
+  const int64_t* peer_nl;
+  void* peer_buf[3][8];
+  int64_t* peer_flags[8];
+  unsigned* done_ctr;
+  int64_t row0;      // rows below row0 have no descriptors (interior rows)
+  int rank, world;
+};
+constexpr int kP2PMaxWorld = 8;
+
 struct StepParams {
   int64_t row_begin, row_end;
   const void* tprev; int64_t ld_prev;
@@ -190,6 +210,11 @@ struct StepParams {
   int total_width;   // all columns of the block (for the profiler's CSR share)
   // moments mode (fp64 only): per-block partial sums written to `part`
   double* part;      // [gridDim.x][3] : <Tc,Tc>, <Tn,Tc>, <Tn,Tn>
+  // fused exchange (nullptr: none): T_{s+1} rows also stored into the peers' buffer
+  // p2p_next; after the launch the last CTA publishes p2p_signal in every peer's flags
+  const P2PDev* p2p;
+  int p2p_next;
+  int64_t p2p_signal;
 };
 
 // launch one fused step for `width` columns starting at the given pointers

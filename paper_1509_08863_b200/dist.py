@@ -263,3 +263,121 @@ class NcclFilter:
         if getattr(self, "comm", None):
             self._lib.sc_comm_free(self.comm)
             self.comm = None
+
+
+# ---------------------------------------------------------------------------
+# fused peer-to-peer exchange (sc_p2p_*): descriptors and drivers
+# ---------------------------------------------------------------------------
+
+def p2p_descriptors(part: LocalPart, recv_counts_all):
+    """Where each of this rank's rows goes in the peers' halos, CSR by local row.
+
+    recv_counts_all[q][r] = rows rank q receives from rank r.  Rank q's halo is grouped by
+    owner in ascending rank order and, inside an owner's block, in ascending global id --
+    the order of the owner's send list to q -- so row send_idx[q][j] lands at q's halo slot
+    sum(recv_counts_all[q][:rank]) + j.  Returns (sd_ptr, sd_row, sd_peer, sd_slot)."""
+    r, nl = part.rank, part.n_local
+    rows, peers, slots = [], [], []
+    so = 0
+    for q in range(part.world):
+        cnt = int(part.send_counts[q])
+        if q == r or cnt == 0:
+            so += cnt
+            continue
+        base = int(sum(recv_counts_all[q][:r]))
+        rows.append(np.asarray(part.send_idx[so:so + cnt], dtype=np.int64))
+        peers.append(np.full(cnt, q, dtype=np.int32))
+        slots.append(base + np.arange(cnt, dtype=np.int64))
+        so += cnt
+    if rows:
+        row = np.concatenate(rows)
+        peer = np.concatenate(peers)
+        slot = np.concatenate(slots)
+        o = np.argsort(row, kind="stable")
+        row, peer, slot = row[o], peer[o], slot[o]
+    else:
+        row = np.zeros(0, np.int64)
+        peer = np.zeros(0, np.int32)
+        slot = np.zeros(0, np.int64)
+    ptr = np.zeros(nl + 1, dtype=np.int64)
+    np.cumsum(np.bincount(row, minlength=nl), out=ptr[1:])
+    return ptr, row, peer, slot
+
+
+def p2p_scatter_reference(parts, T_locals):
+    """Host model of the fused exchange (tests): every rank's descriptors applied to its
+    local rows; returns each rank's halo block."""
+    rc_all = [p.recv_counts for p in parts]
+    halos = [np.zeros((p.n_halo,) + T_locals[p.rank].shape[1:], dtype=T_locals[p.rank].dtype) for p in parts]
+    for p in parts:
+        ptr, row, peer, slot = p2p_descriptors(p, rc_all)
+        for e in range(row.size):
+            halos[int(peer[e])][int(slot[e])] = T_locals[p.rank][int(row[e])]
+    return halos
+
+
+class P2PFilter:
+    """One rank of the fused-exchange filter (one process per GPU): descriptors from the
+    all-gathered receive counts, CUDA IPC handles of every rank's T buffers exchanged with
+    torch.distributed, then sc_p2p_filter_f32 per call."""
+
+    def __init__(self, part: LocalPart, graph_handle, n_global: int, max_R: int, group=None):
+        import torch.distributed as dist
+        from . import _lib as sc
+        self.part, self.sc = part, sc
+        w = part.world
+        rc_all, nl_all, hs = [list(part.recv_counts)], [int(part.n_local)], [None]
+        if w > 1:
+            rc_all, nl_all, hs = [None] * w, [None] * w, [None] * w
+            dist.all_gather_object(rc_all, list(part.recv_counts), group=group)
+            dist.all_gather_object(nl_all, int(part.n_local), group=group)
+        sd = p2p_descriptors(part, rc_all)
+        self.handle = sc.sc_p2p_create(graph_handle, w, part.rank, n_global, *sd, nl_all, max_R)
+        if w > 1:
+            dist.all_gather_object(hs, sc.sc_p2p_export(self.handle), group=group)
+            for q in range(w):
+                if q != part.rank:
+                    sc.sc_p2p_import(self.handle, q, hs[q])
+            dist.barrier(group=group)
+
+    def filter(self, d, order, lambda_max, X, Y, stream=None):
+        self.sc.sc_p2p_filter_f32(self.handle, d, order, lambda_max, X.shape[1], X, Y, stream)
+
+    def close(self):
+        if self.handle:
+            self.sc.sc_p2p_free(self.handle)
+            self.handle = None
+
+
+class P2PGroup:
+    """All ranks of a row partition in one process on one GPU (single-GPU emulation of the
+    fused exchange, tests): sc_p2p_filter_group_f32 runs the same kernels in dependency
+    order on one stream."""
+
+    def __init__(self, row_ptr, col_idx, values, n: int, world: int, max_R: int):
+        from . import _lib as sc
+        from . import Graph
+        self.sc = sc
+        parts = [local_part(row_ptr, col_idx, values, n, r, world) for r in range(world)]
+        halos = [p.halo_gid for p in parts]
+        self.parts = [send_lists_from_halos(p, halos) for p in parts]
+        rc_all = [p.recv_counts for p in self.parts]
+        nl_all = [p.n_local for p in self.parts]
+        self.graphs = [Graph(p.n_local, p.row_ptr, p.col_idx, p.values, n_cols=p.n_local + p.n_halo)
+                       for p in self.parts]
+        self.handles = [sc.sc_p2p_create(self.graphs[r].handle, world, r, n, *p2p_descriptors(self.parts[r], rc_all),
+                                         nl_all, max_R) for r in range(world)]
+        for a in range(world):
+            for b in range(world):
+                if a != b:
+                    sc.sc_p2p_link_local(self.handles[a], self.handles[b])
+
+    def filter(self, d, order, lambda_max, Xs, Ys, stream=None):
+        self.sc.sc_p2p_filter_group_f32(self.handles, d, order, lambda_max, Xs[0].shape[1], Xs, Ys, stream)
+
+    def close(self):
+        for h in self.handles:
+            self.sc.sc_p2p_free(h)
+        self.handles = []
+        for g in self.graphs:
+            g.close()

@@ -114,3 +114,69 @@ def test_partition_and_schedule_pure():
                 seen[s] += st["cy_cur"]
                 seen[s + 1] += st["cy_next"]
         assert np.array_equal(seen, d)
+
+
+# ---------------------------------------------------------------------------
+# fused peer-to-peer exchange: the descriptors a rank's step kernel uses to store its
+# boundary rows straight into the peers' halos (sc_p2p_*)
+# ---------------------------------------------------------------------------
+
+def _p2p_worker(rank, world, port, gspec, R, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_08863_b200 import dist as pdist
+        g = scinputs.sbm(**gspec)
+        part = pdist.exchange_send_lists(pdist.local_part(g.row_ptr, g.col_idx, g.values, g.n, rank, world))
+        rc_all = [None] * world
+        dist.all_gather_object(rc_all, list(part.recv_counts))
+        ptr, row, peer, slot = pdist.p2p_descriptors(part, rc_all)
+        X = scinputs.gaussian_block(9, g.n, R)
+        T_local = X[part.r0:part.r1][part.perm]            # this rank's rows, local (permuted) order
+        out = [(int(peer[e]), int(slot[e]), T_local[int(row[e])]) for e in range(row.size)]
+        sent = [None] * world
+        dist.all_gather_object(sent, out)
+        halo = np.full((part.n_halo, R), np.nan, dtype=X.dtype)
+        writes = np.zeros(part.n_halo, dtype=int)
+        for lst in sent:
+            for pq, sl, v in lst:
+                if pq == rank:
+                    halo[sl] = v
+                    writes[sl] += 1
+        ok = (np.all(writes == 1) and np.array_equal(halo, X[part.halo_gid])
+              and np.all(np.diff(ptr) >= 0) and ptr[-1] == row.size and np.all(np.diff(row) >= 0)
+              and np.all(peer != rank))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_descriptors_fill_every_halo_exactly_once_gloo(world):
+    gspec = dict(n=900, k=3, avg_degree=8, eps=0.1, seed=4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, gspec, 4, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=10) for _ in range(world))
+    assert all(res[r] for r in range(world))
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 5])
+def test_p2p_scatter_reference_reproduces_halos(world):
+    from paper_1509_08863_b200 import dist as pdist
+    g = scinputs.sbm(700, 5, 6, 0.2, seed=6)
+    parts = [pdist.local_part(g.row_ptr, g.col_idx, g.values, g.n, r, world) for r in range(world)]
+    halos = [p.halo_gid for p in parts]
+    parts = [pdist.send_lists_from_halos(p, halos) for p in parts]
+    X = scinputs.gaussian_block(2, g.n, 3)
+    T_locals = [X[p.r0:p.r1][p.perm] for p in parts]
+    got = pdist.p2p_scatter_reference(parts, T_locals)
+    for p, h in zip(parts, got):
+        assert np.array_equal(h, X[p.halo_gid])

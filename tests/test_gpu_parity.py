@@ -572,6 +572,111 @@ def test_row_partitioned_steps_emulated_two_ranks(sc):
     assert rel(Yfull, Yo) <= F32_TOL
 
 
+@pytest.mark.parametrize("world,R,chunk", [(2, 16, None), (3, 6, None), (4, 16, "8"), (2, 12, "4"), (1, 8, None)])
+def test_p2p_fused_exchange_emulated(sc, world, R, chunk, monkeypatch):
+    """The fused-exchange filter (sc_p2p_*): every rank's step kernel stores its boundary rows
+    of T_{s+1} straight into the peers' halos.  All ranks held by this process on one GPU
+    (sc_p2p_filter_group_f32: dependency-ordered launches on one stream, nothing waits), incl.
+    several column chunks, a ragged R and world 1 -- vs the oracle on the whole graph."""
+    from paper_1509_08863_b200 import dist as pdist
+    if chunk:
+        monkeypatch.setenv("SC_CHUNK", chunk)
+    g = scinputs.sbm(3000, 6, 10, 0.1, seed=21)
+    order = 30
+    L = laplacian.laplacian(g)
+    lmax = 2.0 * float(g.degrees().max())
+    d = chebyshev.filter_coeffs(0.15 * lmax, lmax, order, True)
+    X = scinputs.gaussian_block(4, g.n, R)
+    grp = pdist.P2PGroup(g.row_ptr, g.col_idx, g.values, g.n, world, R)
+    try:
+        Xs = [torch.from_numpy(np.ascontiguousarray(X[p.r0:p.r1][p.perm])).cuda() for p in grp.parts]
+        Ys = [torch.full_like(x, float("nan")) for x in Xs]
+        for _ in range(2):                     # twice: call-spanning signal counters, buffer reuse
+            grp.filter(d, order, lmax, Xs, Ys)
+            torch.cuda.synchronize()
+            Y = np.zeros((g.n, R))
+            for p, y in zip(grp.parts, Ys):
+                Y[p.r0 + p.perm] = y.cpu().numpy()
+            Yo = chebyshev.cheb_filter(L, X.astype(np.float64), d, lmax)
+            assert rel(Y, Yo) <= F32_TOL
+        if world > 1:
+            assert all(p.n_halo > 0 for p in grp.parts)
+    finally:
+        grp.close()
+
+
+def test_p2p_filter_single_rank_host_buffers(sc):
+    """sc_p2p_filter_f32 (the multi-process entry point: chunk-start waits, T_0 push,
+    signalled steps) on a 1-rank partition with host X / Y, incl. a ragged R."""
+    from paper_1509_08863_b200 import dist as pdist
+    g = scinputs.sbm(2500, 3, 12, 0.05, seed=34)
+    part = pdist.local_part(g.row_ptr, g.col_idx, g.values, g.n, 0, 1)
+    part = pdist.send_lists_from_halos(part, [part.halo_gid])
+    G = sc.Graph(part.n_local, part.row_ptr, part.col_idx, part.values, n_cols=part.n_local + part.n_halo)
+    pf = pdist.P2PFilter(part, G.handle, g.n, 32)
+    lmax = 2.0 * float(g.degrees().max())
+    L = laplacian.laplacian(g)
+    try:
+        for R, order in [(32, 25), (13, 7)]:
+            d = chebyshev.filter_coeffs(0.1 * lmax, lmax, order, True)
+            X = scinputs.gaussian_block(6, g.n, R)
+            Xp = np.ascontiguousarray(X[part.perm])
+            Yp = np.zeros_like(Xp)
+            pf.filter(d, order, lmax, Xp, Yp)
+            Y = np.empty((g.n, R))
+            Y[part.perm] = Yp
+            Yo = chebyshev.cheb_filter(L, X.astype(np.float64), d, lmax)
+            assert rel(Y, Yo) <= F32_TOL
+    finally:
+        pf.close()
+
+
+def _ipc_worker(rank, world, port, q):
+    import torch.distributed as tdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch as th
+        th.cuda.set_device(0)
+        import paper_1509_08863_b200 as scm
+        from paper_1509_08863_b200 import dist as pdist
+        g = scinputs.sbm(1200, 3, 8, 0.1, seed=8)
+        part = pdist.exchange_send_lists(pdist.local_part(g.row_ptr, g.col_idx, g.values, g.n, rank, world))
+        G = scm.Graph(part.n_local, part.row_ptr, part.col_idx, part.values, n_cols=part.n_local + part.n_halo)
+        pf = pdist.P2PFilter(part, G.handle, g.n, 8)     # export, all-gather, cudaIpcOpenMemHandle
+        tdist.barrier()
+        pf.close()
+        tdist.barrier()
+        q.put((rank, True))
+    except Exception as e:
+        q.put((rank, repr(e)))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_p2p_ipc_handles_map_across_processes(sc):
+    """Two processes exchange and open each other's CUDA IPC handles (the mapping step of
+    the multi-GPU path; both on this GPU, so no filter runs: its steps would wait on each
+    other)."""
+    import socket
+    import torch.multiprocessing as tmp
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}, res
+
+
 def test_nccl_dist_filter_single_rank(sc):
     """sc_dist_filter_f32 end to end on one rank (NCCL communicator of size 1, no halo):
     the library-side multi-GPU schedule against the oracle, incl. a ragged R."""
