@@ -290,8 +290,10 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int64_t m = list ? (int64_t)*list_len : n;
-  const int64_t p0 = (int64_t)blockIdx.x * kAT;
-  if (p0 >= m) return;
+  // grid-stride over 64-point tiles (list mode is launched with a bounded grid: the list
+  // length is only known on the device)
+  for (int64_t p0 = (int64_t)blockIdx.x * kAT; p0 < m; p0 += (int64_t)gridDim.x * kAT) {
+  __syncthreads();   // previous tile's shared-memory reads done
   for (int e = tid; e < kAT * d; e += 256) {
     const int row = e / d, q = e - row * d;
     const int64_t pi = p0 + row;
@@ -372,6 +374,7 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
     lab[gi] = bl;
     dmin[gi] = bv;
     lo[gi] = sqrt(sv);
+  }
   }
 }
 
@@ -924,6 +927,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   const int smem_assign = (int)(sizeof(double) * 2 * (size_t)d * kAT);
   if (smem_assign > 200 * 1024) return fail(SC_ERR_ARG, "sc_kmeans: d must be <= 200");
   const int64_t nblk = (n + kAT - 1) / kAT;
+  const int64_t list_grid = std::min<int64_t>(nblk, (int64_t)sms * 4);   // list-mode scans: grid-stride
   constexpr int64_t kChunk = 512;    // members per exact-sum work item
   const int64_t max_items = 2 * n / kChunk + k + 1;   // (incremental lists: 2 entries per changed point)
   PoolBuf b_lab, b_new, b_d2, b_C, b_cnt, b_cur, b_off, b_perm, b_items, b_part, b_psum, b_misc;
@@ -1039,7 +1043,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
           F, n, d, C, d_Cf, d_cm, k, pruned ? b_list.as<int32_t>() : nullptr, pruned ? b_len.as<int>() : nullptr,
           out_lab, b_dmin.as<double>(), b_lo.as<double>(), b_amb.as<int32_t>(), amb_len);
       SC_CUDA_TRY(cudaGetLastError());
-      assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, b_amb.as<int32_t>(), amb_len, out_lab,
+      assign3_kernel<<<(unsigned)list_grid, 256, smem_assign, s>>>(F, n, d, C, k, b_amb.as<int32_t>(), amb_len, out_lab,
                                                              b_dmin.as<double>(), b_lo.as<double>());
       if (trace_len) {
         int h_len[3] = {0, 0, 0};
@@ -1060,7 +1064,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
           F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(), b_lo.as<double>(),
           b_list.as<int32_t>(), b_len.as<int>());
       SC_CUDA_TRY(cudaGetLastError());
-      assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, b_list.as<int32_t>(), b_len.as<int>(),
+      assign3_kernel<<<(unsigned)list_grid, 256, smem_assign, s>>>(F, n, d, C, k, b_list.as<int32_t>(), b_len.as<int>(),
                                                              out_lab, b_dmin.as<double>(), b_lo.as<double>());
       if (trace_len) {
         int h_len = 0;
