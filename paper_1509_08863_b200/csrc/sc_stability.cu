@@ -12,6 +12,9 @@
 // library's own kernels.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -61,6 +64,52 @@ __global__ void pad_copy_kernel(const float* __restrict__ src, int64_t n, int R,
     const int64_t i = idx / ld;
     const int q = static_cast<int>(idx - i * ld);
     dst[idx] = q < R ? src[i * R + q] : 0.f;
+  }
+}
+
+// ARI of every replicate pair of every cut (§4.3 Eq.(11); same formula and
+// degenerate-case rule as ari_dev / the oracle, R9): block = one pair (cut c,
+// replicates a < b), contingency table of the two labelings in shared memory (labels of cut
+// c are in [0, k_min + c)), then the pair-count sums in fp64 by one thread.
+__global__ void pair_ari_kernel(const int32_t* __restrict__ labels, int64_t n, int J, int k_min,
+                                const int2* __restrict__ pairs_of, const int* __restrict__ cut_of,
+                                double* __restrict__ out) {
+  extern __shared__ unsigned tab[];
+  const int pid = blockIdx.x;
+  const int c = cut_of[pid];
+  const int2 ab = pairs_of[pid];
+  const int k = k_min + c;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) tab[e] = 0u;
+  __syncthreads();
+  const int32_t* la = labels + ((size_t)c * J + ab.x) * n;
+  const int32_t* lb = labels + ((size_t)c * J + ab.y) * n;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&tab[la[i] * k + lb[i]], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    auto c2 = [](double x) { return x * (x - 1.0) / 2.0; };
+    double sum_ij = 0.0, sa = 0.0, sb = 0.0;
+    int64_t nnz = 0;
+    int nra = 0, ncb = 0;
+    for (int i = 0; i < k; ++i) {
+      double ra = 0.0;
+      for (int j = 0; j < k; ++j) {
+        const double v = (double)tab[i * k + j];
+        if (v > 0) ++nnz;
+        sum_ij += c2(v);
+        ra += v;
+      }
+      sa += c2(ra);
+      nra += ra > 0;
+    }
+    for (int j = 0; j < k; ++j) {
+      double cb = 0.0;
+      for (int i = 0; i < k; ++i) cb += (double)tab[i * k + j];
+      sb += c2(cb);
+      ncb += cb > 0;
+    }
+    const double expected = n > 1 ? sa * sb / c2((double)n) : 0.0;
+    const double denom = 0.5 * (sa + sb) - expected;
+    out[pid] = denom == 0.0 ? ((nra == ncb && nnz == nra) ? 1.0 : 0.0) : (sum_ij - expected) / denom;
   }
 }
 
@@ -129,8 +178,12 @@ int stability_scan(sc_graph* g, int k_min, int k_max, int J, int R, int order, b
   int dev = 0;
   cudaGetDevice(&dev);
 
+  const bool trace = std::getenv("SC_STABILITY_TRACE") != nullptr;
+  auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double t_filter = 0.0, t_kmeans = 0.0, t_mark = now();
   for (int j0 = 0; j0 < J; j0 += Jg) {
     const int jn = std::min(Jg, J - j0);
+    if (trace) t_mark = now();
     // 3a. recurrence + every cut's features for replicates j0 .. j0+jn-1 (stream s)
     for (int jj = 0; jj < jn; ++jj) {
       const uint64_t sj = seed + (uint64_t)(j0 + jj);
@@ -174,6 +227,7 @@ int stability_scan(sc_graph* g, int k_min, int k_max, int J, int R, int order, b
         SC_CUDA_TRY(cudaGetLastError());
       }
     }
+    if (trace) { SC_CUDA_TRY(cudaStreamSynchronize(s)); t_filter += now() - t_mark; t_mark = now(); }
     cudaEvent_t ready;
     SC_CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     SC_CUDA_TRY(cudaEventRecord(ready, s));
@@ -218,18 +272,59 @@ int stability_scan(sc_graph* g, int k_min, int k_max, int J, int R, int order, b
     for (auto& th : pool) th.join();
     cudaEventDestroy(ready);
     if (err_code != SC_OK) return fail(err_code, "sc_stability k-means worker: " + err_msg);
+    if (trace) t_kmeans += now() - t_mark;
   }
-  // 4. gamma(k) = 2/(J(J-1)) sum_{a<b} ari(C^a, C^b)   (R7)
-  for (int c = 0; c < K; ++c) {
-    double tot = 0.0;
-    for (int a = 0; a < J; ++a)
-      for (int b = a + 1; b < J; ++b) {
-        double v = 0.0;
-        SC_TRY(ari_dev(labels_dev + ((size_t)c * J + a) * n, labels_dev + ((size_t)c * J + b) * n, n, &v, s));
-        tot += v;
-      }
-    gamma[c] = 2.0 * tot / ((double)J * (J - 1));
+  if (trace) t_mark = now();
+  // 4. gamma(k) = 2/(J(J-1)) sum_{a<b} ari(C^a, C^b)   (R7): every pair's ARI in one
+  // launch when the contingency tables fit shared memory, else pair by pair
+  if ((size_t)k_max * k_max * sizeof(unsigned) <= 96 * 1024) {
+    std::vector<int2> pr;
+    std::vector<int> cut;
+    for (int c = 0; c < K; ++c)
+      for (int a = 0; a < J; ++a)
+        for (int b = a + 1; b < J; ++b) {
+          pr.push_back(make_int2(a, b));
+          cut.push_back(c);
+        }
+    const int np = (int)pr.size();
+    std::vector<double> aris(np, 0.0);
+    if (np) {
+      DevBuf dp, dc, da;
+      SC_TRY(dp.ensure(sizeof(int2) * np));
+      SC_TRY(dc.ensure(sizeof(int) * np));
+      SC_TRY(da.ensure(sizeof(double) * np));
+      SC_CUDA_TRY(cudaMemcpyAsync(dp.ptr, pr.data(), sizeof(int2) * np, cudaMemcpyHostToDevice, s));
+      SC_CUDA_TRY(cudaMemcpyAsync(dc.ptr, cut.data(), sizeof(int) * np, cudaMemcpyHostToDevice, s));
+      const int smem = (int)(sizeof(unsigned) * k_max * k_max);
+      if (smem > 48 * 1024)
+        SC_CUDA_TRY(cudaFuncSetAttribute(pair_ari_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      pair_ari_kernel<<<np, 256, smem, s>>>(labels_dev, n, J, k_min, dp.as<int2>(), dc.as<int>(), da.as<double>());
+      SC_CUDA_TRY(cudaGetLastError());
+      SC_CUDA_TRY(cudaMemcpyAsync(aris.data(), da.ptr, sizeof(double) * np, cudaMemcpyDeviceToHost, s));
+      SC_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    int i = 0;
+    for (int c = 0; c < K; ++c) {
+      double tot = 0.0;
+      for (int a = 0; a < J; ++a)
+        for (int b = a + 1; b < J; ++b) tot += aris[i++];
+      gamma[c] = 2.0 * tot / ((double)J * (J - 1));
+    }
+  } else {
+    for (int c = 0; c < K; ++c) {
+      double tot = 0.0;
+      for (int a = 0; a < J; ++a)
+        for (int b = a + 1; b < J; ++b) {
+          double v = 0.0;
+          SC_TRY(ari_dev(labels_dev + ((size_t)c * J + a) * n, labels_dev + ((size_t)c * J + b) * n, n, &v, s));
+          tot += v;
+        }
+      gamma[c] = 2.0 * tot / ((double)J * (J - 1));
+    }
   }
+  if (trace)
+    std::fprintf(stderr, "[sc_stability] J=%d groups of %d: recurrence+cuts %.4f s, k-means %.4f s, ARI %.4f s\n", J, Jg,
+                 t_filter, t_kmeans, now() - t_mark);
   return SC_OK;
 }
 
