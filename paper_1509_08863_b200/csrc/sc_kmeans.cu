@@ -279,6 +279,9 @@ constexpr int kAT = 64;   // points per block and centroids per tile
 // Full scan of the points in `list` (or all points when list == nullptr): exact argmin
 // (first minimum) and the second-smallest distance, which becomes the point's lower bound
 // lo_i = sqrt(second) for the pruning test of the next iterations (check_kernel).
+// NC centroids per thread (tx, tx+16, ...): centroid tiles of 16 NC columns, so small k is not
+// padded to 64 (k = 10 computes 16 columns, k = 20 or 30 computes 32)
+template <int NC>
 __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ F, int64_t n, int d,
                                                       const double* __restrict__ C, int k,
                                                       const int32_t* __restrict__ list, const int* __restrict__ list_len,
@@ -304,38 +307,41 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
   int bidx[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) { best[i] = INFINITY; second[i] = INFINITY; bidx[i] = -1; }
-  for (int c0 = 0; c0 < k; c0 += kAT) {
-    const int kt = min(kAT, k - c0);
+  constexpr int TW = 16 * NC;   // centroids per tile
+  for (int c0 = 0; c0 < k; c0 += TW) {
+    const int kt = min(TW, k - c0);
     __syncthreads();
-    for (int e = tid; e < kAT * d; e += 256) {
+    for (int e = tid; e < TW * d; e += 256) {
       const int cc = e / d, q = e - cc * d;
       sC[(size_t)q * kAT + cc] = cc < kt ? C[(size_t)(c0 + cc) * d + q] : 0.0;
     }
     __syncthreads();
-    double acc[4][4];
+    double acc[4][NC];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+      for (int j = 0; j < NC; ++j) acc[i][j] = 0.0;
 #pragma unroll 2
     for (int q = 0; q < d; ++q) {
       const double2 xa = *reinterpret_cast<const double2*>(sX + (size_t)q * kAT + ty * 4);
       const double2 xb = *reinterpret_cast<const double2*>(sX + (size_t)q * kAT + ty * 4 + 2);
-      // thread tx owns centroids tx, tx+16, tx+32, tx+48 of the tile: the 16 lanes of a row
-      // read 16 consecutive doubles per load (one wavefront, no bank conflicts)
+      // thread tx owns centroids tx, tx+16, ... of the tile: the 16 lanes of a row read 16
+      // consecutive doubles per load (one wavefront, no bank conflicts)
       const double* cq = sC + (size_t)q * kAT + tx;
       const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
-      const double cv[4] = {cq[0], cq[16], cq[32], cq[48]};
+      double cv[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) cv[j] = cq[16 * j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NC; ++j) {
           const double diff = __dsub_rn(xv[i], cv[j]);
           acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(diff, diff));
         }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NC; ++j) {
       const int cidx = tx + 16 * j;
       if (cidx < kt) {
 #pragma unroll
@@ -1001,7 +1007,17 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   if (amax > 0.0f) { std::frexp((double)amax, &E); }   // amax < 2^E
   const int shift = 100 - E;   // |x| 2^shift < 2^100; sums of < 2^25 members fit 2^125
 
-  SC_CUDA_TRY(cudaFuncSetAttribute(assign3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
+  // exact scan: the centroid tile width 16 NC with the fewest padded columns (ties: wider)
+  int nc_best = 4;
+  {
+    int best_cols = 1 << 30;
+    for (int nc : {4, 2, 1}) {
+      const int tw = 16 * nc, cols = (k + tw - 1) / tw * tw;
+      if (cols < best_cols) { best_cols = cols; nc_best = nc; }
+    }
+  }
+  auto assign3 = nc_best == 4 ? assign3_kernel<4> : nc_best == 2 ? assign3_kernel<2> : assign3_kernel<1>;
+  SC_CUDA_TRY(cudaFuncSetAttribute(assign3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
   const int smem_screen = (int)(sizeof(float) * (size_t)d * (kSLX + kSLC));
   SC_CUDA_TRY(cudaFuncSetAttribute(assign_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_screen));
   // the screen pays off when the exact scan is expensive (env SC_KMEANS_SCREEN=0 disables it)
@@ -1043,7 +1059,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
           F, n, d, C, d_Cf, d_cm, k, pruned ? b_list.as<int32_t>() : nullptr, pruned ? b_len.as<int>() : nullptr,
           out_lab, b_dmin.as<double>(), b_lo.as<double>(), b_amb.as<int32_t>(), amb_len);
       SC_CUDA_TRY(cudaGetLastError());
-      assign3_kernel<<<(unsigned)list_grid, 256, smem_assign, s>>>(F, n, d, C, k, b_amb.as<int32_t>(), amb_len, out_lab,
+      assign3<<<(unsigned)list_grid, 256, smem_assign, s>>>(F, n, d, C, k, b_amb.as<int32_t>(), amb_len, out_lab,
                                                              b_dmin.as<double>(), b_lo.as<double>());
       if (trace_len) {
         int h_len[3] = {0, 0, 0};
@@ -1054,7 +1070,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
       }
     } else if (!old || !prune) {
       // full scan of every point (the first assignment of a restart also sets the bounds lo)
-      assign3_kernel<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, nullptr, nullptr, out_lab,
+      assign3<<<(unsigned)nblk, 256, smem_assign, s>>>(F, n, d, C, k, nullptr, nullptr, out_lab,
                                                              b_dmin.as<double>(), b_lo.as<double>());
     } else {
       // Hamerly pruning: points whose assigned centroid is provably still the unique
@@ -1064,7 +1080,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
           F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(), b_lo.as<double>(),
           b_list.as<int32_t>(), b_len.as<int>());
       SC_CUDA_TRY(cudaGetLastError());
-      assign3_kernel<<<(unsigned)list_grid, 256, smem_assign, s>>>(F, n, d, C, k, b_list.as<int32_t>(), b_len.as<int>(),
+      assign3<<<(unsigned)list_grid, 256, smem_assign, s>>>(F, n, d, C, k, b_list.as<int32_t>(), b_len.as<int>(),
                                                              out_lab, b_dmin.as<double>(), b_lo.as<double>());
       if (trace_len) {
         int h_len = 0;
