@@ -1021,7 +1021,9 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   const int smem_screen = (int)(sizeof(float) * (size_t)d * (kSLX + kSLC));
   SC_CUDA_TRY(cudaFuncSetAttribute(assign_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_screen));
   // the screen pays off when the exact scan is expensive (env SC_KMEANS_SCREEN=0 disables it)
-  const bool screen = (double)n * k * d >= 134217728.0 && !(std::getenv("SC_KMEANS_SCREEN") && std::atoi(std::getenv("SC_KMEANS_SCREEN")) == 0);
+  const double screen_min = std::getenv("SC_KMEANS_SCREEN_MIN") ? std::atof(std::getenv("SC_KMEANS_SCREEN_MIN"))
+                                                                : 134217728.0;
+  const bool screen = (double)n * k * d >= screen_min && !(std::getenv("SC_KMEANS_SCREEN") && std::atoi(std::getenv("SC_KMEANS_SCREEN")) == 0);
   const int smem_rows = (int)(sizeof(float) * kSP * (d + 1));
   const int smem_d2 = smem_rows + (int)(sizeof(double) * d);
   SC_CUDA_TRY(cudaFuncSetAttribute(check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_rows));
