@@ -235,7 +235,7 @@ int stability_scan(sc_graph* g, int k_min, int k_max, int J, int R, int order, b
     // independent and individually too small to fill the GPU: worker threads, each with its
     // own stream and stream-ordered workspaces, run them concurrently
     const int ntask = jn * K;
-    const int nwork = std::min(ntask, 8);
+    const int nwork = std::min(ntask, std::getenv("SC_STABILITY_WORKERS") ? std::max(1, std::atoi(std::getenv("SC_STABILITY_WORKERS"))) : 8);
     std::atomic<int> next{0};
     std::mutex err_mu;
     int err_code = SC_OK;
