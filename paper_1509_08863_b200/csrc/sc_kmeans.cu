@@ -691,31 +691,9 @@ __device__ __forceinline__ bool full_gate(const int* chg, int64_t thresh) {
 }
 
 // members of cluster c land at perm[off[c] .. off[c+1]) (order inside a cluster is
-// arbitrary; the exact integer sums below do not depend on it).  A block takes a range of
-// points, ranks them per cluster in shared memory and reserves one slice per (block,
-// cluster) with a single global atomic.
-__global__ void scatter_members_kernel(const int32_t* __restrict__ lab, int64_t n, int k, int64_t per_block,
-                                       unsigned* __restrict__ cursor, const int64_t* __restrict__ off,
-                                       int32_t* __restrict__ perm, const int* __restrict__ chg, int64_t thresh) {
-  if (!full_gate(chg, thresh)) return;
-  extern __shared__ unsigned hist[];   // [k] local counts, then [k] bases
-  unsigned* base = hist + k;
-  for (int c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
-  __syncthreads();
-  const int64_t a = blockIdx.x * per_block, b = min(n, a + per_block);
-  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) atomicAdd(&hist[lab[i]], 1u);
-  __syncthreads();
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
-    base[c] = hist[c] ? atomicAdd(&cursor[c], hist[c]) : 0u;
-    hist[c] = 0;
-  }
-  __syncthreads();
-  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
-    const int c = lab[i];
-    perm[off[c] + base[c] + atomicAdd(&hist[c], 1u)] = static_cast<int32_t>(i);
-  }
-}
-
+// arbitrary; the exact integer sums below do not depend on it).  scatter_any_kernel (below)
+// ranks a block's points per cluster in shared memory and reserves one slice per (block,
+// cluster) with a single global atomic; this simple variant serves k > 6144.
 __global__ void scatter_members_simple_kernel(const int32_t* __restrict__ lab, int64_t n,
                                               unsigned* __restrict__ cursor, const int64_t* __restrict__ off,
                                               int32_t* __restrict__ perm, const int* __restrict__ chg,
@@ -739,12 +717,37 @@ __global__ void zero_acc_kernel(unsigned long long* __restrict__ acc4, int64_t c
 
 // (full recompute: histogram of the labels; incremental: histogram of the changed points'
 // old and new labels)
+// Zeroing for the next steps rides along (one launch instead of several memsets): the
+// histograms, changed-label slot and queue lengths the next assignment accumulates into, the
+// scatter cursors, and (full recompute, small k d) the limb accumulators.
+struct PlanZero {
+  int* changed_slot;          // next assignment's changed-label counter
+  unsigned* counts_next;      // [k] next assignment's histogram
+  unsigned* dcount_next;      // [k] next assignment's changed-point histogram
+  unsigned* cursor;           // [k] scatter cursors
+  int* len;                   // pruning / ambiguous queue lengths ([0] and [2])
+  unsigned long long* acc4;   // limb accumulators (zeroed here iff acc_n > 0 and full recompute)
+  int64_t acc_n;
+};
+
 __global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __restrict__ counts_full,
                                                            const unsigned* __restrict__ counts_delta, int k,
                                                            int64_t chunk, int64_t* __restrict__ off,
                                                            int32_t* __restrict__ item0, int* __restrict__ total_items,
-                                                           const int* __restrict__ chg, int64_t thresh) {
-  const unsigned* __restrict__ counts = full_gate(chg, thresh) ? counts_full : counts_delta;
+                                                           const int* __restrict__ chg, int64_t thresh, PlanZero z) {
+  const bool full = full_gate(chg, thresh);
+  const unsigned* __restrict__ counts = full ? counts_full : counts_delta;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    if (z.counts_next) z.counts_next[c] = 0u;
+    if (z.dcount_next) z.dcount_next[c] = 0u;
+    if (z.cursor) z.cursor[c] = 0u;
+  }
+  if (threadIdx.x == 0) {
+    if (z.changed_slot) *z.changed_slot = 0;
+    if (z.len) { z.len[0] = 0; z.len[2] = 0; }
+  }
+  if (full && z.acc_n > 0)
+    for (int64_t e = threadIdx.x; e < z.acc_n; e += blockDim.x) z.acc4[e] = 0ull;
   __shared__ long long s_cnt[256];
   __shared__ int s_ni[256];
   __shared__ long long carry_off;
@@ -858,6 +861,43 @@ __global__ void member_sum_kernel(const float* __restrict__ F, int d, const int3
   }
 }
 
+// Full or incremental scatter in one launch (device-side choice, block-uniform branch):
+// full -> counting sort of all points by label (scatter_members_kernel's scheme, blocks of
+// per_block points), incremental -> the changed points filed +/- (scatter_delta_kernel).
+__global__ void scatter_any_kernel(const int32_t* __restrict__ lab, int64_t n, int k, int64_t per_block,
+                                   unsigned* __restrict__ cursor, const int64_t* __restrict__ off,
+                                   int32_t* __restrict__ perm, const int32_t* __restrict__ chg_list,
+                                   const int* __restrict__ chg, const int32_t* __restrict__ prev, int64_t thresh) {
+  extern __shared__ unsigned hist[];   // [k] local counts, then [k] bases
+  if (full_gate(chg, thresh)) {
+    unsigned* base = hist + k;
+    const int64_t a = blockIdx.x * per_block;
+    if (a >= n) return;
+    const int64_t b = min(n, a + per_block);
+    for (int c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
+    __syncthreads();
+    for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) atomicAdd(&hist[lab[i]], 1u);
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+      base[c] = hist[c] ? atomicAdd(&cursor[c], hist[c]) : 0u;
+      hist[c] = 0;
+    }
+    __syncthreads();
+    for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+      const int c = lab[i];
+      perm[off[c] + base[c] + atomicAdd(&hist[c], 1u)] = static_cast<int32_t>(i);
+    }
+  } else {
+    const int m = *chg;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+      const int32_t i = chg_list[j];
+      const int bl = lab[i], al = prev[i];
+      perm[off[bl] + atomicAdd(&cursor[bl], 1u)] = i;
+      perm[off[al] + atomicAdd(&cursor[al], 1u)] = static_cast<int32_t>(static_cast<uint32_t>(i) | 0x80000000u);
+    }
+  }
+}
+
 // Incremental exact update: every changed point (old label a -> new label b) is listed
 // under cluster b with sign + and under cluster a with sign - (bit 31 of the entry); the
 // member sums then move its fixed-point image between the clusters exactly.
@@ -941,7 +981,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_TRY(b_new.ensure(sizeof(int32_t) * n, s));
   SC_TRY(b_d2.ensure(sizeof(double) * n, s));
   SC_TRY(b_C.ensure(sizeof(double) * k * d, s));
-  SC_TRY(b_cnt.ensure(sizeof(unsigned) * k, s));
+  SC_TRY(b_cnt.ensure(sizeof(unsigned) * 2 * k, s));   // histograms, by assignment parity
   SC_TRY(b_cur.ensure(sizeof(unsigned) * k, s));
   SC_TRY(b_off.ensure(sizeof(int64_t) * (k + 1), s));
   SC_TRY(b_perm.ensure(sizeof(int32_t) * 2 * n, s));
@@ -961,7 +1001,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   // screened assignment: fp32 centroids, C_m, queue of the points the screen cannot decide
   PoolBuf b_Cf, b_amb, b_chgl, b_dcnt;
   SC_TRY(b_chgl.ensure(sizeof(int32_t) * n, s));
-  SC_TRY(b_dcnt.ensure(sizeof(unsigned) * k, s));
+  SC_TRY(b_dcnt.ensure(sizeof(unsigned) * 2 * k, s));
   SC_TRY(b_Cf.ensure(sizeof(float) * (size_t)k * d + 64, s));
   SC_TRY(b_amb.ensure(sizeof(int32_t) * n, s));
   float* d_Cf = b_Cf.as<float>();
@@ -1039,16 +1079,17 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   // block partials of the inertia in b_part
   int* changed_dev = b_chg.as<int>();
   const bool trace_len = std::getenv("SC_KMEANS_TRACE") != nullptr;
+  // (the counters an assignment accumulates into -- changed_dev[slot], the histograms of
+  // parity slot & 1, the queue lengths -- were zeroed by the preceding update's plan kernel,
+  // or before the first assignment of a restart)
+  auto cnt_of = [&](int slot) { return b_cnt.as<unsigned>() + (size_t)(slot & 1) * k; };
+  auto dcnt_of = [&](int slot) { return b_dcnt.as<unsigned>() + (size_t)(slot & 1) * k; };
   auto assign_all = [&](int32_t* out_lab, const int32_t* old, int slot, bool try_check) -> int {
-    SC_CUDA_TRY(cudaMemsetAsync(changed_dev + slot, 0, sizeof(int), s));
-    SC_CUDA_TRY(cudaMemsetAsync(b_cnt.ptr, 0, sizeof(unsigned) * k, s));
-    SC_CUDA_TRY(cudaMemsetAsync(b_dcnt.ptr, 0, sizeof(unsigned) * k, s));
     if (screen) {
       // fp32 screen + exact verification of every point (or of the pruning queue), exact
       // fp64 scan of the points it cannot decide
       const bool pruned = old && prune && try_check;
       int* amb_len = b_len.as<int>() + 2;
-      SC_CUDA_TRY(cudaMemsetAsync(b_len.ptr, 0, 3 * sizeof(int), s));
       if (pruned) {
         check_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_rows, s>>>(
             F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(), b_lo.as<double>(),
@@ -1077,7 +1118,6 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     } else {
       // Hamerly pruning: points whose assigned centroid is provably still the unique
       // nearest keep it; the rest are queued and fully rescanned
-      SC_CUDA_TRY(cudaMemsetAsync(b_len.ptr, 0, sizeof(int), s));
       check_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_rows, s>>>(
           F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(), b_lo.as<double>(),
           b_list.as<int32_t>(), b_len.as<int>());
@@ -1093,8 +1133,8 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     }
     SC_CUDA_TRY(cudaGetLastError());
     assign_stats_kernel<<<(unsigned)nstat, 256, 0, s>>>(out_lab, old, b_dmin.as<double>(), n, b_part.as<double>(),
-                                                       changed_dev + slot, b_cnt.as<unsigned>(),
-                                                       b_chgl.as<int32_t>(), b_dcnt.as<unsigned>());
+                                                       changed_dev + slot, cnt_of(slot),
+                                                       b_chgl.as<int32_t>(), dcnt_of(slot));
     SC_CUDA_TRY(cudaGetLastError());
     return SC_OK;
   };
@@ -1116,35 +1156,43 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   // full recompute when more than n/4 labels changed (or no previous sums), else incremental
   // (2 gathered rows per changed point against n)
   const int64_t delta_thresh = n / 4;
-  auto update = [&](const int32_t* cur, const int32_t* prev, const int* chg) -> int {
+  // update(it): centroids from the labels of assignment it-1 (histograms of parity it-1);
+  // its plan kernel zeroes what assignment it accumulates into
+  const int64_t acc_elems = 4 * (int64_t)k * d;
+  auto update = [&](const int32_t* cur, const int32_t* prev, const int* chg, int it) -> int {
     if (!prev) chg = nullptr;
     if (prune) SC_CUDA_TRY(cudaMemcpyAsync(b_Cold.ptr, C, sizeof(double) * k * d, cudaMemcpyDeviceToDevice, s));
-    zero_acc_kernel<<<std::max(1, std::min(grid, (int)((4 * (int64_t)k * d + kB - 1) / kB))), kB, 0, s>>>(
-        b_psum.as<unsigned long long>(), 4 * (int64_t)k * d, chg, delta_thresh);
-    plan_members_kernel<<<1, 256, 0, s>>>(b_cnt.as<unsigned>(), b_dcnt.as<unsigned>(), k, kChunk, d_off, d_item0,
-                                          d_total, chg, delta_thresh);
+    const bool big_acc = acc_elems > 65536;
+    if (big_acc) {
+      zero_acc_kernel<<<std::max(1, std::min(grid, (int)((acc_elems + kB - 1) / kB))), kB, 0, s>>>(
+          b_psum.as<unsigned long long>(), acc_elems, chg, delta_thresh);
+      SC_CUDA_TRY(cudaGetLastError());
+    }
+    const PlanZero z{changed_dev + it, cnt_of(it), dcnt_of(it), b_cur.as<unsigned>(), b_len.as<int>(),
+                     b_psum.as<unsigned long long>(), big_acc ? 0 : acc_elems};
+    plan_members_kernel<<<1, 256, 0, s>>>(cnt_of(it - 1), dcnt_of(it - 1), k, kChunk, d_off, d_item0, d_total, chg,
+                                          delta_thresh, z);
     SC_CUDA_TRY(cudaGetLastError());
-    SC_CUDA_TRY(cudaMemsetAsync(b_cur.ptr, 0, sizeof(unsigned) * k, s));
     if (k <= 6144) {
       const int64_t per_block = std::max<int64_t>(4096, (n + grid - 1) / grid);
-      scatter_members_kernel<<<(unsigned)((n + per_block - 1) / per_block), kB, sizeof(unsigned) * 2 * k, s>>>(
-          cur, n, k, per_block, b_cur.as<unsigned>(), d_off, b_perm.as<int32_t>(), chg, delta_thresh);
+      const int64_t sgrid = std::max<int64_t>((n + per_block - 1) / per_block, prev ? grid : 1);
+      scatter_any_kernel<<<(unsigned)sgrid, kB, sizeof(unsigned) * 2 * k, s>>>(
+          cur, n, k, per_block, b_cur.as<unsigned>(), d_off, b_perm.as<int32_t>(), b_chgl.as<int32_t>(), chg, prev,
+          delta_thresh);
     } else {
       scatter_members_simple_kernel<<<grid, kB, 0, s>>>(cur, n, b_cur.as<unsigned>(), d_off, b_perm.as<int32_t>(),
                                                         chg, delta_thresh);
+      if (prev)
+        scatter_delta_kernel<<<grid, kB, 0, s>>>(b_chgl.as<int32_t>(), chg, prev, cur, b_cur.as<unsigned>(), d_off,
+                                                 b_perm.as<int32_t>(), delta_thresh);
     }
     SC_CUDA_TRY(cudaGetLastError());
-    if (prev) {
-      scatter_delta_kernel<<<grid, kB, 0, s>>>(b_chgl.as<int32_t>(), chg, prev, cur, b_cur.as<unsigned>(), d_off,
-                                               b_perm.as<int32_t>(), delta_thresh);
-      SC_CUDA_TRY(cudaGetLastError());
-    }
     const int slots = std::max(1, 256 / d);
     member_sum_kernel<<<(unsigned)max_items, slots * d, sizeof(unsigned long long) * 2 * slots * d, s>>>(
         F, d, b_perm.as<int32_t>(), d_off, d_item0, k, kChunk, d_total, shift, b_psum.as<unsigned long long>());
     SC_CUDA_TRY(cudaGetLastError());
     member_finalize_kernel<<<(unsigned)(((int64_t)k * d + 255) / 256), 256, 0, s>>>(
-        b_psum.as<unsigned long long>(), b_cnt.as<unsigned>(), k, d, shift, C);
+        b_psum.as<unsigned long long>(), cnt_of(it - 1), k, d, shift, C);
     SC_CUDA_TRY(cudaGetLastError());
     if (prune) {
       centroid_shift_kernel<<<1, 256, 0, s>>>(C, b_Cold.as<double>(), k, d, b_dmax.as<double>());
@@ -1182,6 +1230,11 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     // assignment repeats, further iterations are idempotent (same labels -> same exact
     // means -> same labels), so the one issued speculatively changes nothing but time.
     if (trace) { SC_CUDA_TRY(cudaStreamSynchronize(s)); t_seed += now() - t_mark; t_mark = now(); }
+    // counters of the first assignment (later ones are zeroed by the update plan kernels)
+    SC_CUDA_TRY(cudaMemsetAsync(changed_dev, 0, sizeof(int), s));
+    SC_CUDA_TRY(cudaMemsetAsync(b_cnt.ptr, 0, sizeof(unsigned) * k, s));
+    SC_CUDA_TRY(cudaMemsetAsync(b_dcnt.ptr, 0, sizeof(unsigned) * k, s));
+    SC_CUDA_TRY(cudaMemsetAsync(b_len.ptr, 0, 3 * sizeof(int), s));
     SC_TRY(assign_all(lab, nullptr, 0, false));
     int it = 0, conv = -1;
     // With the screen on, the Hamerly check is only worth its extra pass over the features
@@ -1192,7 +1245,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     for (it = 1; it <= max_iter; ++it) {
       const bool try_check = !screen || use_check || it - last_check >= 8;
       if (try_check) last_check = it;
-      SC_TRY(update(lab, it >= 2 ? nw : nullptr, changed_dev + (it - 1)));
+      SC_TRY(update(lab, it >= 2 ? nw : nullptr, changed_dev + (it - 1), it));
       SC_TRY(assign_all(nw, lab, it, try_check));
       SC_CUDA_TRY(cudaMemcpyAsync(h_chg + it, changed_dev + it, sizeof(int), cudaMemcpyDeviceToHost, s));
       if (screen && try_check)
