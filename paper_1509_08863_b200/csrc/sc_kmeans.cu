@@ -71,7 +71,7 @@ __device__ __forceinline__ void stage_rows(const float* __restrict__ F, int64_t 
 // d2[i] = (first ? dist : min(d2[i], dist)) to centre c (device fp64 row)
 __global__ void __launch_bounds__(kSP) d2_update_kernel(const float* __restrict__ F, int64_t n, int d,
                                                         const double* __restrict__ c, double* __restrict__ d2,
-                                                        int first) {
+                                                        int first, int32_t* __restrict__ near) {
   extern __shared__ unsigned char smd[];
   double* sc_ = reinterpret_cast<double*>(smd);
   float* sx = reinterpret_cast<float*>(sc_ + d);
@@ -88,6 +88,35 @@ __global__ void __launch_bounds__(kSP) d2_update_kernel(const float* __restrict_
       acc = __dadd_rn(acc, __dmul_rn(diff, diff));
     }
     d2[i] = first ? acc : fmin(d2[i], acc);
+    if (first && near) near[i] = 0;
+  }
+}
+
+// D^2 update for seed t >= 1 with the triangle inequality: if the point's distance r to its
+// nearest seed j satisfies r (1 + 1e-9) <= half_gap[j] (= ||c_t - c_j|| / 2, rounded down),
+// then ||x - c_t|| >= ||c_t - c_j|| - r >= r (1 + 1e-9) and the computed new D^2 exceeds the
+// computed d2 (both carry < 1e-13 relative rounding): min(d2, new) = d2 exactly as in the
+// full computation, so the row is not read.  Other points: the exact R8 distance.
+__global__ void __launch_bounds__(256) d2_update_skip_kernel(const float* __restrict__ F, int64_t n, int d,
+                                                             const double* __restrict__ c, int t,
+                                                             const double* __restrict__ half_gap,
+                                                             double* __restrict__ d2, int32_t* __restrict__ near) {
+  extern __shared__ double sct[];
+  for (int q = threadIdx.x; q < d; q += blockDim.x) sct[q] = c[q];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double cur = d2[i];
+    if (sqrt(cur) * (1.0 + 1e-9) <= half_gap[near[i]]) continue;
+    const float* x = F + i * d;
+    double acc = 0.0;
+    for (int q = 0; q < d; ++q) {
+      const double diff = __dsub_rn((double)__ldg(x + q), sct[q]);
+      acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    if (acc < cur) {
+      d2[i] = acc;
+      near[i] = t;
+    }
   }
 }
 
@@ -143,7 +172,8 @@ __device__ __forceinline__ void block_inclusive_scan(double v, double* s_w, doub
 __global__ void __launch_bounds__(kSel) seed_select_kernel(const double* __restrict__ bsum, int G,
                                                            const double* __restrict__ v, int64_t n, int64_t chunk,
                                                            double u, const float* __restrict__ F, int d,
-                                                           double* __restrict__ c_out) {
+                                                           double* __restrict__ c_out, int tseed,
+                                                           double* __restrict__ half_gap) {
   __shared__ double s_w[64];
   __shared__ double s_inc[kSel];
   __shared__ int s_first;
@@ -200,6 +230,19 @@ __global__ void __launch_bounds__(kSel) seed_select_kernel(const double* __restr
   }
   const int64_t idx = s_idx;
   for (int q = t; q < d; q += blockDim.x) c_out[q] = (double)F[idx * d + q];
+  if (half_gap) {
+    // half distances from the new seed (c_out = C[tseed]) to the earlier seeds C[0..tseed-1],
+    // rounded down (d2_update_skip_kernel's triangle test)
+    __syncthreads();
+    for (int j = t; j < tseed; j += blockDim.x) {
+      double s2 = 0.0;
+      for (int q = 0; q < d; ++q) {
+        const double df = c_out[q] - c_out[(int64_t)(j - tseed) * d + q];
+        s2 += df * df;
+      }
+      half_gap[j] = 0.5 * sqrt(s2) * (1.0 - 1e-9);
+    }
+  }
 }
 
 __global__ void row_to_centroid_kernel(const float* __restrict__ F, int64_t idx, int d, double* __restrict__ c) {
@@ -996,8 +1039,10 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_TRY(b_len.ensure(16, s));   // [0] pruning queue length, [1] member work items, [2] ambiguous
   SC_TRY(b_dmax.ensure(16, s));
   SC_TRY(b_Cold.ensure(sizeof(double) * k * d, s));
-  PoolBuf b_chg;
+  PoolBuf b_chg, b_near, b_gap;
   SC_TRY(b_chg.ensure(sizeof(int) * (max_iter + 2), s));
+  SC_TRY(b_near.ensure(sizeof(int32_t) * n, s));     // k-means++: nearest seed per point
+  SC_TRY(b_gap.ensure(sizeof(double) * (k + 1), s));  // half distances new seed -> earlier seeds
   // screened assignment: fp32 centroids, C_m, queue of the points the screen cannot decide
   PoolBuf b_Cf, b_amb, b_chgl, b_dcnt;
   SC_TRY(b_chgl.ensure(sizeof(int32_t) * n, s));
@@ -1215,14 +1260,15 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     // ---- k-means++ seeding (device-resident: block sums, then one selection kernel per draw)
     int64_t idx = std::min<int64_t>((int64_t)std::floor(u[0] * n), n - 1);
     row_to_centroid_kernel<<<1, 128, 0, s>>>(F, idx, d, C);
-    d2_update_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_d2, s>>>(F, n, d, C, b_d2.as<double>(), 1);
+    d2_update_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_d2, s>>>(F, n, d, C, b_d2.as<double>(), 1,
+                                                                          b_near.as<int32_t>());
     SC_CUDA_TRY(cudaGetLastError());
     for (int t = 1; t < k; ++t) {
       range_sums_kernel<<<G, kB, 0, s>>>(b_d2.as<double>(), n, chunk, b_part.as<double>());
       seed_select_kernel<<<1, kSel, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk, u[t], F, d,
-                                          C + (size_t)t * d);
-      d2_update_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_d2, s>>>(F, n, d, C + (size_t)t * d,
-                                                                            b_d2.as<double>(), 0);
+                                          C + (size_t)t * d, t, b_gap.as<double>());
+      d2_update_skip_kernel<<<grid, 256, sizeof(double) * d, s>>>(F, n, d, C + (size_t)t * d, t, b_gap.as<double>(),
+                                                                  b_d2.as<double>(), b_near.as<int32_t>());
       SC_CUDA_TRY(cudaGetLastError());
     }
     // ---- Lloyd.  Iterations are issued without waiting; the changed-label count of
