@@ -515,11 +515,20 @@ __global__ void __launch_bounds__(256) assign_screen_kernel(const float* __restr
   const int64_t m = list ? (int64_t)*list_len : n;
   const int64_t p0 = (int64_t)blockIdx.x * kSPT;
   if (p0 >= m) return;
-  // staging: a warp reads one row (coalesced), lanes store down the column
+  // staging: a warp takes one row (coalesced 4-byte cp.async, lanes along the row, stored
+  // down the column), every copy of the tile in flight at once
   for (int row = warp; row < kSPT; row += 8) {
     const int64_t pi = p0 + row;
     const int64_t gi = pi < m ? (list ? (int64_t)list[pi] : pi) : -1;
-    for (int q = lane; q < d; q += 32) sX[(size_t)q * kSLX + row] = gi >= 0 ? F[gi * d + q] : 0.f;
+    for (int q = lane; q < d; q += 32) {
+      float* dst = sX + (size_t)q * kSLX + row;
+      if (gi >= 0) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                     "l"(F + gi * d + q) : "memory");
+      } else {
+        *dst = 0.f;
+      }
+    }
   }
   float best[8], second[8];
   int bidx[8];
@@ -529,7 +538,16 @@ __global__ void __launch_bounds__(256) assign_screen_kernel(const float* __restr
     const int kt = min(kAT, k - c0);
     __syncthreads();
     for (int cc = warp; cc < kAT; cc += 8)
-      for (int q = lane; q < d; q += 32) sC[(size_t)q * kSLC + cc] = cc < kt ? Cf[(size_t)(c0 + cc) * d + q] : 0.f;
+      for (int q = lane; q < d; q += 32) {
+        float* dst = sC + (size_t)q * kSLC + cc;
+        if (cc < kt) {
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                       "l"(Cf + (size_t)(c0 + cc) * d + q) : "memory");
+        } else {
+          *dst = 0.f;
+        }
+      }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     uint64_t acc[8][2];
 #pragma unroll
