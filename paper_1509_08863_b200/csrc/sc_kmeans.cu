@@ -340,11 +340,28 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
   // length is only known on the device)
   for (int64_t p0 = (int64_t)blockIdx.x * kAT; p0 < m; p0 += (int64_t)gridDim.x * kAT) {
   __syncthreads();   // previous tile's shared-memory reads done
-  for (int e = tid; e < kAT * d; e += 256) {
-    const int row = e / d, q = e - row * d;
-    const int64_t pi = p0 + row;
-    const int64_t gi = pi < m ? (list ? (int64_t)list[pi] : pi) : -1;
-    sX[(size_t)q * kAT + row] = gi >= 0 ? (double)F[gi * d + q] : 0.0;
+  // staging with 8 independent loads in flight per thread
+  for (int e0 = tid; e0 < kAT * d; e0 += 256 * 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256;
+      v[u] = 0.f;
+      if (e < kAT * d) {
+        const int row = e / d, q = e - row * d;
+        const int64_t pi = p0 + row;
+        const int64_t gi = pi < m ? (list ? (int64_t)list[pi] : pi) : -1;
+        if (gi >= 0) v[u] = __ldg(F + gi * d + q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256;
+      if (e < kAT * d) {
+        const int row = e / d, q = e - row * d;
+        sX[(size_t)q * kAT + row] = (double)v[u];
+      }
+    }
   }
   double best[4], second[4];
   int bidx[4];
@@ -354,9 +371,25 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
   for (int c0 = 0; c0 < k; c0 += TW) {
     const int kt = min(TW, k - c0);
     __syncthreads();
-    for (int e = tid; e < TW * d; e += 256) {
-      const int cc = e / d, q = e - cc * d;
-      sC[(size_t)q * kAT + cc] = cc < kt ? C[(size_t)(c0 + cc) * d + q] : 0.0;
+    for (int e0 = tid; e0 < TW * d; e0 += 256 * 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * 256;
+        v[u] = 0.0;
+        if (e < TW * d) {
+          const int cc = e / d, q = e - cc * d;
+          if (cc < kt) v[u] = __ldg(C + (size_t)(c0 + cc) * d + q);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * 256;
+        if (e < TW * d) {
+          const int cc = e / d, q = e - cc * d;
+          sC[(size_t)q * kAT + cc] = v[u];
+        }
+      }
     }
     __syncthreads();
     double acc[4][NC];
