@@ -527,7 +527,7 @@ constexpr int kSPT = 128;              // points per block of the screen
 constexpr int kSLX = kSPT + 4;         // padded leading dimensions (16-byte aligned rows)
 constexpr int kSLC = kAT + 4;
 
-__global__ void __launch_bounds__(256) assign_screen_kernel(const float* __restrict__ F, int64_t n, int d,
+__global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __restrict__ F, int64_t n, int d,
                                                             const double* __restrict__ C,
                                                             const float* __restrict__ Cf,
                                                             const double* __restrict__ cm, int k,
