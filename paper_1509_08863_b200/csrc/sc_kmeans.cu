@@ -6,7 +6,9 @@
 // Decision arithmetic is fixed so that the result does not depend on thread
 // scheduling (reading R8):
 //   * distances: fp64, explicit differences, summed in ascending q with
-//     __dsub_rn/__dmul_rn/__dadd_rn (no FMA contraction);
+//     __dsub_rn/__dmul_rn/__dadd_rn (no FMA contraction); large problems screen the
+//     candidates in fp32 first with a rigorous error bound and compute the exact fp64
+//     distance of the proven winner (undecided points get the exact full scan);
 //   * centroid sums: members grouped by cluster (counting sort), exact 128-bit
 //     fixed-point accumulation of the fp32 features (x * 2^(100-E), E the exponent
 //     bound of max|x|; integer sums are order independent), rounded once to fp64
@@ -778,7 +780,8 @@ __global__ void __launch_bounds__(256) assign_stats_kernel(const int32_t* __rest
 
 // Centroid sums are kept as exact integers, so they can also be updated incrementally: the
 // full recompute (plan, scatter, member sums) runs iff full_gate(); otherwise
-// member_delta_kernel moves the changed points' contributions between clusters.  The
+// the changed points are filed +/- under their new / old clusters (scatter_any_kernel) and
+// the member sums move their contributions between clusters.  The
 // decision reads the device-side changed-label count (no host round trip).
 __device__ __forceinline__ bool full_gate(const int* chg, int64_t thresh) {
   return chg == nullptr || (int64_t)*chg > thresh;
@@ -956,8 +959,8 @@ __global__ void member_sum_kernel(const float* __restrict__ F, int d, const int3
 }
 
 // Full or incremental scatter in one launch (device-side choice, block-uniform branch):
-// full -> counting sort of all points by label (scatter_members_kernel's scheme, blocks of
-// per_block points), incremental -> the changed points filed +/- (scatter_delta_kernel).
+// full -> counting sort of all points by label (blocks of per_block points, per-block
+// shared-memory ranks, one global atomic per (block, cluster)), incremental -> the changed points filed +/- (scatter_delta_kernel).
 __global__ void scatter_any_kernel(const int32_t* __restrict__ lab, int64_t n, int k, int64_t per_block,
                                    unsigned* __restrict__ cursor, const int64_t* __restrict__ off,
                                    int32_t* __restrict__ perm, const int32_t* __restrict__ chg_list,
