@@ -31,6 +31,7 @@
 // every rank, then step s+1 ...), with the peers' buffers being ordinary device memory: the
 // single-GPU emulation the tests use (no kernel ever waits on another one).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -367,13 +368,24 @@ int sc_p2p_filter_group_f32(sc_p2p* const* ps, int world, const double* coeffs, 
   }
   const int Rp = (R + 3) / 4 * 4;
   const std::vector<int> chunks = chunk_widths<float>(Rp, ps[0]->n_global);
+  // SC_P2P_GROUP_WAITS=1 (tests): also launch every rank's flag wait where the multi-process
+  // path does.  In this order each wait's flags were published by kernels that precede it on
+  // the stream, so it returns at once -- it checks the signal protocol without any kernel
+  // waiting for another one to be scheduled.
+  const bool waits = std::getenv("SC_P2P_GROUP_WAITS") && std::atoi(std::getenv("SC_P2P_GROUP_WAITS")) != 0;
   int col0 = 0;
   for (int w : chunks) {
     for (int q = 0; q < world; ++q) SC_TRY(chunk_start(runs[q], col0, w, R, s));
-    for (int q = 0; q < world; ++q) SC_TRY(push(runs[q], w, s));
+    for (int q = 0; q < world; ++q) {
+      if (waits) SC_TRY(wait_peers(ps[q], s));
+      SC_TRY(push(runs[q], w, s));
+    }
     std::vector<int> added(world, -1);
     for (int st = 0; st < order; ++st)
-      for (int q = 0; q < world; ++q) SC_TRY(step(runs[q], coeffs, order, lambda_max, Rp, col0, w, st, added[q], s));
+      for (int q = 0; q < world; ++q) {
+        if (waits) SC_TRY(wait_peers(ps[q], s));
+        SC_TRY(step(runs[q], coeffs, order, lambda_max, Rp, col0, w, st, added[q], s));
+      }
     col0 += w;
   }
   for (int q = 0; q < world; ++q) {

@@ -572,8 +572,9 @@ def test_row_partitioned_steps_emulated_two_ranks(sc):
     assert rel(Yfull, Yo) <= F32_TOL
 
 
-@pytest.mark.parametrize("world,R,chunk", [(2, 16, None), (3, 6, None), (4, 16, "8"), (2, 12, "4"), (1, 8, None)])
-def test_p2p_fused_exchange_emulated(sc, world, R, chunk, monkeypatch):
+@pytest.mark.parametrize("world,R,chunk,waits", [(2, 16, None, False), (3, 6, None, False), (4, 16, "8", False),
+                                                 (2, 12, "4", False), (1, 8, None, False), (3, 16, "8", True)])
+def test_p2p_fused_exchange_emulated(sc, world, R, chunk, waits, monkeypatch):
     """The fused-exchange filter (sc_p2p_*): every rank's step kernel stores its boundary rows
     of T_{s+1} straight into the peers' halos.  All ranks held by this process on one GPU
     (sc_p2p_filter_group_f32: dependency-ordered launches on one stream, nothing waits), incl.
@@ -581,6 +582,8 @@ def test_p2p_fused_exchange_emulated(sc, world, R, chunk, monkeypatch):
     from paper_1509_08863_b200 import dist as pdist
     if chunk:
         monkeypatch.setenv("SC_CHUNK", chunk)
+    if waits:   # also run the flag waits of the multi-process path (each already satisfied)
+        monkeypatch.setenv("SC_P2P_GROUP_WAITS", "1")
     g = scinputs.sbm(3000, 6, 10, 0.1, seed=21)
     order = 30
     L = laplacian.laplacian(g)
