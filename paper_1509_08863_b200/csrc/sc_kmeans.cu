@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
   // the same rounding as scalar code, so the bound above holds lane by lane).
   extern __shared__ float smf[];
   float* sX = smf;                                    // [d][kSLX]
-  float* sC = smf + (size_t)d * kSLX;                 // [d][kSLC]
+  float* sCb = smf + (size_t)d * kSLX;                // 2 x [d][kSLC]: double-buffered centroid tiles
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tx = tid & 15, ty = tid >> 4;
   const int64_t m = list ? (int64_t)*list_len : n;
@@ -569,12 +569,12 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
   int bidx[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) { best[i] = INFINITY; second[i] = INFINITY; bidx[i] = -1; }
-  for (int c0 = 0; c0 < k; c0 += kAT) {
+  // centroid tile t goes to buffer t & 1; tile t+1 is requested before tile t is computed
+  auto stage_c = [&](int c0, float* buf) {
     const int kt = min(kAT, k - c0);
-    __syncthreads();
     for (int cc = warp; cc < kAT; cc += 8)
       for (int q = lane; q < d; q += 32) {
-        float* dst = sC + (size_t)q * kSLC + cc;
+        float* dst = buf + (size_t)q * kSLC + cc;
         if (cc < kt) {
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
                        "l"(Cf + (size_t)(c0 + cc) * d + q) : "memory");
@@ -582,7 +582,18 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
           *dst = 0.f;
         }
       }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage_c(0, sCb);   // (commits the point tile's copies too)
+  for (int c0 = 0, t = 0; c0 < k; c0 += kAT, ++t) {
+    const int kt = min(kAT, k - c0);
+    float* sC = sCb + (size_t)(t & 1) * d * kSLC;
+    if (c0 + kAT < k) {
+      stage_c(c0 + kAT, sCb + (size_t)((t + 1) & 1) * d * kSLC);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
     uint64_t acc[8][2];
 #pragma unroll
@@ -604,6 +615,7 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
         asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc[i][1]) : "l"(d1));
       }
     }
+    __syncthreads();   // every warp is done reading sC before the next request refills it
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -1157,7 +1169,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   }
   auto assign3 = nc_best == 4 ? assign3_kernel<4> : nc_best == 2 ? assign3_kernel<2> : assign3_kernel<1>;
   SC_CUDA_TRY(cudaFuncSetAttribute(assign3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
-  const int smem_screen = (int)(sizeof(float) * (size_t)d * (kSLX + kSLC));
+  const int smem_screen = (int)(sizeof(float) * (size_t)d * (kSLX + 2 * kSLC));
   SC_CUDA_TRY(cudaFuncSetAttribute(assign_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_screen));
   // the screen pays off when the exact scan is expensive (env SC_KMEANS_SCREEN=0 disables it)
   const double screen_min = std::getenv("SC_KMEANS_SCREEN_MIN") ? std::atof(std::getenv("SC_KMEANS_SCREEN_MIN"))
