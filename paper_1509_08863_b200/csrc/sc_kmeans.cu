@@ -728,31 +728,6 @@ __global__ void __launch_bounds__(kSP) check_kernel(const float* __restrict__ F,
   }
 }
 
-// max_c ||C[c] - C_old[c]|| (inflated by 1e-9 relative for rounding) into *dmax
-__global__ void centroid_shift_kernel(const double* __restrict__ C, const double* __restrict__ Cold, int k, int d,
-                                      double* __restrict__ dmax) {
-  __shared__ double sh[256];
-  double m = 0.0;
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
-    double s = 0.0;
-    for (int q = 0; q < d; ++q) {
-      const double t = C[(size_t)c * d + q] - Cold[(size_t)c * d + q];
-      s += t * t;
-    }
-    m = fmax(m, sqrt(s));
-  }
-  sh[threadIdx.x] = m;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *dmax = sh[0] * (1.0 + 1e-9) + 1e-300;
-}
-
-// per-block inertia partials over fixed index ranges (deterministic whatever path
-// produced each point), changed count, label histogram; with old labels also the list of
-// the changed points and the histogram of their old and new labels (incremental update)
 __global__ void __launch_bounds__(256) assign_stats_kernel(const int32_t* __restrict__ lab,
                                                            const int32_t* __restrict__ old_lab,
                                                            const double* __restrict__ dmin, int64_t n,
@@ -837,6 +812,8 @@ struct PlanZero {
   int* len;                   // pruning / ambiguous queue lengths ([0] and [2])
   unsigned long long* acc4;   // limb accumulators (zeroed here iff acc_n > 0 and full recompute)
   int64_t acc_n;
+  double* cm;                 // max centroid norm / largest shift, merged by the finalize kernel
+  double* dmax;
 };
 
 __global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __restrict__ counts_full,
@@ -854,6 +831,8 @@ __global__ void __launch_bounds__(256) plan_members_kernel(const unsigned* __res
   if (threadIdx.x == 0) {
     if (z.changed_slot) *z.changed_slot = 0;
     if (z.len) { z.len[0] = 0; z.len[2] = 0; }
+    if (z.cm) *z.cm = 0.0;
+    if (z.dmax) *z.dmax = 0.0;
   }
   if (full && z.acc_n > 0)
     for (int64_t e = threadIdx.x; e < z.acc_n; e += blockDim.x) z.acc4[e] = 0ull;
@@ -1027,19 +1006,49 @@ __global__ void scatter_delta_kernel(const int32_t* __restrict__ chg_list, const
 // C[c][q] = correctly rounded (cluster sum) / count; empty clusters keep C.  The sum is
 // sum_l acc[c][q][l] 2^(32 l) mod 2^128, read as a signed 128-bit integer; the limbs are
 // rewritten in canonical form (each < 2^32), so the next update starts from one add per limb.
-__global__ void member_finalize_kernel(unsigned long long* __restrict__ acc4, const unsigned* __restrict__ counts,
-                                       int k, int d, int shift, double* __restrict__ C) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)k * d) return;
-  const int c = (int)(e / d);
-  unsigned long long* a = acc4 + e * 4;
-  unsigned __int128 u = 0;
+// One block per centroid, which also produces what the next assignment's bounds need (no
+// separate passes): the fp32 copy Cf for the screen, max_c ||c|| (cm) and the largest
+// centroid shift max_c ||c_new - c_old|| (dmax, Hamerly), both rounded up by 1e-9 and merged
+// with atomicMax on their bit patterns (non-negative doubles order as integers); cm and dmax
+// were zeroed by the plan kernel.
+__global__ void __launch_bounds__(256) member_finalize_kernel(unsigned long long* __restrict__ acc4,
+                                                              const unsigned* __restrict__ counts, int k, int d,
+                                                              int shift, double* __restrict__ C,
+                                                              float* __restrict__ Cf, double* __restrict__ cm,
+                                                              double* __restrict__ dmax) {
+  __shared__ double s_n[256], s_d[256];
+  const int c = blockIdx.x;
+  const unsigned cnt = counts[c];
+  double n2 = 0.0, d2 = 0.0;
+  for (int q = threadIdx.x; q < d; q += blockDim.x) {
+    const int64_t e = (int64_t)c * d + q;
+    unsigned long long* a = acc4 + e * 4;
+    unsigned __int128 u = 0;
 #pragma unroll
-  for (int l = 0; l < 4; ++l) u += (unsigned __int128)a[l] << (32 * l);
+    for (int l = 0; l < 4; ++l) u += (unsigned __int128)a[l] << (32 * l);
 #pragma unroll
-  for (int l = 0; l < 4; ++l) a[l] = (unsigned long long)(u >> (32 * l)) & 0xffffffffull;
-  if (counts[c] == 0) return;
-  C[e] = fixed_to_double((__int128)u, shift) / (double)counts[c];
+    for (int l = 0; l < 4; ++l) a[l] = (unsigned long long)(u >> (32 * l)) & 0xffffffffull;
+    const double old = C[e];
+    const double v = cnt ? fixed_to_double((__int128)u, shift) / (double)cnt : old;
+    C[e] = v;
+    if (Cf) Cf[e] = (float)v;
+    n2 += v * v;
+    d2 += (v - old) * (v - old);
+  }
+  if (!cm && !dmax) return;   // (small problems: no screen, no pruning)
+  s_n[threadIdx.x] = n2;
+  s_d[threadIdx.x] = d2;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) { s_n[threadIdx.x] += s_n[threadIdx.x + o]; s_d[threadIdx.x] += s_d[threadIdx.x + o]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (cm) atomicMax(reinterpret_cast<unsigned long long*>(cm),
+                      (unsigned long long)__double_as_longlong(sqrt(s_n[0]) * (1.0 + 1e-9)));
+    if (dmax) atomicMax(reinterpret_cast<unsigned long long*>(dmax),
+                        (unsigned long long)__double_as_longlong(sqrt(s_d[0]) * (1.0 + 1e-9) + 1e-300));
+  }
 }
 
 int num_sms_current() {
@@ -1098,13 +1107,12 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_TRY(b_psum.ensure(sizeof(unsigned long long) * 4 * (size_t)k * d, s));
   const int64_t nstat = (n + 255) / 256;
   SC_TRY(b_part.ensure(sizeof(double) * std::max<int64_t>(std::max<int64_t>(grid, G), std::max(nblk, nstat)), s));
-  PoolBuf b_dmin, b_lo, b_list, b_len, b_dmax, b_Cold;
+  PoolBuf b_dmin, b_lo, b_list, b_len, b_dmax;
   SC_TRY(b_dmin.ensure(sizeof(double) * n, s));
   SC_TRY(b_lo.ensure(sizeof(double) * n, s));
   SC_TRY(b_list.ensure(sizeof(int32_t) * n, s));
   SC_TRY(b_len.ensure(16, s));   // [0] pruning queue length, [1] member work items, [2] ambiguous
   SC_TRY(b_dmax.ensure(16, s));
-  SC_TRY(b_Cold.ensure(sizeof(double) * k * d, s));
   PoolBuf b_chg, b_near, b_gap;
   SC_TRY(b_chg.ensure(sizeof(int) * (max_iter + 2), s));
   SC_TRY(b_near.ensure(sizeof(int32_t) * n, s));     // k-means++: nearest seed per point
@@ -1207,8 +1215,10 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
             b_list.as<int32_t>(), b_len.as<int>());
         SC_CUDA_TRY(cudaGetLastError());
       }
-      centroid_prep_kernel<<<1, 256, 0, s>>>(C, k, d, d_Cf, d_cm);
-      SC_CUDA_TRY(cudaGetLastError());
+      if (!old) {   // first assignment of a restart; later ones get Cf, cm from the finalize kernel
+        centroid_prep_kernel<<<1, 256, 0, s>>>(C, k, d, d_Cf, d_cm);
+        SC_CUDA_TRY(cudaGetLastError());
+      }
       assign_screen_kernel<<<(unsigned)((n + kSPT - 1) / kSPT), 256, smem_screen, s>>>(
           F, n, d, C, d_Cf, d_cm, k, pruned ? b_list.as<int32_t>() : nullptr, pruned ? b_len.as<int>() : nullptr,
           out_lab, b_dmin.as<double>(), b_lo.as<double>(), b_amb.as<int32_t>(), amb_len);
@@ -1272,7 +1282,6 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   const int64_t acc_elems = 4 * (int64_t)k * d;
   auto update = [&](const int32_t* cur, const int32_t* prev, const int* chg, int it) -> int {
     if (!prev) chg = nullptr;
-    if (prune) SC_CUDA_TRY(cudaMemcpyAsync(b_Cold.ptr, C, sizeof(double) * k * d, cudaMemcpyDeviceToDevice, s));
     const bool big_acc = acc_elems > 65536;
     if (big_acc) {
       zero_acc_kernel<<<std::max(1, std::min(grid, (int)((acc_elems + kB - 1) / kB))), kB, 0, s>>>(
@@ -1280,7 +1289,8 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
       SC_CUDA_TRY(cudaGetLastError());
     }
     const PlanZero z{changed_dev + it, cnt_of(it), dcnt_of(it), b_cur.as<unsigned>(), b_len.as<int>(),
-                     b_psum.as<unsigned long long>(), big_acc ? 0 : acc_elems};
+                     b_psum.as<unsigned long long>(), big_acc ? 0 : acc_elems, screen ? d_cm : nullptr,
+                     prune ? b_dmax.as<double>() : nullptr};
     plan_members_kernel<<<1, 256, 0, s>>>(cnt_of(it - 1), dcnt_of(it - 1), k, kChunk, d_off, d_item0, d_total, chg,
                                           delta_thresh, z);
     SC_CUDA_TRY(cudaGetLastError());
@@ -1302,13 +1312,15 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     member_sum_kernel<<<(unsigned)max_items, slots * d, sizeof(unsigned long long) * 2 * slots * d, s>>>(
         F, d, b_perm.as<int32_t>(), d_off, d_item0, k, kChunk, d_total, shift, b_psum.as<unsigned long long>());
     SC_CUDA_TRY(cudaGetLastError());
-    member_finalize_kernel<<<(unsigned)(((int64_t)k * d + 255) / 256), 256, 0, s>>>(
-        b_psum.as<unsigned long long>(), cnt_of(it - 1), k, d, shift, C);
-    SC_CUDA_TRY(cudaGetLastError());
-    if (prune) {
-      centroid_shift_kernel<<<1, 256, 0, s>>>(C, b_Cold.as<double>(), k, d, b_dmax.as<double>());
-      SC_CUDA_TRY(cudaGetLastError());
+    {
+      // bounds wanted: 256 threads (power of two for the block reduction); else one warp-multiple
+      const bool bounds = screen || prune;
+      const int fin_threads = bounds ? 256 : std::min(256, (d + 31) / 32 * 32);
+      member_finalize_kernel<<<(unsigned)k, fin_threads, 0, s>>>(
+          b_psum.as<unsigned long long>(), cnt_of(it - 1), k, d, shift, C, screen ? d_Cf : nullptr,
+          screen ? d_cm : nullptr, prune ? b_dmax.as<double>() : nullptr);
     }
+    SC_CUDA_TRY(cudaGetLastError());
     return SC_OK;
   };
 
