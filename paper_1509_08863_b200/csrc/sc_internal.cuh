@@ -77,15 +77,16 @@ struct DevBuf {
 // (default: 0, i.e. trimmed at every synchronisation, so each call re-maps its workspaces --
 // measured as sporadic 0.2-0.9 s host stalls on repeated calls).  Idempotent, cheap.
 inline void keep_pool_reserved() {
-  static bool done[64] = {};
+  static std::once_flag once[64];
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = 8ull << 30;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[dev] = true;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::call_once(once[dev], [dev] {   // worker threads may get here concurrently
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = 8ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
 }
 
 struct PoolBuf {
