@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -1077,6 +1078,38 @@ struct KmResult {
 };
 }  // namespace
 
+// Process-wide pool of pinned int buffers (never returned to the driver).
+struct PinnedSlot {
+  int* p = nullptr;
+  size_t n = 0;
+  static std::mutex& mu() { static std::mutex m; return m; }
+  static std::vector<std::pair<int*, size_t>>& free_list() {
+    static std::vector<std::pair<int*, size_t>> f;
+    return f;
+  }
+  int acquire(size_t want) {
+    {
+      std::lock_guard<std::mutex> lk(mu());
+      auto& f = free_list();
+      for (size_t i = 0; i < f.size(); ++i)
+        if (f[i].second >= want) {
+          p = f[i].first;
+          n = f[i].second;
+          f.erase(f.begin() + (long)i);
+          return SC_OK;
+        }
+    }
+    SC_CUDA_TRY(cudaMallocHost(&p, sizeof(int) * want));
+    n = want;
+    return SC_OK;
+  }
+  ~PinnedSlot() {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu());
+    free_list().emplace_back(p, n);
+  }
+};
+
 // Restarts r0, r0 + rstep, ... < restarts on stream s; the best of them (lowest inertia,
 // ties -> lowest r) goes to *res and its labels to labels_dev.
 static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rstep, int restarts, int max_iter,
@@ -1125,20 +1158,11 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_TRY(b_amb.ensure(sizeof(int32_t) * n, s));
   float* d_Cf = b_Cf.as<float>();
   double* d_cm = reinterpret_cast<double*>(b_Cf.as<char>() + ((sizeof(float) * (size_t)k * d + 15) / 16) * 16);
-  // pinned per-thread landing slots for the changed-label counts (kept across calls)
-  struct PinnedInts {
-    int* p = nullptr;
-    size_t n = 0;
-    ~PinnedInts() { if (p) cudaFreeHost(p); }
-  };
-  static thread_local PinnedInts pin;
-  if (pin.n < 2 * ((size_t)max_iter + 2)) {
-    if (pin.p) cudaFreeHost(pin.p);
-    pin.p = nullptr;
-    pin.n = 0;
-    SC_CUDA_TRY(cudaMallocHost(&pin.p, sizeof(int) * 2 * (max_iter + 2)));
-    pin.n = 2 * ((size_t)max_iter + 2);
-  }
+  // pinned landing slots for the changed-label counts, from a process-wide pool (worker
+  // threads are short-lived: a per-thread cudaMallocHost / cudaFreeHost pair per call
+  // synchronises the device and showed up as 0.5-0.9 s outliers in the stability scan)
+  PinnedSlot pin;
+  SC_TRY(pin.acquire(2 * ((size_t)max_iter + 2)));
   int* h_chg = pin.p;
   int* h_rescan = pin.p + max_iter + 2;   // pruning-queue length per iteration (-1: no check run)
   cudaEvent_t ev_chg[2];
