@@ -441,6 +441,42 @@ def test_kmeans_on_filtered_features_and_default_uniforms(sc):
     assert np.array_equal(lab, lo) and best == ro
 
 
+def test_kmeans_full_size_properties(sc):
+    """configs[3]-sized k-means (10^6 x 64, k = 100: fp32 screen, Hamerly checks, incremental
+    exact updates, concurrent restarts) checked by properties the oracle can compute at this
+    size: sampled labels are the exact fp64 argmin (oracle arithmetic, lowest index on ties)
+    under the returned centroids, sampled centroids are the correctly rounded member means,
+    and the inertia is the oracle's sum of exact distances."""
+    import math
+    rng = np.random.default_rng(77)
+    n, d, k = 1_000_000, 64, 100
+    centers = rng.standard_normal((k, d)) * 0.5
+    X = (centers[rng.integers(0, k, n)] + rng.standard_normal((n, d))).astype(np.float32)
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    C = np.zeros((k, d), dtype=np.float64)
+    u = np.stack([scinputs.uniforms(3, k, offset=k * r) for r in range(2)])
+    inertia, it, best = sc.sc_kmeans(torch.from_numpy(X).cuda(), n, d, k, 2, 8, 0, u, lab, C)
+    L = lab.cpu().numpy()
+    idx = rng.choice(n, 3000, replace=False)
+    D = kmeans.sq_dists(X[idx], C)
+    assert np.array_equal(L[idx], np.argmin(D, axis=1))
+    # centroids of the final assignment: the member means of the labels the last update used
+    # differ from L only if the run stopped at max_iter; check the converged-or-not invariant
+    # through the exact dmin instead, plus member means when converged
+    Xd = X.astype(np.float64)
+    dm = np.zeros(n)
+    for q in range(d):
+        diff = Xd[:, q] - C[L, q]
+        dm += diff * diff
+    assert inertia == pytest.approx(math.fsum(dm), rel=1e-12)
+    if it < 8:   # converged: C are the exact member means of L
+        for c in rng.choice(k, 4, replace=False):
+            M = Xd[L == c]
+            if len(M):
+                want = np.array([math.fsum(M[:, q]) / len(M) for q in range(d)])
+                assert np.array_equal(C[c], want)
+
+
 def test_ari_matches_oracle(sc):
     rng = np.random.default_rng(0)
     for n, ka, kb in [(1000, 5, 7), (100000, 20, 20), (10, 1, 1), (4, 2, 2)]:
