@@ -551,11 +551,17 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
   const int64_t m = list ? (int64_t)*list_len : n;
   const int64_t p0 = (int64_t)blockIdx.x * kSPT;
   if (p0 >= m) return;
+  // the tile's point indices first (one load per thread, not one dependent load per row)
+  __shared__ int s_gi[kSPT];
+  if (tid < kSPT) {
+    const int64_t pi = p0 + tid;
+    s_gi[tid] = pi < m ? (list ? list[pi] : static_cast<int>(pi)) : -1;
+  }
+  __syncthreads();
   // staging: a warp takes one row (coalesced 4-byte cp.async, lanes along the row, stored
   // down the column), every copy of the tile in flight at once
   for (int row = warp; row < kSPT; row += 8) {
-    const int64_t pi = p0 + row;
-    const int64_t gi = pi < m ? (list ? (int64_t)list[pi] : pi) : -1;
+    const int64_t gi = s_gi[row];
     for (int q = lane; q < d; q += 32) {
       float* dst = sX + (size_t)q * kSLX + row;
       if (gi >= 0) {
@@ -655,7 +661,7 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
   const int col = ty * 8 + i;
   const int64_t pi = p0 + col;
   if (tx < 8 && pi < m) {
-    const int64_t gi = list ? (int64_t)list[pi] : pi;
+    const int64_t gi = s_gi[col];
     const ScreenBound sb(*cm, d);
     bool unique = false;
     double low = 0.0;
