@@ -231,9 +231,12 @@ void prof_launch_end(cudaStream_t s, cudaEvent_t e0, double algo_bytes, int step
 
 // all `order` steps of one column chunk in one cooperative launch when the CSR fits the
 // aggregate shared memory; *ok = false otherwise (sc_resident.cu)
+// stack != nullptr: stack mode (every T_j kept at stack + j * slot, row stride ld_x, T_0 in slot
+// 0, no Y) -- sc_stability's recurrence
 template <typename T>
 int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, int w, const T* Xc, int64_t ld_x,
-                    T* Yc, int64_t ld_y, T* buf0, T* buf1, cudaStream_t s, bool* ok);
+                    T* Yc, int64_t ld_y, T* buf0, T* buf1, cudaStream_t s, bool* ok, T* stack = nullptr,
+                    int64_t slot = 0);
 
 // column chunk widths (each a supported kernel width) covering R columns
 template <typename T>

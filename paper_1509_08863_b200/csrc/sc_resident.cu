@@ -82,9 +82,12 @@ struct ResidentParams {
   const StepCoef* coef;             // [order]
   const int64_t* tile_begin;        // [grid + 1] tile range of each CTA
   int cap_rows, cap_nnz;            // shared-memory capacity of a CTA's slice
+  // stack mode (sc_stability): every T_j kept, T_j at stack + j * slot, row stride ld_stack;
+  // T_0 is read from slot 0 and T_order is written (no Y)
+  void* stack; int64_t slot, ld_stack;
 };
 
-template <typename T, int VPR, int EB, bool UNIT>
+template <typename T, int VPR, int EB, bool UNIT, bool STACK>
 __global__ void __launch_bounds__(kRThreads, 2)
 cheb_resident_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                      const float* __restrict__ val, const T* __restrict__ strength,
@@ -125,13 +128,25 @@ cheb_resident_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restr
 
   for (int s = 0; s < rp.order; ++s) {
     const StepCoef cf = rp.coef[s];
-    const T* tcur = s == 0 ? static_cast<const T*>(rp.x) : static_cast<const T*>(s & 1 ? rp.buf1 : rp.buf0);
-    const int64_t ld_cur = s == 0 ? rp.ld_x : (int64_t)(SW * W);
-    const T* tprev = s == 0 ? nullptr
+    const T* tcur;
+    const T* tprev;
+    T* tnext;
+    int64_t ld_cur, ld_prev, ld_next;
+    if constexpr (STACK) {
+      T* st = static_cast<T*>(rp.stack);
+      tcur = st + s * rp.slot;
+      tprev = s == 0 ? nullptr : st + (s - 1) * rp.slot;
+      tnext = st + (s + 1) * rp.slot;
+      ld_cur = ld_prev = ld_next = rp.ld_stack;
+    } else {
+      tcur = s == 0 ? static_cast<const T*>(rp.x) : static_cast<const T*>(s & 1 ? rp.buf1 : rp.buf0);
+      ld_cur = s == 0 ? rp.ld_x : (int64_t)(SW * W);
+      tprev = s == 0 ? nullptr
                      : (s == 1 ? static_cast<const T*>(rp.x) : static_cast<const T*>((s - 1) & 1 ? rp.buf1 : rp.buf0));
-    const int64_t ld_prev = s == 1 ? rp.ld_x : (int64_t)(SW * W);
-    T* tnext = s == rp.order - 1 ? nullptr : static_cast<T*>((s + 1) & 1 ? rp.buf1 : rp.buf0);
-    const int64_t ld_next = SW * W;
+      ld_prev = s == 1 ? rp.ld_x : (int64_t)(SW * W);
+      tnext = s == rp.order - 1 ? nullptr : static_cast<T*>((s + 1) & 1 ? rp.buf1 : rp.buf0);
+      ld_next = SW * W;
+    }
     const char* gbase = reinterpret_cast<const char*>(tcur + c);
     const uint32_t ldb = static_cast<uint32_t>(ld_cur * sizeof(T));
     const T a = static_cast<T>(cf.a), bc = static_cast<T>(cf.b_cur), bp = static_cast<T>(cf.b_prev);
@@ -226,24 +241,32 @@ template <typename T>
 using RKernel = void (*)(const int64_t*, const int32_t*, const float*, const T*, const uint16_t*, ResidentParams);
 
 template <typename T, int VPR>
-RKernel<T> pick_r2(bool unit) {
+RKernel<T> pick_r2(bool unit, bool stack) {
   constexpr int EB = sizeof(T) == 4 ? 6 : 4;
-  if (unit) return cheb_resident_kernel<T, VPR, EB, true>;
-  return cheb_resident_kernel<T, VPR, EB, false>;
+  if constexpr (sizeof(T) == 4) {   // stack mode: fp32 only (sc_stability)
+    if (stack) {
+      if (unit) return cheb_resident_kernel<T, VPR, EB, true, true>;
+      return cheb_resident_kernel<T, VPR, EB, false, true>;
+    }
+  } else if (stack) {
+    return nullptr;
+  }
+  if (unit) return cheb_resident_kernel<T, VPR, EB, true, false>;
+  return cheb_resident_kernel<T, VPR, EB, false, false>;
 }
 template <typename T>
-RKernel<T> pick_r(int vpr, bool unit) {
+RKernel<T> pick_r(int vpr, bool unit, bool stack) {
   switch (vpr) {
-    case 1: return pick_r2<T, 1>(unit);
-    case 2: return pick_r2<T, 2>(unit);
-    case 3: return pick_r2<T, 3>(unit);
-    case 4: return pick_r2<T, 4>(unit);
-    case 6: return pick_r2<T, 6>(unit);
-    case 8: return pick_r2<T, 8>(unit);
-    case 12: return pick_r2<T, 12>(unit);
-    case 16: return pick_r2<T, 16>(unit);
-    case 24: return pick_r2<T, 24>(unit);
-    case 32: return pick_r2<T, 32>(unit);
+    case 1: return pick_r2<T, 1>(unit, stack);
+    case 2: return pick_r2<T, 2>(unit, stack);
+    case 3: return pick_r2<T, 3>(unit, stack);
+    case 4: return pick_r2<T, 4>(unit, stack);
+    case 6: return pick_r2<T, 6>(unit, stack);
+    case 8: return pick_r2<T, 8>(unit, stack);
+    case 12: return pick_r2<T, 12>(unit, stack);
+    case 16: return pick_r2<T, 16>(unit, stack);
+    case 24: return pick_r2<T, 24>(unit, stack);
+    case 32: return pick_r2<T, 32>(unit, stack);
     default: return nullptr;
   }
 }
@@ -263,18 +286,18 @@ size_t resident_smem(int cap_rows, int cap_nnz, bool unit) {
 // Returns SC_OK with *ok = false when the graph does not fit (caller uses the streaming path).
 template <typename T>
 int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, int w, const T* Xc, int64_t ld_x,
-                    T* Yc, int64_t ld_y, T* buf0, T* buf1, cudaStream_t s, bool* ok) {
+                    T* Yc, int64_t ld_y, T* buf0, T* buf1, cudaStream_t s, bool* ok, T* stack, int64_t slot) {
   *ok = false;
   const int total_w = (int)ld_x;
   constexpr int W = sizeof(T) == 4 ? 4 : 2;
   if (w % W || g->n_cols != g->n_rows) return SC_OK;
   const int vpr = w / W;
   if (vpr < 1 || vpr > 32) return SC_OK;
-  RKernel<T> k = pick_r<T>(vpr, g->unit_weights);
+  RKernel<T> k = pick_r<T>(vpr, g->unit_weights, stack != nullptr);
   if (!k) return SC_OK;
   const int tr = kRW * (32 / vpr);
   const int64_t n = g->n_rows, ntiles = (n + tr - 1) / tr;
-  const auto key = std::make_pair(w, (int)sizeof(T));
+  const auto key = std::make_pair(w | (stack ? (1 << 16) : 0), (int)sizeof(T));   // (the smem attribute is per kernel)
   auto pit = g->resident_plans.find(key);
   if (pit == g->resident_plans.end()) {
     // plan once per (graph, width): one CTA per SM (cooperative), tiles split evenly, the
@@ -332,7 +355,7 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
     c.b_cur = st == 0 ? -1.0 : -2.0;
     c.b_prev = st == 0 ? 0.0 : -1.0;
     const bool last = st == order - 1;
-    if (last || (st + 1) - added == 3) {
+    if (!stack && (last || (st + 1) - added == 3)) {
       c.cy_prev = (st >= 1 && added < st - 1) ? d[st - 1] : 0.0;
       c.cy_cur = (added < st) ? d[st] : 0.0;
       c.cy_next = d[st + 1];
@@ -357,6 +380,9 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
   rp.tile_begin = g->resident_tiles[key]->as<int64_t>();
   rp.cap_rows = cap_rows;
   rp.cap_nnz = cap_nnz;
+  rp.stack = stack;
+  rp.slot = slot;
+  rp.ld_stack = ld_x;
   const int64_t* a_rp = g->row_ptr.as<int64_t>();
   const int32_t* a_col = g->col_idx.as<int32_t>();
   const float* a_val = g->unit_weights ? nullptr : g->values.as<float>();
@@ -369,14 +395,14 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
   // algorithmic bytes as for the streaming path (§0(d)): per step the CSR share of this chunk
   // (prorated by w / total_w) and the dense operands touched once
   const double csr = (double)n * 8.0 + (double)g->nnz * (g->unit_weights ? 4.0 : 8.0);
-  const double dense = (double)n * w * sizeof(T) * (3.0 + 2.0 / 3.0);
+  const double dense = (double)n * w * sizeof(T) * (stack ? 3.0 : 3.0 + 2.0 / 3.0);
   prof_launch_end(s, e0, order * (csr * w / std::max(total_w, w) + dense), order);
   *ok = true;
   return SC_OK;
 }
 template int resident_filter<float>(sc_graph*, const double*, int, double, int, const float*, int64_t, float*, int64_t,
-                                    float*, float*, cudaStream_t, bool*);
+                                    float*, float*, cudaStream_t, bool*, float*, int64_t);
 template int resident_filter<double>(sc_graph*, const double*, int, double, int, const double*, int64_t, double*,
-                                     int64_t, double*, double*, cudaStream_t, bool*);
+                                     int64_t, double*, double*, cudaStream_t, bool*, double*, int64_t);
 
 }  // namespace sc

@@ -27,6 +27,11 @@
 namespace sc {
 namespace {
 
+bool env_resident() {
+  const char* v = std::getenv("SC_RESIDENT");
+  return !(v && std::atoi(v) == 0);
+}
+
 constexpr int kKG = 8;   // cuts formed per pass over the T_m stack
 
 // Y[g][i*R + q] = sum_m D[g][m] * T[m][i*ld + q]  for the kg cuts of this pass
@@ -195,8 +200,23 @@ int stability_scan(sc_graph* g, int k_min, int k_max, int J, int R, int order, b
         pad_copy_kernel<<<grid, 256, 0, s>>>(sig.as<float>(), n, R, T, ld);
         SC_CUDA_TRY(cudaGetLastError());
       }
-      // T_{m+1} = 2 L~ T_m - T_{m-1}  (T_1 = L~ T_0), every term kept
-      for (int st = 0; st < order; ++st) {
+      // T_{m+1} = 2 L~ T_m - T_{m-1}  (T_1 = L~ T_0), every term kept: one cooperative launch
+      // per column chunk when the CSR fits shared memory (resident kernel, stack mode), else
+      // one streaming launch per step and chunk
+      bool resident = env_resident();
+      if (resident) {
+        int col0 = 0;
+        for (int w : chunks) {
+          bool ok = false;
+          SC_TRY(resident_filter<float>(g, nullptr, order, lambda_max, w, T + col0, ld, nullptr, 0, nullptr, nullptr, s,
+                                        &ok, T + col0, slot));
+          if (!ok) { resident = false; break; }
+          col0 += w;
+        }
+        // (a graph that fits does so for every chunk width of the plan; if the first chunk
+        // did not, nothing was launched)
+      }
+      for (int st = 0; st < order && !resident; ++st) {
         int col0 = 0;
         for (int w : chunks) {
           StepParams p{};
