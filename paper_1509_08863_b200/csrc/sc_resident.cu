@@ -240,9 +240,12 @@ cheb_resident_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restr
 template <typename T>
 using RKernel = void (*)(const int64_t*, const int32_t*, const float*, const T*, const uint16_t*, ResidentParams);
 
+#ifndef SC_REB_F32
+#define SC_REB_F32 4   // gathers in flight per lane, resident kernel (fp32; measured best of 3-8)
+#endif
 template <typename T, int VPR>
 RKernel<T> pick_r2(bool unit, bool stack) {
-  constexpr int EB = sizeof(T) == 4 ? 6 : 4;
+  constexpr int EB = sizeof(T) == 4 ? SC_REB_F32 : 4;
   if constexpr (sizeof(T) == 4) {   // stack mode: fp32 only (sc_stability)
     if (stack) {
       if (unit) return cheb_resident_kernel<T, VPR, EB, true, true>;
