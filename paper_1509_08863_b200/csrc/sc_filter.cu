@@ -20,6 +20,7 @@
 // blocks instead of 5.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -93,6 +94,18 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+#ifndef SC_GATHER_HINT
+#define SC_GATHER_HINT 0   // L2 policy of the gathers: 0 default (ld.global.nc), 1 evict_last, 2 evict_normal
+#endif
+__device__ __forceinline__ uint64_t policy_gather() {
+  uint64_t pol;
+#if SC_GATHER_HINT == 1
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#else
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
 // 16-byte global -> shared async copy (LDGSTS, bypasses L1) with an L2 policy
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
@@ -115,6 +128,11 @@ template <> struct Stream<float> {
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
                  : "l"(p), "l"(pol));
   }
+  __device__ __forceinline__ static void ld_hint(const float* p, float (&v)[4], uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                 : "l"(p), "l"(pol));
+  }
   __device__ __forceinline__ static void st(float* p, const float (&v)[4], uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v[0]),
                  "f"(v[1]), "f"(v[2]), "f"(v[3]), "l"(pol)
@@ -126,6 +144,9 @@ template <> struct Stream<double> {
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                  : "=d"(v[0]), "=d"(v[1])
                  : "l"(p), "l"(pol));
+  }
+  __device__ __forceinline__ static void ld_hint(const double* p, double (&v)[2], uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
   }
   __device__ __forceinline__ static void st(double* p, const double (&v)[2], uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v[0]), "d"(v[1]),
@@ -164,6 +185,10 @@ template <> struct Stream<double> {
 #endif
 #ifndef SC_EB_F32
 #define SC_EB_F32 6       // gathers in flight per lane (fp32)
+#endif
+#ifndef SC_L2_PREFETCH
+#define SC_L2_PREFETCH 0  // 1: producer warp prefetches the next tile's gathered rows into L2
+                          // (measured 7-10 % slower on configs[3]: profiles/r01_chunk_l2_sweep.md)
 #endif
 #ifndef SC_EB_F64
 #define SC_EB_F64 4       // gathers in flight per lane (fp64)
@@ -239,6 +264,9 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   __syncthreads();
 
   const uint64_t pol_stream = policy_evict_first();
+#if SC_GATHER_HINT
+  const uint64_t pol_gather = policy_gather();
+#endif
 
   if (warp == kNC) {
     // ------------------------------------------------------------ producer
@@ -280,6 +308,31 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
             if (!UNIT) bulk_g2s(st + lay.val_off, val + ca, (uint32_t)(ncol * 4), &full[s], pol_stream);
           }
         }
+#if SC_L2_PREFETCH
+        // L2 prefetch of the rows of T_s that tile i-1 will gather (its column segment has
+        // landed in stage (i-1) % S by now; the consumers are still on older tiles): the DRAM
+        // misses of the random gathers are taken by fire-and-forget prefetches that hold no
+        // registers, so the consumers' register window mostly sees L2 hits.
+        if (i >= 1) {
+          const int sp = (i - 1) % S;
+          mbar_wait(&full[sp], ((i - 1) / S) & 1);
+          const TileMeta& mp = meta[sp];
+          if (!mp.overflow) {
+            const unsigned char* stp = stages + (size_t)sp * lay.stage_bytes;
+            const int64_t* rpp = reinterpret_cast<const int64_t*>(stp + lay.rp_off);
+            const int32_t* cip = reinterpret_cast<const int32_t*>(stp + lay.col_off);
+            const int q0 = static_cast<int>(rpp[mp.r0 - mp.rpa] - mp.ca);
+            const int q1 = static_cast<int>(rpp[mp.r1 - mp.rpa] - mp.ca);
+            constexpr int kLines = (VPR * 16 + 127) / 128;
+            for (int q = q0 + lane; q < q1; q += 32) {
+              const char* a = reinterpret_cast<const char*>(p.tcur) +
+                              static_cast<uint64_t>(static_cast<uint32_t>(cip[q])) * (uint64_t)(p.ld_cur * sizeof(T));
+#pragma unroll
+              for (int l = 0; l < kLines; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + l * 128));
+            }
+          }
+        }
+#endif
       }
     }
     // drain: wait until the consumers released every stage still in use
@@ -346,7 +399,12 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
         const int k = ok ? ci[pos] : 0;
         if (!UNIT) wv[e] = ok ? static_cast<T>(wi[pos]) : T(0);
         if (ok) {
+#if SC_GATHER_HINT
+          Stream<T>::ld_hint(reinterpret_cast<const T*>(gbase + static_cast<uint64_t>(static_cast<uint32_t>(k)) * ldb),
+                             g[e], pol_gather);
+#else
           Vec<T>::ldg(reinterpret_cast<const T*>(gbase + static_cast<uint64_t>(static_cast<uint32_t>(k)) * ldb), g[e]);
+#endif
         } else {
 #pragma unroll
           for (int w = 0; w < W; ++w) g[e][w] = T(0);
@@ -553,6 +611,29 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
+// SC_PERSIST_MB > 0 (experiment): reserve that much L2 for persisting lines and launch every
+// step with an access-policy window over its gathered table
+size_t g_persist_max_window = 0;
+size_t persist_bytes() {
+  static const size_t v = [] {
+    const int mb = env_int("SC_PERSIST_MB", 0);
+    if (mb <= 0) return (size_t)0;
+    int dev = 0, maxp = 0, maxw = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    const size_t want = std::min((size_t)mb << 20, (size_t)maxp);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+    g_persist_max_window = (size_t)maxw;
+    std::fprintf(stderr, "[sc] persisting L2: max %d B, window max %d B, set %zu B\n", maxp, maxw, got);
+    return got;
+  }();
+  return v;
+}
+size_t persist_max_window() { return g_persist_max_window; }
+
 template <typename T>
 using KernelFn = void (*)(const int64_t*, const int32_t*, const float*, const T*, const uint16_t*, StepParams, int,
                           int);
@@ -655,9 +736,32 @@ int launch_step_impl(const sc_graph* g, const StepParams& p, cudaStream_t s, boo
   const uint16_t* order = tile_order(g, tr, p.row_begin, p.row_end, s);
   if (!order) return fail(SC_ERR_NOMEM, "tile order allocation failed");
   StepParams q = p;
-  k<<<grid, kThreads, smem, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(),
-                                 g->unit_weights ? nullptr : g->values.as<float>(), strength_of<T>(g), order, q, cap,
-                                 nst);
+  const size_t persist = persist_bytes();
+  if (persist) {
+    // experiment (SC_PERSIST_MB): an L2 persisting window over the gathered table T_s
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    const size_t tbytes = (size_t)g->n_cols * p.ld_cur * sizeof(T);
+    at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(p.tcur);
+    at[0].val.accessPolicyWindow.num_bytes = std::min(tbytes, persist_max_window());
+    at[0].val.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist / (double)tbytes);
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(),
+                                   g->unit_weights ? nullptr : g->values.as<float>(), strength_of<T>(g), order, q, cap,
+                                   nst));
+  } else {
+    k<<<grid, kThreads, smem, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(),
+                                   g->unit_weights ? nullptr : g->values.as<float>(), strength_of<T>(g), order, q, cap,
+                                   nst);
+  }
   SC_CUDA_TRY(cudaGetLastError());
   if (g_prof.on) {
     cudaEventRecord(e1, s);
