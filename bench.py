@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="row-partitioned runs: halo rows stored by the step kernel into the peers (p2p, CUDA IPC "
                          "over NVLink) or exchanged with NCCL send/recv")
+    ap.add_argument("--col-groups", type=int, default=0,
+                    help="multi-GPU: column groups of the 2-D decomposition (0 = auto: the most groups "
+                         "with >= 32 columns each; 1 = pure row partition)")
     ap.add_argument("--dist-path", action="store_true",
                     help="use the row-partitioned NCCL filter even on one rank (exercises the multi-GPU path)")
     return ap.parse_args()
@@ -225,7 +228,16 @@ def base_config(args, g, w, world):
             "l2": (f"inputs larger than L2 ({ws / 2**20:.0f} MB working set > 126 MB L2); no flush" if ws > 2 * L2_BYTES
                    else f"working set {ws / 2**20:.0f} MB fits L2: L2 flushed (256 MB write) before every timed step, "
                         "each step timed alone"),
-            "parallelism": f"row-partitioned x{world}" if world > 1 else "single GPU"}
+            "parallelism": grid_label(args, w, world)}
+
+
+def grid_label(args, w, world):
+    if world == 1:
+        return "single GPU"
+    from paper_1509_08863_b200 import dist as pdist
+    cg, rg = pdist.grid_shape(world, w.R, col_groups=args.col_groups or None)
+    return (f"{cg} column groups x {rg} row blocks (columns sharded without exchange, rows "
+            f"row-partitioned with halo exchange)" if cg > 1 else f"row-partitioned x{world}")
 
 
 # ---------------------------------------------------------------------------
@@ -264,8 +276,15 @@ def run_ours(args):
         # lambda bounds on rank-local copies are not needed: Gershgorin bound + fixed cut
         lmax = 2.0 * float(g.degrees().max())
         lam_k, count_k = 0.25 * lmax, float("nan")
-        part = pdist.local_part(g.row_ptr, g.col_idx, g.values, n, rank, world)
-        part = (pdist.exchange_send_lists(part) if world > 1
+        # 2-D decomposition: column group cgrp filters columns [c0, c1) of every row; its
+        # n_row ranks row-partition the graph and exchange halos among themselves only
+        n_cg, n_row = pdist.grid_shape(world, R, col_groups=args.col_groups or None)
+        cgrp, rrank, _ = pdist.grid_coords(rank, world, n_cg)
+        c0, c1 = pdist.column_range(R, n_cg, cgrp)
+        groups = pdist.make_row_groups(world, n_cg)
+        rgroup = groups[cgrp] if world > 1 else None
+        part = pdist.local_part(g.row_ptr, g.col_idx, g.values, n, rrank, n_row)
+        part = (pdist.exchange_send_lists(part, group=rgroup) if n_row > 1
                 else pdist.send_lists_from_halos(part, [part.halo_gid]))
         Gl = sc.Graph(part.n_local, part.row_ptr, part.col_idx, part.values, n_cols=part.n_local + part.n_halo)
         handle = Gl.handle
@@ -283,18 +302,22 @@ def run_ours(args):
         from paper_1509_08863_b200 import dist as pdist
         Xl = torch.empty((part.n_local, R), dtype=torch.float32, device=dev)
         sc.sc_random_signals_f32(part.n_local, R, part.r0, args.seed, 0, 0.0, Xl)
-        Xp = Xl[torch.as_tensor(part.perm, device=dev)].contiguous()   # the rank's local row order
+        # the rank's rows in local (interior-first) order, its column group's columns
+        Xp = Xl[torch.as_tensor(part.perm, device=dev), c0:c1].contiguous()
+        del Xl
         Yp = torch.empty_like(Xp)
         exchange = args.exchange
         if exchange == "p2p":
             try:
-                nf = pdist.P2PFilter(part, handle, n, R)
+                nf = pdist.P2PFilter(part, handle, n, c1 - c0, group=rgroup)
             except Exception as e:   # IPC mapping unavailable: the NCCL schedule instead
                 print(f"[bench] p2p exchange setup failed ({e}); using NCCL", file=sys.stderr)
                 exchange = f"nccl (p2p setup failed: {str(e)[:80]})"
-                nf = pdist.NcclFilter(part, handle)
+                nf = pdist.NcclFilter(part, handle, group=rgroup)
         else:
-            nf = pdist.NcclFilter(part, handle)
+            nf = pdist.NcclFilter(part, handle, group=rgroup)
+        if n_row == 1:
+            exchange = "none (one row block per column group: no halo)"
 
         def step():
             dd = sc.sc_cheby_coeffs(lam_k, lmax, order, w.jackson)
@@ -355,14 +378,16 @@ def run_ours(args):
     bytes_per_launch = algo_bytes / max(step_launches, 1)
     achieved = bytes_per_launch / avg_launch_s / 1e9
     traffic = ncu_traffic(args.workload)
-    # gathered bytes: every nonzero of W reads one R-wide row of T_s per step
-    gather_gbps = float(g.nnz) * R * 4 * order * args.steps / (kern_ms / 1e3) / 1e9
+    # gathered bytes: every nonzero of W reads one R-wide row of T_s per step (rank 0's share
+    # of the graph and of the columns when partitioned: its own launches are the ones timed)
+    nnz_r, R_r, n_tab = ((int(part.col_idx.size), c1 - c0, n) if partitioned else (int(g.nnz), R, n))
+    gather_gbps = float(nnz_r) * R_r * 4 * order * args.steps / (kern_ms / 1e3) / 1e9
     cw = int(os.environ.get("SC_CHUNK", "0")) or None
     if cw is None:   # the library's chunk rule, in 16-byte vectors
-        cv = next((v for v in (32, 24, 16, 12, 8, 6, 4, 3, 2, 1) if n * v * 16 <= 128 * 2 ** 20), 1)
+        cv = next((v for v in (32, 24, 16, 12, 8, 6, 4, 3, 2, 1) if n_tab * v * 16 <= 128 * 2 ** 20), 1)
         cw = 4 * (cv if cv * 16 >= 128 else 16)
-    cw = min(cw, R)
-    gceil, gcase = gather_ceiling(cw * 4, n * cw * 4)
+    cw = min(cw, R_r)
+    gceil, gcase = gather_ceiling(cw * 4, (part.n_local + part.n_halo if partitioned else n) * cw * 4)
 
     out = None
     if rank == 0:
@@ -389,9 +414,9 @@ def run_ours(args):
     # ---- e2e through the C ABI with pinned host buffers, row-partitioned: every rank copies
     # its local rows in and out; bytes are the whole job's, time the max over ranks
     if partitioned and not args.no_e2e:
-        Xh = torch.empty((part.n_local, R), dtype=torch.float32, pin_memory=True)
+        Xh = torch.empty(tuple(Xp.shape), dtype=torch.float32, pin_memory=True)
         Xh.copy_(Xp)
-        Yh = torch.empty((part.n_local, R), dtype=torch.float32, pin_memory=True)
+        Yh = torch.empty(tuple(Xp.shape), dtype=torch.float32, pin_memory=True)
         for _ in range(2):
             nf.filter(d, order, lmax, Xh, Yh)
         barrier()

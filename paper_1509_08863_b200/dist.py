@@ -123,6 +123,58 @@ def send_lists_from_halos(part: LocalPart, halos) -> LocalPart:
 
 
 # ---------------------------------------------------------------------------
+# 2-D decomposition: column groups x row blocks
+# ---------------------------------------------------------------------------
+#
+# The columns of the signal block are independent filters (Y[:, q] = F^p R[:, q], PAPER.md
+# Eq.(10) l.321 applies the same filter to every signal), so they shard across ranks with no
+# exchange at all; only a row split needs the halo of T_j every step.  On graphs whose
+# edges are spread at random (SBM) a row block's halo is nearly every other row, so the
+# per-step halo traffic of a pure row partition grows with the number of ranks while its
+# compute shrinks; splitting the columns first keeps each rank's gathered rows >= 128 bytes
+# (the kernel is bound by gathered lines) and divides the halo traffic by the
+# number of column groups.  Ranks [c * n_row, (c + 1) * n_row) form column group c; inside it
+# they row-partition the graph exactly as above.
+
+def grid_shape(world: int, R: int, min_cols: int = 32, col_groups: int | None = None):
+    """(n_col_groups, n_row_blocks) for `world` ranks and R columns: the most column groups
+    that divide world and R (in 4-column vectors) with >= min_cols columns each, unless
+    col_groups is given."""
+    if col_groups is not None:
+        if world % col_groups or R % col_groups or (R // col_groups) % 4:
+            raise ValueError(f"{col_groups} column groups do not divide world={world} and R={R} into 4-column sets")
+        return col_groups, world // col_groups
+    best = 1
+    for c in range(1, world + 1):
+        if world % c == 0 and R % c == 0 and (R // c) % 4 == 0 and R // c >= min_cols:
+            best = c
+    return best, world // best
+
+
+def grid_coords(rank: int, world: int, n_col_groups: int):
+    """(column group, row rank inside the group, global ranks of the group)."""
+    n_row = world // n_col_groups
+    c = rank // n_row
+    return c, rank % n_row, list(range(c * n_row, (c + 1) * n_row))
+
+
+def column_range(R: int, n_col_groups: int, c: int):
+    """Columns [c0, c1) of column group c."""
+    w = R // n_col_groups
+    return c * w, (c + 1) * w
+
+
+def make_row_groups(world: int, n_col_groups: int):
+    """One process group per column group (collective: every rank calls it with the same
+    arguments); returns the list indexed by column group (None for world 1)."""
+    import torch.distributed as dist
+    if world == 1:
+        return [None]
+    n_row = world // n_col_groups
+    return [dist.new_group(list(range(c * n_row, (c + 1) * n_row))) for c in range(n_col_groups)]
+
+
+# ---------------------------------------------------------------------------
 # step schedule (coefficients per launch; DESIGN.md "fused step")
 # ---------------------------------------------------------------------------
 
@@ -247,7 +299,7 @@ class NcclFilter:
         uid = [_lib.sc_nccl_unique_id() if part.rank == 0 else None]
         if part.world > 1:
             import torch.distributed as dist
-            dist.broadcast_object_list(uid, src=0, group=group)
+            dist.broadcast_object_list(uid, group=group, group_src=0)
         self.comm = _lib.sc_comm_init(uid[0], part.world, part.rank)
         self.plan = _lib.sc_dist_create(graph_handle, self.comm, part.n_interior, part.send_idx,
                                         np.asarray(part.send_counts, dtype=np.int64),

@@ -180,3 +180,74 @@ def test_p2p_scatter_reference_reproduces_halos(world):
     got = pdist.p2p_scatter_reference(parts, T_locals)
     for p, h in zip(parts, got):
         assert np.array_equal(h, X[p.halo_gid])
+
+
+# ---------------------------------------------------------------------------
+# 2-D decomposition: column groups (no exchange) x row blocks (halo exchange inside the
+# group's own process group)
+# ---------------------------------------------------------------------------
+
+def _grid_worker(rank, world, port, gspec, R, order, n_cg, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_08863_b200 import dist as pdist
+        g = scinputs.sbm(**gspec)
+        n_cg2, n_row = pdist.grid_shape(world, R, min_cols=4, col_groups=n_cg)
+        cgrp, rrank, members = pdist.grid_coords(rank, world, n_cg2)
+        c0, c1 = pdist.column_range(R, n_cg2, cgrp)
+        groups = pdist.make_row_groups(world, n_cg2)
+        part = pdist.local_part(g.row_ptr, g.col_idx, g.values, g.n, rrank, n_row)
+        part = (pdist.exchange_send_lists(part, group=groups[cgrp]) if n_row > 1
+                else pdist.send_lists_from_halos(part, [part.halo_gid]))
+        lmax = 2.0 * float(g.degrees().max())
+        d = chebyshev.filter_coeffs(0.15 * lmax, lmax, order, True)
+        X = torch.from_numpy(scinputs.gaussian_block(5, g.n, R).astype(np.float64))
+        Xl = X[part.r0:part.r1, c0:c1].contiguous()
+        Y = pdist.run_filter(part, _cpu_step_fn(part), d, order, lmax, Xl, group=groups[cgrp])
+        outs = [None] * world
+        dist.all_gather_object(outs, (part.r0, part.r1, c0, c1, Y.numpy(), rank in members))
+        if rank == 0:
+            Yfull = np.full((g.n, R), np.nan)
+            for r0, r1, a, b, y, _ in outs:
+                assert np.all(np.isnan(Yfull[r0:r1, a:b]))   # every block written exactly once
+                Yfull[r0:r1, a:b] = y
+            Yo = chebyshev.cheb_filter(laplacian.laplacian(g), X.numpy(), d, lmax)
+            err = np.linalg.norm(Yfull - Yo) / np.linalg.norm(Yo)
+            q.put((err, (n_cg2, n_row), all(o[5] for o in outs)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_cg", [(4, 2), (2, 2)])
+def test_column_x_row_grid_filter_gloo(world, n_cg):
+    gspec = dict(n=1000, k=4, avg_degree=8, eps=0.1, seed=7)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grid_worker, args=(r, world, port, gspec, 8, 15, n_cg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+        assert p.exitcode == 0
+    err, shape, member_ok = q.get(timeout=10)
+    assert shape == (n_cg, world // n_cg) and member_ok
+    assert err < 1e-12
+
+
+def test_grid_shape_rule():
+    from paper_1509_08863_b200 import dist as pdist
+    # configs[3] (R = 64): 2 column groups of 32 once there are >= 2 ranks
+    assert [pdist.grid_shape(w, 64) for w in (1, 2, 4, 8)] == [(1, 1), (2, 1), (2, 2), (2, 4)]
+    # configs[4] (R = 96): 2 groups of 48 (3 does not divide 2, 4 or 8; 4 groups would be 24 wide)
+    assert [pdist.grid_shape(w, 96) for w in (1, 2, 4, 8)] == [(1, 1), (2, 1), (2, 2), (2, 4)]
+    # R too narrow for two >= 32-column groups: pure row partition
+    assert pdist.grid_shape(8, 48) == (1, 8)
+    assert pdist.grid_shape(8, 64, col_groups=1) == (1, 8)
+    assert pdist.grid_shape(8, 64, col_groups=4) == (4, 2)
+    with pytest.raises(ValueError):
+        pdist.grid_shape(8, 64, col_groups=3)
+    assert pdist.grid_coords(5, 8, 2) == (1, 1, [4, 5, 6, 7])
+    assert pdist.column_range(64, 2, 1) == (32, 64)

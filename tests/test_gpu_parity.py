@@ -644,6 +644,37 @@ def test_p2p_fused_exchange_emulated(sc, world, R, chunk, waits, monkeypatch):
         grp.close()
 
 
+@pytest.mark.parametrize("world,n_cg,R", [(4, 2, 16), (8, 2, 24), (2, 2, 8)])
+def test_column_x_row_grid_emulated(sc, world, n_cg, R):
+    """The 2-D decomposition bench.py uses on N GPUs (dist.grid_shape): column group c filters
+    columns column_range(R, n_cg, c) of every row; its world/n_cg ranks row-partition the graph
+    with the fused peer-store exchange among themselves only.  Each column group's ranks are
+    emulated on this GPU (sc_p2p_filter_group_f32); the assembled block vs the oracle."""
+    from paper_1509_08863_b200 import dist as pdist
+    g = scinputs.sbm(2400, 6, 10, 0.1, seed=22)
+    order = 25
+    lmax = 2.0 * float(g.degrees().max())
+    d = chebyshev.filter_coeffs(0.15 * lmax, lmax, order, True)
+    X = scinputs.gaussian_block(6, g.n, R)
+    cg, n_row = pdist.grid_shape(world, R, min_cols=4, col_groups=n_cg)
+    Y = np.full((g.n, R), np.nan)
+    for c in range(cg):
+        c0, c1 = pdist.column_range(R, cg, c)
+        grp = pdist.P2PGroup(g.row_ptr, g.col_idx, g.values, g.n, n_row, c1 - c0)
+        try:
+            Xs = [torch.from_numpy(np.ascontiguousarray(X[p.r0:p.r1, c0:c1][p.perm])).cuda() for p in grp.parts]
+            Ys = [torch.full_like(x, float("nan")) for x in Xs]
+            grp.filter(d, order, lmax, Xs, Ys)
+            torch.cuda.synchronize()
+            for p, y in zip(grp.parts, Ys):
+                Y[p.r0 + p.perm, c0:c1] = y.cpu().numpy()
+        finally:
+            grp.close()
+    Yo = chebyshev.cheb_filter(laplacian.laplacian(g), X.astype(np.float64), d, lmax)
+    assert not np.isnan(Y).any()
+    assert rel(Y, Yo) <= F32_TOL
+
+
 def test_p2p_filter_single_rank_host_buffers(sc):
     """sc_p2p_filter_f32 (the multi-process entry point: chunk-start waits, T_0 push,
     signalled steps) on a 1-rank partition with host X / Y, incl. a ragged R."""
