@@ -636,21 +636,40 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
     uint64_t acc[8][2];
 #pragma unroll
     for (int i = 0; i < 8; ++i) { acc[i][0] = 0ull; acc[i][1] = 0ull; }
+    if (kt > 32) {
 #pragma unroll 4
-    for (int q = 0; q < d; ++q) {
-      const float4 xa = *reinterpret_cast<const float4*>(sX + (size_t)q * kSLX + ty * 8);
-      const float4 xb = *reinterpret_cast<const float4*>(sX + (size_t)q * kSLX + ty * 8 + 4);
-      const uint64_t c01 = *reinterpret_cast<const uint64_t*>(sC + (size_t)q * kSLC + 2 * tx);
-      const uint64_t c23 = *reinterpret_cast<const uint64_t*>(sC + (size_t)q * kSLC + 2 * tx + 32);
-      const float xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+      for (int q = 0; q < d; ++q) {
+        const float4 xa = *reinterpret_cast<const float4*>(sX + (size_t)q * kSLX + ty * 8);
+        const float4 xb = *reinterpret_cast<const float4*>(sX + (size_t)q * kSLX + ty * 8 + 4);
+        const uint64_t c01 = *reinterpret_cast<const uint64_t*>(sC + (size_t)q * kSLC + 2 * tx);
+        const uint64_t c23 = *reinterpret_cast<const uint64_t*>(sC + (size_t)q * kSLC + 2 * tx + 32);
+        const float xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint64_t xv = pack2(xs[i], xs[i]);
-        uint64_t d0, d1;
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d0) : "l"(xv), "l"(c01));
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d1) : "l"(xv), "l"(c23));
-        asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc[i][0]) : "l"(d0));
-        asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc[i][1]) : "l"(d1));
+        for (int i = 0; i < 8; ++i) {
+          const uint64_t xv = pack2(xs[i], xs[i]);
+          uint64_t d0, d1;
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d0) : "l"(xv), "l"(c01));
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d1) : "l"(xv), "l"(c23));
+          asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc[i][0]) : "l"(d0));
+          asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc[i][1]) : "l"(d1));
+        }
+      }
+    } else {
+      // tail tile of <= 32 centroids (e.g. k = 200 = 3 x 64 + 8): the upper half of the
+      // tile is padding, skip its arithmetic
+#pragma unroll 4
+      for (int q = 0; q < d; ++q) {
+        const float4 xa = *reinterpret_cast<const float4*>(sX + (size_t)q * kSLX + ty * 8);
+        const float4 xb = *reinterpret_cast<const float4*>(sX + (size_t)q * kSLX + ty * 8 + 4);
+        const uint64_t c01 = *reinterpret_cast<const uint64_t*>(sC + (size_t)q * kSLC + 2 * tx);
+        const float xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint64_t xv = pack2(xs[i], xs[i]);
+          uint64_t d0;
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d0) : "l"(xv), "l"(c01));
+          asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc[i][0]) : "l"(d0));
+        }
       }
     }
     __syncthreads();   // every warp is done reading sC before the next request refills it
