@@ -275,7 +275,7 @@ def run_ours(args):
         from paper_1509_08863_b200 import dist as pdist
         # lambda bounds on rank-local copies are not needed: Gershgorin bound + fixed cut
         lmax = 2.0 * float(g.degrees().max())
-        lam_k, count_k = 0.25 * lmax, float("nan")
+        lam_k, count_k = 0.25 * lmax, None
         # 2-D decomposition: column group cgrp filters columns [c0, c1) of every row; its
         # n_row ranks row-partition the graph and exchange halos among themselves only
         n_cg, n_row = pdist.grid_shape(world, R, col_groups=args.col_groups or None)
