@@ -559,8 +559,9 @@ __global__ void centroid_prep_kernel(const double* __restrict__ C, int k, int d,
 
 constexpr int kSPT = 128;              // points per block of the screen
 constexpr int kSLX = kSPT + 4;         // padded leading dimensions (16-byte aligned rows)
-constexpr int kSLC = kAT + 4;
+constexpr int kSLC = kAT + 2;         // (8-byte aligned rows; staging writes at most 2-way conflicted)
 
+template <int NBUF>
 __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __restrict__ F, int64_t n, int d,
                                                             const double* __restrict__ C,
                                                             const float* __restrict__ Cf,
@@ -570,13 +571,15 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
                                                             int32_t* __restrict__ lab, double* __restrict__ dmin,
                                                             double* __restrict__ lo, int32_t* __restrict__ amb,
                                                             int* __restrict__ amb_len) {
+  constexpr int nbuf = NBUF;
   // 128 points x 64-centroid tiles per block; thread (ty, tx) owns points ty*8 .. ty*8+7 and
   // the centroid pairs (2tx, 2tx+1), (2tx+32, 2tx+33) of a tile: 16 packed accumulators.
   // Packed fp32x2 arithmetic (FADD2/FFMA2: two IEEE round-to-nearest lanes per instruction,
   // the same rounding as scalar code, so the bound above holds lane by lane).
   extern __shared__ float smf[];
   float* sX = smf;                                    // [d][kSLX]
-  float* sCb = smf + (size_t)d * kSLX;                // 2 x [d][kSLC]: double-buffered centroid tiles
+  float* sCb = smf + (size_t)d * kSLX;                // nbuf x [d][kSLC]: centroid tiles (double-
+                                                      // buffered unless that costs the 3rd block/SM)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tx = tid & 15, ty = tid >> 4;
   const int64_t m = list ? (int64_t)*list_len : n;
@@ -625,8 +628,8 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
   stage_c(0, sCb);   // (commits the point tile's copies too)
   for (int c0 = 0, t = 0; c0 < k; c0 += kAT, ++t) {
     const int kt = min(kAT, k - c0);
-    float* sC = sCb + (size_t)(t & 1) * d * kSLC;
-    if (c0 + kAT < k) {
+    float* sC = sCb + (size_t)(nbuf == 2 ? (t & 1) : 0) * d * kSLC;
+    if (nbuf == 2 && c0 + kAT < k) {
       stage_c(c0 + kAT, sCb + (size_t)((t + 1) & 1) * d * kSLC);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
@@ -673,6 +676,7 @@ __global__ void __launch_bounds__(256, 3) assign_screen_kernel(const float* __re
       }
     }
     __syncthreads();   // every warp is done reading sC before the next request refills it
+    if (nbuf == 1 && c0 + kAT < k) stage_c(c0 + kAT, sCb);
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -1257,8 +1261,15 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   }
   auto assign3 = nc_best == 4 ? assign3_kernel<4> : nc_best == 2 ? assign3_kernel<2> : assign3_kernel<1>;
   SC_CUDA_TRY(cudaFuncSetAttribute(assign3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
-  const int smem_screen = (int)(sizeof(float) * (size_t)d * (kSLX + 2 * kSLC));
-  SC_CUDA_TRY(cudaFuncSetAttribute(assign_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_screen));
+  // double-buffered centroid tiles unless that drops the screen below 3 blocks per SM (d > ~70)
+  int smem_sm = 0, cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, cur_dev);
+  const auto screen_bytes = [&](int nb) { return (int)(sizeof(float) * (size_t)d * (kSLX + nb * kSLC)); };
+  const int screen_nbuf = 3 * (screen_bytes(2) + 512 + 1024) <= smem_sm ? 2 : 1;
+  const int smem_screen = screen_bytes(screen_nbuf);
+  SC_CUDA_TRY(cudaFuncSetAttribute(screen_nbuf == 2 ? assign_screen_kernel<2> : assign_screen_kernel<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_screen));
   // the screen pays off when the exact scan is expensive (env SC_KMEANS_SCREEN=0 disables it)
   const double screen_min = std::getenv("SC_KMEANS_SCREEN_MIN") ? std::atof(std::getenv("SC_KMEANS_SCREEN_MIN"))
                                                                 : 134217728.0;
@@ -1300,7 +1311,8 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
         centroid_prep_kernel<<<1, 256, 0, s>>>(C, k, d, d_Cf, d_cm);
         SC_CUDA_TRY(cudaGetLastError());
       }
-      assign_screen_kernel<<<(unsigned)((n + kSPT - 1) / kSPT), 256, smem_screen, s>>>(
+      (screen_nbuf == 2 ? assign_screen_kernel<2> : assign_screen_kernel<1>)<<<(unsigned)((n + kSPT - 1) / kSPT),
+                                                                               256, smem_screen, s>>>(
           F, n, d, C, d_Cf, d_cm, k, pruned ? b_list.as<int32_t>() : nullptr, pruned ? b_len.as<int>() : nullptr,
           out_lab, b_dmin.as<double>(), b_lo.as<double>(), b_amb.as<int32_t>(), amb_len);
       SC_CUDA_TRY(cudaGetLastError());
@@ -1502,7 +1514,8 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   // its own stream and stream-ordered workspace (the pruned Lloyd phase and the k-means++
   // draws are latency-bound, so concurrent restarts overlap); the winner is the same as in
   // a sequential loop (lowest inertia, ties -> lowest restart index).
-  const int P = (restarts > 1 && (double)n * d >= 4.0e6) ? std::min(restarts, 4) : 1;
+  static const int max_workers = std::getenv("SC_KMEANS_WORKERS") ? std::max(1, std::atoi(std::getenv("SC_KMEANS_WORKERS"))) : 4;
+  const int P = (restarts > 1 && (double)n * d >= 4.0e6) ? std::min(restarts, max_workers) : 1;
   std::vector<KmResult> res(P);
   if (P == 1) {
     SC_TRY(kmeans_worker(F, n, d, k, 0, 1, restarts, max_iter, seed, uniforms_host, labels_dev, &res[0], s));
