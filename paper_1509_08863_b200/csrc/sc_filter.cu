@@ -191,7 +191,13 @@ template <> struct Stream<double> {
                           // (measured 7-10 % slower on configs[3]: profiles/r01_chunk_l2_sweep.md)
 #endif
 #ifndef SC_EB_F64
-#define SC_EB_F64 4       // gathers in flight per lane (fp64)
+#define SC_EB_F64 5       // gathers in flight per lane (fp64; measured 4/5/6: 230/219/220 ms, c3 fp64 pass)
+#endif
+#ifndef SC_EB_F64_W
+#define SC_EB_F64_W 4     // fp64, weighted graphs (5 spills)
+#endif
+#ifndef SC_EB_F64_MOM
+#define SC_EB_F64_MOM 4   // fp64 with moments (5 and 6 spill: lambda_k 123 / 125 / 136 ms on c3 for 4/5/6)
 #endif
 #ifndef SC_BULK_SLOTS
 #define SC_BULK_SLOTS 0   // gathers landing in shared memory through bulk copies, per warp, beside EB
@@ -726,25 +732,26 @@ template <typename T>
 using KernelFn = void (*)(const int64_t*, const int32_t*, const float*, const T*, const uint16_t*, StepParams, int,
                           int);
 
-template <typename T, int VPR, int EB, bool MOM>
+// EBU / EBW: gathers in flight per lane for unit / weighted graphs (weights take registers)
+template <typename T, int VPR, int EBU, int EBW, bool MOM>
 KernelFn<T> pick_unit(bool unit) {
-  if (unit) return cheb_step_kernel<T, VPR, EB, true, MOM>;
-  return cheb_step_kernel<T, VPR, EB, false, MOM>;
+  if (unit) return cheb_step_kernel<T, VPR, EBU, true, MOM>;
+  return cheb_step_kernel<T, VPR, EBW, false, MOM>;
 }
 
-template <typename T, int EB, bool MOM>
+template <typename T, int EBU, int EBW, bool MOM>
 KernelFn<T> pick_vpr(int vpr, bool unit) {
   switch (vpr) {
-    case 1: return pick_unit<T, 1, EB, MOM>(unit);
-    case 2: return pick_unit<T, 2, EB, MOM>(unit);
-    case 3: return pick_unit<T, 3, EB, MOM>(unit);
-    case 4: return pick_unit<T, 4, EB, MOM>(unit);
-    case 6: return pick_unit<T, 6, EB, MOM>(unit);
-    case 8: return pick_unit<T, 8, EB, MOM>(unit);
-    case 12: return pick_unit<T, 12, EB, MOM>(unit);
-    case 16: return pick_unit<T, 16, EB, MOM>(unit);
-    case 24: return pick_unit<T, 24, EB, MOM>(unit);
-    case 32: return pick_unit<T, 32, EB, MOM>(unit);
+    case 1: return pick_unit<T, 1, EBU, EBW, MOM>(unit);
+    case 2: return pick_unit<T, 2, EBU, EBW, MOM>(unit);
+    case 3: return pick_unit<T, 3, EBU, EBW, MOM>(unit);
+    case 4: return pick_unit<T, 4, EBU, EBW, MOM>(unit);
+    case 6: return pick_unit<T, 6, EBU, EBW, MOM>(unit);
+    case 8: return pick_unit<T, 8, EBU, EBW, MOM>(unit);
+    case 12: return pick_unit<T, 12, EBU, EBW, MOM>(unit);
+    case 16: return pick_unit<T, 16, EBU, EBW, MOM>(unit);
+    case 24: return pick_unit<T, 24, EBU, EBW, MOM>(unit);
+    case 32: return pick_unit<T, 32, EBU, EBW, MOM>(unit);
     default: return nullptr;
   }
 }
@@ -754,14 +761,15 @@ KernelFn<T> pick_kernel(int width, bool unit, bool moments) {
   constexpr int W = Vec<T>::W;
   if (width % W) return nullptr;
   const int vpr = width / W;
-  // 8 (fp32) / 4 (fp64) gathers of 16 bytes in flight per lane: fits the 56-register
-  // budget of 2 x 544-thread CTAs per SM without spills
-  constexpr int EB = sizeof(T) == 4 ? SC_EB_F32 : SC_EB_F64;
+  // SC_EB_* gathers of 16 bytes in flight per lane within the 56-register budget of 2 x
+  // 544-thread CTAs per SM (the 128-byte-row unit-weight kernels the configs use do not spill;
+  // the weighted fp32, moments and odd-width fp64 variants spill a few bytes)
   if (moments) {
-    if constexpr (sizeof(T) == 8) return pick_vpr<T, EB, true>(vpr, unit);
+    if constexpr (sizeof(T) == 8) return pick_vpr<T, SC_EB_F64_MOM, SC_EB_F64_MOM, true>(vpr, unit);
     return nullptr;   // moments are accumulated in fp64 only
   }
-  return pick_vpr<T, EB, false>(vpr, unit);
+  if constexpr (sizeof(T) == 4) return pick_vpr<T, SC_EB_F32, SC_EB_F32, false>(vpr, unit);
+  else return pick_vpr<T, SC_EB_F64, SC_EB_F64_W, false>(vpr, unit);
 }
 
 template <typename T> const T* strength_of(const sc_graph* g);
