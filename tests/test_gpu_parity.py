@@ -400,6 +400,25 @@ def test_kmeans_bit_exact(sc, n, k, d, spread, restarts, max_iter):
     assert inertia == pytest.approx(io, rel=1e-12)
 
 
+def test_kmeans_unaligned_features_same_labels(sc):
+    """Features whose base pointer is not 16-byte aligned (a view one float into its storage)
+    take the 4-byte staging path of the per-point kernels; d % 4 == 0 aligned features the
+    16-byte path: both give the oracle's labels."""
+    n, k, d = 40000, 110, 32      # n*k*d >= 2^27: fp32 screen and Hamerly check on
+    X = _features(n + 3, n, k, d, 0.9)
+    u = np.stack([scinputs.uniforms(13, k, offset=k * r) for r in range(2)])
+    lo, Co, io, ito, ro, _ = kmeans.kmeans(X, k, u, 8)
+    big = torch.zeros(n * d + 1, dtype=torch.float32, device="cuda")
+    big[1:] = torch.from_numpy(X).cuda().reshape(-1)
+    for F in (torch.from_numpy(X).cuda(), big[1:].view(n, d)):
+        assert (F.data_ptr() % 16 == 0) == (F.storage_offset() == 0)
+        lab = torch.empty(n, dtype=torch.int32, device="cuda")
+        C = np.zeros((k, d), dtype=np.float64)
+        inertia, it, best = sc.sc_kmeans(F, n, d, k, 2, 8, 0, u, lab, C)
+        assert np.array_equal(lab.cpu().numpy(), lo)
+        assert np.array_equal(C, Co) and best == ro and it == ito
+
+
 @pytest.mark.parametrize("case", ["k1", "k_eq_n", "d1", "three_distinct_rows"])
 def test_kmeans_edge_cases(sc, case):
     """Degenerate k-means inputs: one cluster, one point per cluster, one dimension, and
