@@ -1289,9 +1289,12 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   const int smem_screen = screen_bytes(screen_nbuf);
   SC_CUDA_TRY(cudaFuncSetAttribute(screen_nbuf == 2 ? assign_screen_kernel<2> : assign_screen_kernel<1>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_screen));
-  // the screen pays off when the exact scan is expensive (env SC_KMEANS_SCREEN=0 disables it)
+  // the screen pays off when the exact scan is expensive (env SC_KMEANS_SCREEN=0 disables it);
+  // threshold measured on the configs[2] stability scan (k-means 0.57 s at 2^27, 0.47 s at 3e7
+  // and 1e7: 10^5 x 48 features, k = 10..30); the Hamerly check follows the same size rule
+  // (0.475 -> 0.466 s)
   const double screen_min = std::getenv("SC_KMEANS_SCREEN_MIN") ? std::atof(std::getenv("SC_KMEANS_SCREEN_MIN"))
-                                                                : 134217728.0;
+                                                                : 3.0e7;
   const bool screen = (double)n * k * d >= screen_min && !(std::getenv("SC_KMEANS_SCREEN") && std::atoi(std::getenv("SC_KMEANS_SCREEN")) == 0);
   const int smem_rows = (int)(sizeof(float) * kSP * (d + 4));   // (row stride d + 4 or d + 1)
   const int smem_d2 = smem_rows + (int)(sizeof(double) * d);
@@ -1303,7 +1306,9 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   // partials), the number of changed labels and the label histogram
   // Hamerly pruning pays off when a full assignment is expensive; small problems (many of
   // them in a stability scan) are launch-bound and take the plain full scan
-  const bool prune = (double)n * k * d >= 134217728.0;
+  const double prune_min = std::getenv("SC_KMEANS_PRUNE_MIN") ? std::atof(std::getenv("SC_KMEANS_PRUNE_MIN"))
+                                                              : 3.0e7;
+  const bool prune = (double)n * k * d >= prune_min;
   // Lloyd assignment of every point, no host synchronisation: labels, exact dmin, the
   // number of changed labels into changed_dev[slot] and the label histogram (device);
   // block partials of the inertia in b_part
