@@ -197,7 +197,8 @@ template <> struct Stream<double> {
 #define SC_EB_F64_W 4     // fp64, weighted graphs (5 spills)
 #endif
 #ifndef SC_EB_F64_MOM
-#define SC_EB_F64_MOM 4   // fp64 with moments (5 and 6 spill: lambda_k 123 / 125 / 136 ms on c3 for 4/5/6)
+#define SC_EB_F64_MOM 5   // fp64 with moments (per-tile warp-reduced partials, no spills: lambda_k on
+                          // c3 126 / 121 / 170 ms for EB 4 / 5 / 6)
 #endif
 #ifndef SC_BULK_SLOTS
 #define SC_BULK_SLOTS 0   // gathers landing in shared memory through bulk copies, per warp, beside EB
@@ -379,7 +380,9 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   T* d_own = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 0) * 32 + lane) * 16);
   T* d_prv = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 1) * 32 + lane) * 16);
   T* d_y = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 2) * 32 + lane) * 16);
-  double m_cc = 0.0, m_nc = 0.0, m_nn = 0.0;
+  // MOMENTS: each tile's contributions are warp-reduced and added to this warp's slots of
+  // `red` in tile order (deterministic), so no accumulator stays live across the gathers
+  if (MOMENTS && lane < 3) red[warp * 3 + lane] = 0.0;
   uint64_t* bbar = bbar_all + warp * (kBulk > 0 ? kBulk : 1);
   unsigned char* bslot = bulk_all + (size_t)warp * kBulk * 512;
   uint32_t bphase = 0;   // bit b: parity of slot b's next completed phase
@@ -401,6 +404,7 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
     const int64_t row = m.r0 + (valid ? ord[rank] : 0);
     int deg = 0;
     int64_t b = 0;
+    double m_cc = 0.0, m_nc = 0.0, m_nn = 0.0;   // (MOMENTS) this tile's contributions
     T acc[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) acc[w] = T(0);
@@ -579,6 +583,19 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
         }
       }
     }
+    if (MOMENTS) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        m_cc += __shfl_xor_sync(FULL, m_cc, o);
+        m_nc += __shfl_xor_sync(FULL, m_nc, o);
+        m_nn += __shfl_xor_sync(FULL, m_nn, o);
+      }
+      if (lane == 0) {
+        red[warp * 3 + 0] += m_cc;
+        red[warp * 3 + 1] += m_nc;
+        red[warp * 3 + 2] += m_nn;
+      }
+    }
   }
 
   if (p.p2p) {
@@ -600,18 +617,7 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   }
 
   if (MOMENTS) {
-    // deterministic CTA reduction over the consumer warps (named barrier 1)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      m_cc += __shfl_xor_sync(FULL, m_cc, o);
-      m_nc += __shfl_xor_sync(FULL, m_nc, o);
-      m_nn += __shfl_xor_sync(FULL, m_nn, o);
-    }
-    if (lane == 0) {
-      red[warp * 3 + 0] = m_cc;
-      red[warp * 3 + 1] = m_nc;
-      red[warp * 3 + 2] = m_nn;
-    }
+    // deterministic CTA reduction over the consumer warps' slots (named barrier 1)
     asm volatile("bar.sync 1, %0;" ::"r"(kNC * 32) : "memory");
     if (threadIdx.x < 3) {
       double sum = 0.0;
