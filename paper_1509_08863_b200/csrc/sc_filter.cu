@@ -190,6 +190,9 @@ template <> struct Stream<double> {
 #define SC_L2_PREFETCH 0  // 1: producer warp prefetches the next tile's gathered rows into L2
                           // (measured 7-10 % slower on configs[3]: profiles/r01_chunk_l2_sweep.md)
 #endif
+#ifndef SC_EB_F32W
+#define SC_EB_F32W 5      // fp32, weighted graphs (6 spills: 168.7 vs 163.1 ms, c3 pattern with weights)
+#endif
 #ifndef SC_EB_F64
 #define SC_EB_F64 5       // gathers in flight per lane (fp64; measured 4/5/6: 230/219/220 ms, c3 fp64 pass)
 #endif
@@ -774,7 +777,7 @@ KernelFn<T> pick_kernel(int width, bool unit, bool moments) {
     if constexpr (sizeof(T) == 8) return pick_vpr<T, SC_EB_F64_MOM, SC_EB_F64_MOM, true>(vpr, unit);
     return nullptr;   // moments are accumulated in fp64 only
   }
-  if constexpr (sizeof(T) == 4) return pick_vpr<T, SC_EB_F32, SC_EB_F32, false>(vpr, unit);
+  if constexpr (sizeof(T) == 4) return pick_vpr<T, SC_EB_F32, SC_EB_F32W, false>(vpr, unit);
   else return pick_vpr<T, SC_EB_F64, SC_EB_F64_W, false>(vpr, unit);
 }
 
