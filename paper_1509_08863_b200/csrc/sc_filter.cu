@@ -186,10 +186,6 @@ template <> struct Stream<double> {
 #ifndef SC_EB_F32
 #define SC_EB_F32 6       // gathers in flight per lane (fp32)
 #endif
-#ifndef SC_L2_PREFETCH
-#define SC_L2_PREFETCH 0  // 1: producer warp prefetches the next tile's gathered rows into L2
-                          // (measured 7-10 % slower on configs[3]: profiles/r01_chunk_l2_sweep.md)
-#endif
 #ifndef SC_EB_F32W
 #define SC_EB_F32W 5      // fp32, weighted graphs (6 spills: 168.7 vs 163.1 ms, c3 pattern with weights)
 #endif
@@ -203,14 +199,7 @@ template <> struct Stream<double> {
 #define SC_EB_F64_MOM 5   // fp64 with moments (per-tile warp-reduced partials, no spills: lambda_k on
                           // c3 126 / 121 / 170 ms for EB 4 / 5 / 6)
 #endif
-#ifndef SC_BULK_SLOTS
-#define SC_BULK_SLOTS 0   // gathers landing in shared memory through bulk copies, per warp, beside EB
-                          // (parity green, measured 1.6-2.7x slower on configs[3]: the bulk-copy
-                          // path is far slower than register gathers for 128-byte rows;
-                          // profiles/r01_chunk_l2_sweep.md)
-#endif
 constexpr int kNC = SC_NC;
-constexpr int kBulk = SC_BULK_SLOTS;
 constexpr int kThreads = (kNC + 1) * 32;   // + one producer warp
 constexpr int kMaxStages = 3;
 
@@ -228,7 +217,7 @@ struct SmemLayout {
   int cap;          // col entries per stage
   int trp;          // row_ptr entries per stage
   int stages;
-  size_t stage_bytes, rp_off, ord_off, col_off, val_off, dense_off, red_off, total, bbar_off = 0, bulk_off = 0;
+  size_t stage_bytes, rp_off, ord_off, col_off, val_off, dense_off, red_off, total;
   __host__ __device__ SmemLayout(int tr, int cap_, bool unit, int nst) {
     cap = cap_;
     stages = nst;
@@ -242,11 +231,6 @@ struct SmemLayout {
     dense_off = 256 + (size_t)stages * stage_bytes;
     red_off = dense_off + (size_t)kNC * 3 * 32 * 16;
     total = red_off + kNC * 3 * sizeof(double);
-    // bulk-copy landing slots (SC_BULK_SLOTS): per consumer warp B slots of 32 x 16 bytes and
-    // one mbarrier per slot
-    bbar_off = (total + 7) & ~(size_t)7;
-    bulk_off = (bbar_off + (size_t)kNC * kBulk * 8 + 127) & ~(size_t)127;
-    if (kBulk) total = bulk_off + (size_t)kNC * kBulk * 512;
   }
 };
 
@@ -276,14 +260,11 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   const int64_t nrows = p.row_end - p.row_begin;
   const int64_t ntiles = (nrows + TR - 1) / TR;
 
-  uint64_t* bbar_all = reinterpret_cast<uint64_t*>(smem + lay.bbar_off);
-  unsigned char* bulk_all = smem + lay.bulk_off;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kNC);
     }
-    for (int b = 0; b < kNC * kBulk; ++b) mbar_init(&bbar_all[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -291,9 +272,6 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   const uint64_t pol_stream = policy_evict_first();
 #if SC_GATHER_HINT
   const uint64_t pol_gather = policy_gather();
-#endif
-#if SC_BULK_SLOTS
-  const uint64_t pol_gather_b = policy_gather();
 #endif
 
   if (warp == kNC) {
@@ -336,31 +314,6 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
             if (!UNIT) bulk_g2s(st + lay.val_off, val + ca, (uint32_t)(ncol * 4), &full[s], pol_stream);
           }
         }
-#if SC_L2_PREFETCH
-        // L2 prefetch of the rows of T_s that tile i-1 will gather (its column segment has
-        // landed in stage (i-1) % S by now; the consumers are still on older tiles): the DRAM
-        // misses of the random gathers are taken by fire-and-forget prefetches that hold no
-        // registers, so the consumers' register window mostly sees L2 hits.
-        if (i >= 1) {
-          const int sp = (i - 1) % S;
-          mbar_wait(&full[sp], ((i - 1) / S) & 1);
-          const TileMeta& mp = meta[sp];
-          if (!mp.overflow) {
-            const unsigned char* stp = stages + (size_t)sp * lay.stage_bytes;
-            const int64_t* rpp = reinterpret_cast<const int64_t*>(stp + lay.rp_off);
-            const int32_t* cip = reinterpret_cast<const int32_t*>(stp + lay.col_off);
-            const int q0 = static_cast<int>(rpp[mp.r0 - mp.rpa] - mp.ca);
-            const int q1 = static_cast<int>(rpp[mp.r1 - mp.rpa] - mp.ca);
-            constexpr int kLines = (VPR * 16 + 127) / 128;
-            for (int q = q0 + lane; q < q1; q += 32) {
-              const char* a = reinterpret_cast<const char*>(p.tcur) +
-                              static_cast<uint64_t>(static_cast<uint32_t>(cip[q])) * (uint64_t)(p.ld_cur * sizeof(T));
-#pragma unroll
-              for (int l = 0; l < kLines; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + l * 128));
-            }
-          }
-        }
-#endif
       }
     }
     // drain: wait until the consumers released every stage still in use
@@ -386,9 +339,6 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   // MOMENTS: each tile's contributions are warp-reduced and added to this warp's slots of
   // `red` in tile order (deterministic), so no accumulator stays live across the gathers
   if (MOMENTS && lane < 3) red[warp * 3 + lane] = 0.0;
-  uint64_t* bbar = bbar_all + warp * (kBulk > 0 ? kBulk : 1);
-  unsigned char* bslot = bulk_all + (size_t)warp * kBulk * 512;
-  uint32_t bphase = 0;   // bit b: parity of slot b's next completed phase
 
   int i = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
@@ -444,72 +394,6 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
           for (int w = 0; w < W; ++w) g[e][w] = T(0);
         }
       };
-#if SC_BULK_SLOTS
-      // window of EB register slots + kBulk shared-memory slots: edge pos goes to slot
-      // pos mod (EB + kBulk); a shared slot is filled by one cp.async.bulk per row (issued by
-      // the row's first lane) completing on the slot's mbarrier -- in flight without registers
-      constexpr int WIN = EB + kBulk;
-      T bw[kBulk];
-      uint32_t armed = 0;
-      auto issue_b = [&](int b, int pos) {
-        const bool ok = pos < deg;
-        const unsigned m = __ballot_sync(FULL, ok && sl == 0);
-        if (m) {
-          if (lane == 0) mbar_arrive_expect_tx(&bbar[b], (uint32_t)(__popc(m) * VPR * 16));
-          __syncwarp();
-          if (ok && sl == 0) {
-            const int k = ci[pos];
-            bulk_g2s(bslot + (size_t)b * 512 + (size_t)sub * VPR * 16,
-                     gbase - c * sizeof(T) + static_cast<uint64_t>(static_cast<uint32_t>(k)) * ldb,
-                     (uint32_t)(VPR * 16), &bbar[b], pol_gather_b);
-          }
-          armed |= 1u << b;
-        } else {
-          armed &= ~(1u << b);
-        }
-        if (!UNIT) bw[b] = ok ? static_cast<T>(wi[pos]) : T(0);
-      };
-      auto consume_b = [&](int b, int pos) {
-        if (armed & (1u << b)) {
-          mbar_wait(&bbar[b], (bphase >> b) & 1u);
-          bphase ^= 1u << b;
-          if (pos < deg) {
-            T v[W];
-            Vec<T>::ld(reinterpret_cast<const T*>(bslot + (size_t)b * 512 + (size_t)lane * 16), v);
-#pragma unroll
-            for (int w = 0; w < W; ++w) {
-              if (UNIT) acc[w] += v[w];
-              else acc[w] = fma(bw[b], v[w], acc[w]);
-            }
-          }
-          __syncwarp();
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // reads before the next bulk write
-        }
-      };
-#pragma unroll
-      for (int e = 0; e < EB; ++e) issue(e, e);
-#pragma unroll
-      for (int b = 0; b < kBulk; ++b) issue_b(b, EB + b);
-      for (int base = 0; base < maxdeg; base += WIN) {
-#pragma unroll
-        for (int e = 0; e < EB; ++e) {
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            if (UNIT) acc[w] += g[e][w];
-            else acc[w] = fma(wv[e], g[e][w], acc[w]);
-          }
-          issue(e, base + WIN + e);
-        }
-#pragma unroll
-        for (int b = 0; b < kBulk; ++b) {
-          consume_b(b, base + EB + b);
-          issue_b(b, base + WIN + EB + b);
-        }
-      }
-      // drain: slots armed by the last round (positions past maxdeg) still complete their phase
-#pragma unroll
-      for (int b = 0; b < kBulk; ++b) consume_b(b, INT_MAX);
-#else
 #pragma unroll
       for (int e = 0; e < EB; ++e) issue(e, e);
       for (int base = 0; base < maxdeg; base += EB) {
@@ -523,7 +407,6 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
           issue(e, base + EB + e);
         }
       }
-#endif
     };
     if (!m.overflow) {
       // column indices (and weights) from the staged shared-memory segment
