@@ -201,7 +201,11 @@ template <> struct Stream<double> {
 #endif
 constexpr int kNC = SC_NC;
 constexpr int kThreads = (kNC + 1) * 32;   // + one producer warp
-constexpr int kMaxStages = 3;
+#ifndef SC_NSTAGES
+#define SC_NSTAGES 3      // CSR ring stages (4: 116.2 vs 115.0-115.6 ms on c3; the header fits 4)
+#endif
+constexpr int kMaxStages = SC_NSTAGES;
+static_assert(kMaxStages <= 4, "barrier + TileMeta header holds at most 4 stages");
 
 struct TileMeta {
   int64_t r0, r1;      // rows [r0, r1)
@@ -674,7 +678,7 @@ template <> const double* strength_of<double>(const sc_graph* g) { return g->str
 // SM).  Tiles whose segment exceeds the capacity read their columns from global
 // memory (correct, slower).
 void stage_plan(int tr, bool unit, int* cap, int* nstages) {
-  const int ns = 3;
+  const int ns = kMaxStages;
   const int per_entry = unit ? 4 : 8;
   const int budget = 100 * 1024 - 256 - kNC * 3 * 32 * 16 - kNC * 3 * 8;
   const int per_stage = budget / ns - (tr + 6) * 8 - tr * 2 - 144;
