@@ -212,7 +212,7 @@ struct TileMeta {
   int64_t rpa;         // first row_ptr index staged (r0 rounded down to even)
   int64_t ca;          // first col index staged (row_ptr[r0] rounded down to a multiple of 4)
   int32_t overflow;    // 1: the tile's col segment did not fit, read from global
-  int32_t pad;
+  int32_t tile;        // tile index (dynamic scheduling); r0 < 0 marks the end
 };
 
 __host__ __device__ constexpr int tile_rows(int vpr) { return kNC * (32 / vpr); }
@@ -282,6 +282,52 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   const uint64_t pol_gather = policy_gather();
 #endif
 
+  if (warp == kNC && p.tile_ctr) {
+    // ------------------------------------------------- producer, dynamic schedule
+    // tiles are taken one at a time from the launch's counter (the 3-stage ring hides the
+    // atomic + bounds + bulk-copy chain); a stage with r0 = -1 tells the consumers to stop
+    int i = 0;
+    for (;; ++i) {
+      const int s = i % S;
+      if (lane == 0) {
+        const int64_t t = atomicAdd(p.tile_ctr, 1u);
+        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+        TileMeta& m = meta[s];
+        if (t >= ntiles) {
+          m.r0 = -1;
+          mbar_arrive(&full[s]);
+        } else {
+          const int64_t r0 = p.row_begin + t * TR;
+          const int64_t r1 = min(r0 + TR, p.row_end);
+          const int64_t e0 = __ldg(row_ptr + r0), e1 = __ldg(row_ptr + r1);
+          const int64_t rpa = r0 & ~int64_t(1);
+          const int64_t nrp = ((r1 + 1 - rpa) + 1) & ~int64_t(1);
+          const int64_t ca = e0 & ~int64_t(3);
+          const int64_t ncol = ((e1 - ca) + 3) & ~int64_t(3);
+          const int overflow = ncol > lay.cap;
+          m.r0 = r0; m.r1 = r1; m.rpa = rpa; m.ca = ca; m.overflow = overflow; m.tile = (int32_t)t;
+          unsigned char* st = stages + (size_t)s * lay.stage_bytes;
+          uint32_t tx = (uint32_t)(nrp * 8) + (uint32_t)(TR * 2);
+          const bool cp_col = !overflow && ncol > 0;
+          if (cp_col) tx += (uint32_t)(ncol * 4 * (UNIT ? 1 : 2));
+          mbar_arrive_expect_tx(&full[s], tx);
+          bulk_g2s(st + lay.rp_off, row_ptr + rpa, (uint32_t)(nrp * 8), &full[s], pol_stream);
+          bulk_g2s(st + lay.ord_off, order + t * TR, (uint32_t)(TR * 2), &full[s], pol_stream);
+          if (cp_col) {
+            bulk_g2s(st + lay.col_off, col + ca, (uint32_t)(ncol * 4), &full[s], pol_stream);
+            if (!UNIT) bulk_g2s(st + lay.val_off, val + ca, (uint32_t)(ncol * 4), &full[s], pol_stream);
+          }
+        }
+        i = t >= ntiles ? -i - 1 : i;   // (encode "done" for the warp)
+      }
+      i = __shfl_sync(FULL, i, 0);
+      if (i < 0) { i = -i - 1; break; }
+    }
+    // drain: wait until the consumers released every real tile's stage still in use
+    if (lane == 0)
+      for (int j = max(0, i - S); j < i; ++j) mbar_wait(&empty[j % S], (j / S) & 1);
+    return;
+  }
   if (warp == kNC) {
     // ------------------------------------------------------------ producer
     int i = 0;
@@ -350,10 +396,15 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   if (MOMENTS && lane < 3) red[warp * 3 + lane] = 0.0;
 
   int i = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+  const bool dyn = p.tile_ctr != nullptr;
+  for (int64_t t = blockIdx.x; dyn || t < ntiles; t += gridDim.x, ++i) {
     const int s = i % S;
     mbar_wait(&full[s], (i / S) & 1);
     const TileMeta m = meta[s];
+    if (dyn) {
+      if (m.r0 < 0) break;   // the producer ran out of tiles
+      t = m.tile;
+    }
     const unsigned char* st = stages + (size_t)s * lay.stage_bytes;
     const int64_t* rps = reinterpret_cast<const int64_t*>(st + lay.rp_off);
 
@@ -629,6 +680,25 @@ size_t persist_bytes() {
 }
 size_t persist_max_window() { return g_persist_max_window; }
 
+// dynamic tile scheduling of the step kernel (env SC_DYN_TILES=0 disables)
+bool dyn_tiles_on() {
+  static const bool v = env_int("SC_DYN_TILES", 1) != 0;
+  return v;
+}
+constexpr int kTileCtrRing = 1024;
+unsigned* next_tile_ctr(const sc_graph* g, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(g->tile_ctr_mu);
+  if (!g->tile_ctr_ring.ptr) {
+    if (g->tile_ctr_ring.ensure(sizeof(unsigned) * kTileCtrRing) != SC_OK) return nullptr;
+    if (cudaMemsetAsync(g->tile_ctr_ring.ptr, 0, sizeof(unsigned) * kTileCtrRing, s) != cudaSuccess) return nullptr;
+  }
+  const int idx = static_cast<int>(g->tile_ctr_seq++ % kTileCtrRing);
+  if (idx == 0 && g->tile_ctr_seq > 1 &&
+      cudaMemsetAsync(g->tile_ctr_ring.ptr, 0, sizeof(unsigned) * kTileCtrRing, s) != cudaSuccess)
+    return nullptr;
+  return g->tile_ctr_ring.as<unsigned>() + idx;
+}
+
 // step launches with programmatic dependent launch (env SC_PDL=0 disables; measured neutral on
 // configs[3]: 115.2 vs 115.3 ms per pass -- a ~290 us launch has little prologue to hide)
 bool pdl_on() {
@@ -740,6 +810,7 @@ int launch_step_impl(const sc_graph* g, const StepParams& p, cudaStream_t s, boo
   const uint16_t* order = tile_order(g, tr, p.row_begin, p.row_end, s);
   if (!order) return fail(SC_ERR_NOMEM, "tile order allocation failed");
   StepParams q = p;
+  q.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
   const size_t persist = persist_bytes();
   if (persist) {
     // experiment (SC_PERSIST_MB): an L2 persisting window over the gathered table T_s

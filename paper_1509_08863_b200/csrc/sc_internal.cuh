@@ -169,6 +169,11 @@ struct sc_graph {
   std::map<std::pair<int, int>, std::vector<int64_t>> resident_plans;
   std::map<std::pair<int, int>, std::unique_ptr<sc::DevBuf>> resident_tiles;
   sc::DevBuf resident_coef;
+  // dynamic tile scheduling of the step kernel: one tile counter per launch from a ring of
+  // kTileCtrRing slots, re-zeroed (stream-ordered memset) each time the ring wraps
+  mutable sc::DevBuf tile_ctr_ring;
+  mutable int64_t tile_ctr_seq = 0;
+  mutable std::mutex tile_ctr_mu;
   int num_sms = 148;
   int device = 0;
 };
@@ -216,6 +221,8 @@ struct StepParams {
   const P2PDev* p2p;
   int p2p_next;
   int64_t p2p_signal;
+  // dynamic tile scheduling (nullptr: static round-robin): tiles are taken from this counter
+  unsigned* tile_ctr;
 };
 
 // launch one fused step for `width` columns starting at the given pointers
