@@ -17,6 +17,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cstdlib>
+
 #include "sc_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -285,6 +287,11 @@ size_t resident_smem(int cap_rows, int cap_nnz, bool unit) {
 
 }  // namespace
 
+static int env_int_r(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 // Plan of the resident path for chunk width w: CTA tile ranges with their largest CSR slice.
 // Returns SC_OK with *ok = false when the graph does not fit (caller uses the streaming path).
 template <typename T>
@@ -315,6 +322,25 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
       if (!coop || grid <= 0) break;
       std::vector<int64_t> tb(grid + 1), rpb(grid + 1);
       for (int b = 0; b <= grid; ++b) tb[b] = ntiles * b / grid;
+      // balance the CTAs' step work (every step waits for the slowest CTA): boundaries where the
+      // cumulative nnz + 2 x rows crosses b / grid of the total (SC_RESIDENT_BALANCE=0: equal
+      // tile counts)
+      if (env_int_r("SC_RESIDENT_BALANCE", 1) && n <= (int64_t)1 << 24) {
+        std::vector<int64_t> rph(n + 1);
+        SC_CUDA_TRY(cudaMemcpy(rph.data(), g->row_ptr.as<int64_t>(), sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+        auto cost = [&](int64_t t) {   // cost of tiles [0, t)
+          const int64_t r = std::min(t * tr, n);
+          return (double)rph[r] + 2.0 * (double)r;
+        };
+        const double total = cost(ntiles);
+        int64_t t = 0;
+        for (int b = 1; b < grid; ++b) {
+          const double target = total * b / grid;
+          while (t < ntiles && cost(t) < target) ++t;
+          tb[b] = std::max<int64_t>(tb[b - 1] + 1, std::min<int64_t>(t, ntiles - (grid - b)));
+        }
+        tb[grid] = ntiles;
+      }
       for (int b = 0; b <= grid; ++b) {
         const int64_t r = std::min(tb[b] * tr, n);
         SC_CUDA_TRY(cudaMemcpy(&rpb[b], g->row_ptr.as<int64_t>() + r, sizeof(int64_t), cudaMemcpyDeviceToHost));
