@@ -12,10 +12,11 @@ Metric (BASELINE.json): filter nnz*R*p/s, nnz = nnz(L) = nnz(W) + N.  ``value``
 is device-timed (CUDA events on the launching stream, barrier + synchronize on
 both sides, max over ranks); ``e2e`` is the same metric through the C ABI with
 pinned HOST buffers (H2D of X and D2H of Y inside the timed region).  The roofline's
-kernel time comes from CUDA events around every launch of the last timed step.
+kernel time comes from CUDA events around every launch of the timed steps.
 
 ``--impl reference`` times the fp64 CPU oracle (the only reference this run
-has) on a bounded sample of the same workload.
+has; oracle/cfilter.c on every host core) on a bounded sample of the same workload:
+all R columns, a bounded number of recurrence steps.
 """
 
 from __future__ import annotations
@@ -167,24 +168,28 @@ def ncu_traffic(workload):
 # ---------------------------------------------------------------------------
 # oracle (CPU) timing -- cpu_baseline and --impl reference
 # ---------------------------------------------------------------------------
-def oracle_sample(g, w, lam_c, lmax, cols=1, order=None, budget_s=20.0):
-    """Time the fp64 oracle filter on `cols` columns and `order` recurrence steps of
-    the same graph (bounded sample); returns (nnz*R*p per second, description)."""
+def oracle_sample(g, w, lam_c, lmax, order=None, budget_s=20.0):
+    """Time the oracle's fp64 filter (oracle/cfilter.c: the definition written out in plain C,
+    the rows of each recurrence step on every host core) on all R columns of the workload for a
+    bounded number of recurrence steps; returns (nnz*R*p per second, seconds, description,
+    threads)."""
     import scinputs
-    from oracle import chebyshev, laplacian
-    L = laplacian.laplacian(g)
-    X = scinputs.gaussian_block(7, g.n, cols).astype(np.float64)
+    from oracle import cfilter, chebyshev
+    X = scinputs.gaussian_block(7, g.n, w.R).astype(np.float64)
+    threads = cfilter.num_threads()
     # calibrate the order so that the sample stays within budget
     t0 = time.perf_counter()
-    chebyshev.lowpass_filter(L, X, lam_c, lmax, 2, w.jackson)
+    cfilter.cheb_filter(g, X, chebyshev.filter_coeffs(lam_c, lmax, 2, w.jackson), lmax)
     per_step = max((time.perf_counter() - t0) / 2.0, 1e-6)
     if order is None:
         order = int(max(2, min(w.order, budget_s / per_step)))
     t0 = time.perf_counter()
-    chebyshev.lowpass_filter(L, X, lam_c, lmax, order, w.jackson)
+    cfilter.cheb_filter(g, X, chebyshev.filter_coeffs(lam_c, lmax, order, w.jackson), lmax)
     dt = time.perf_counter() - t0
     nnz_l = g.nnz + g.n
-    return nnz_l * cols * order / dt, dt, f"oracle fp64 filter, {cols} of {w.R} columns, order {order} of {w.order}"
+    return (nnz_l * w.R * order / dt, dt,
+            f"oracle fp64 filter (oracle/cfilter.c, OpenMP rows), all {w.R} columns, order {order} of {w.order}",
+            threads)
 
 
 def run_reference(args):
@@ -199,7 +204,7 @@ def run_reference(args):
     vals = []
     budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
     for i in range(args.warmup + args.steps):
-        v, dt, desc = oracle_sample(g, w, lam_c, lmax, cols=1, budget_s=budget)
+        v, dt, desc, threads = oracle_sample(g, w, lam_c, lmax, budget_s=budget)
         if i >= args.warmup:
             vals.append((v, dt, desc))
     value = statistics.median(v for v, _, _ in vals)
@@ -208,7 +213,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": base_config(args, g, w, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": vals[0][2]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": vals[0][2]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -338,13 +343,13 @@ def run_ours(args):
     clocks.start()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # per-launch CUDA events (the roofline's kernel time and launch count) ride on the LAST
-    # timed step only: events around all 400 launches of every step cost ~1.3 % of the step
-    # (measured 117.2 vs 115.7 ms on configs[3]); every step launches the same kernels
-    prof_steps = 1
+    # per-launch CUDA events (the roofline's kernel time and the launch count) on every launch
+    # of every timed step: the kernel time is measured over the timed region itself (their own
+    # cost, ~1 % of a configs[3] step, is inside the timed value too)
+    prof_steps = args.steps
 
     def prof_on(i):
-        if i == args.steps - prof_steps and not args.no_prof:
+        if i == 0 and not args.no_prof:
             sc.sc_profile_begin()
 
     if l2_resident:
@@ -418,8 +423,8 @@ def run_ours(args):
                                            "measured random-gather ceiling in profiles/r01_gather_probe.txt",
                          "kernel_share_of_step": (kern_ms / prof_steps / (ms / args.steps)) if ms > 0 else None,
                          "profiled_steps": prof_steps},
-            # launches of the profiled step x timed steps (each step launches the same kernels)
-            "gpu_launches": int(launches) * args.steps // prof_steps,
+            # every kernel of ours launched in the timed region (counted by the library)
+            "gpu_launches": int(launches),
             "clocks": clk,
         }
 
@@ -513,8 +518,8 @@ def run_ours(args):
         G2.close()
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, desc = oracle_sample(g, w, lam_k, lmax, cols=1, budget_s=15.0)
-        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+        v, dt, desc, threads = oracle_sample(g, w, lam_k, lmax, budget_s=15.0)
+        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
                                "seconds": dt}
     if rank == 0:
         print(json.dumps(out), flush=True)

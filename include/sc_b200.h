@@ -249,6 +249,12 @@ int sc_ari(const int32_t* a, const int32_t* b, int64_t n, double* out, void* str
  * optional row normalisation, k-means (restarts).  labels: n int32.
  * info (host, may be NULL): [lambda_max, lambda_k, count_k, inertia,
  * kmeans_iters, best_restart].
+ * The eigencount of step 2 always uses the Jackson-damped polynomial, whatever
+ * `jackson` says: the count ||F X||^2 estimates #{lambda_l <= lambda_c} only if
+ * the polynomial stays in [0, 1] (R5); the undamped truncated series
+ * overshoots (Gibbs) and would bias the count.  `jackson` selects the filter of
+ * step 5 only.  Random draws: Lanczos start (seed ^ 0x1a2b3c4d), probes (stream 2,
+ * seed ^ 0x5e5e5e5e), signals (stream 0, seed), k-means++ uniforms (stream 1, seed).
  */
 int sc_cluster(sc_graph* g, int k, int R, int order, int jackson, int n_probe,
                uint64_t seed, int restarts, int max_iter, int normalize, int32_t* labels,

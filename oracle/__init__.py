@@ -21,6 +21,8 @@ Modules (each function cites the PAPER.md passage it follows):
     ari         -- adjusted Rand index                          (§4.3, §5)
     stability   -- gamma(k), Eq. (11)                           (§4.3)
     pipeline    -- the six-step accelerated algorithm           (§4.1)
+    cfilter     -- chebyshev.cheb_filter written out in plain C, rows of each step on
+                   OpenMP threads (full-size columns, all-core cpu_baseline)   (§2.4, §4.1)
 
 Parity status of every function is recorded in DESIGN.md §"Oracle pins".
 """

@@ -228,6 +228,7 @@ int sc_graph_load(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ro
 }
 
 int sc_graph_free(sc_graph* g) {
+  if (g) sell_release(g);
   delete g;
   return SC_OK;
 }

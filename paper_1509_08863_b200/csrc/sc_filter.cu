@@ -27,133 +27,10 @@
 #include <mutex>
 
 #include "sc_internal.cuh"
+#include "sc_ptx.cuh"
 
 namespace sc {
 namespace {
-
-constexpr unsigned FULL = 0xffffffffu;
-
-template <typename T> struct Vec;
-template <> struct Vec<float> {
-  static constexpr int W = 4;
-  __device__ __forceinline__ static void ldg(const float* p, float (&v)[4]) {
-    float4 t = __ldg(reinterpret_cast<const float4*>(p));
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  }
-  __device__ __forceinline__ static void ld(const float* p, float (&v)[4]) {
-    float4 t = *reinterpret_cast<const float4*>(p);
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  }
-  __device__ __forceinline__ static void st(float* p, const float (&v)[4]) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  }
-};
-template <> struct Vec<double> {
-  static constexpr int W = 2;
-  __device__ __forceinline__ static void ldg(const double* p, double (&v)[2]) {
-    double2 t = __ldg(reinterpret_cast<const double2*>(p));
-    v[0] = t.x; v[1] = t.y;
-  }
-  __device__ __forceinline__ static void ld(const double* p, double (&v)[2]) {
-    double2 t = *reinterpret_cast<const double2*>(p);
-    v[0] = t.x; v[1] = t.y;
-  }
-  __device__ __forceinline__ static void st(double* p, const double (&v)[2]) {
-    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
-  }
-};
-
-// ---------------------------------------------------------------------------
-// PTX helpers: mbarrier + 1-D bulk copy (TMA engine) + L2 cache policies
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-#ifndef SC_GATHER_HINT
-#define SC_GATHER_HINT 0   // L2 policy of the gathers: 0 default (ld.global.nc), 1 evict_last, 2 evict_normal
-#endif
-__device__ __forceinline__ uint64_t policy_gather() {
-  uint64_t pol;
-#if SC_GATHER_HINT == 1
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-#else
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-#endif
-  return pol;
-}
-// 16-byte global -> shared async copy (LDGSTS, bypasses L1) with an L2 policy
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
-               : "memory");
-}
-// global -> shared bulk copy completing on `bar` (bytes and both addresses 16-byte multiples)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-
-// streaming (read-once / write-once) 16-byte accesses with an L2 evict-first policy
-template <typename T> struct Stream;
-template <> struct Stream<float> {
-  __device__ __forceinline__ static void ld(const float* p, float (&v)[4], uint64_t pol) {
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
-                 : "l"(p), "l"(pol));
-  }
-  __device__ __forceinline__ static void ld_hint(const float* p, float (&v)[4], uint64_t pol) {
-    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
-                 : "l"(p), "l"(pol));
-  }
-  __device__ __forceinline__ static void st(float* p, const float (&v)[4], uint64_t pol) {
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v[0]),
-                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "l"(pol)
-                 : "memory");
-  }
-};
-template <> struct Stream<double> {
-  __device__ __forceinline__ static void ld(const double* p, double (&v)[2], uint64_t pol) {
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                 : "=d"(v[0]), "=d"(v[1])
-                 : "l"(p), "l"(pol));
-  }
-  __device__ __forceinline__ static void ld_hint(const double* p, double (&v)[2], uint64_t pol) {
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
-  }
-  __device__ __forceinline__ static void st(double* p, const double (&v)[2], uint64_t pol) {
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v[0]), "d"(v[1]),
-                 "l"(pol)
-                 : "memory");
-  }
-};
 
 // ---------------------------------------------------------------------------
 // The fused step kernel.
@@ -278,6 +155,10 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
   // consumer waits for this whole grid (griddepcontrol.wait) before touching T, Y or the peers
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint64_t pol_stream = policy_evict_first();
+  const unsigned own_c = p.l2pol & 3u, next_c = (p.l2pol >> 2) & 3u, prev_c = (p.l2pol >> 4) & 3u;
+  const uint64_t pol_own = own_c == 0 ? pol_stream : (own_c == 1 ? policy_evict_normal() : policy_evict_last());
+  const uint64_t pol_prev = prev_c == 0 ? pol_stream : policy_evict_normal();
+  const uint64_t pol_next = next_c == 1 ? pol_stream : (next_c == 2 ? policy_evict_last() : policy_evict_normal());
 #if SC_GATHER_HINT
   const uint64_t pol_gather = policy_gather();
 #endif
@@ -290,7 +171,10 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
     for (;; ++i) {
       const int s = i % S;
       if (lane == 0) {
-        const int64_t t = atomicAdd(p.tile_ctr, 1u);
+        const unsigned tv = atomicAdd(p.tile_ctr, 1u);
+        // the launch's last increment resets the slot (reusable without a host memset)
+        if ((int64_t)tv == ntiles + gridDim.x - 1) atomicExch(p.tile_ctr, 0u);
+        const int64_t t = tv;
         if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
         TileMeta& m = meta[s];
         if (t >= ntiles) {
@@ -424,8 +308,8 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
     if (valid) {
       b = rps[row - m.rpa];
       deg = static_cast<int>(rps[row - m.rpa + 1] - b);
-      cp_async16(d_own, tcur + row * p.ld_cur + c, pol_stream);
-      if (tprev) cp_async16(d_prv, tprev + row * p.ld_prev + c, pol_stream);
+      cp_async16(d_own, tcur + row * p.ld_cur + c, pol_own);
+      if (tprev) cp_async16(d_prv, tprev + row * p.ld_prev + c, pol_prev);
       if (p.y_mode == 2) cp_async16(d_y, y + row * p.ld_y + c, pol_stream);
     }
     int maxdeg = deg;   // over the warp's rows (an upper bound of each row's degree)
@@ -501,7 +385,10 @@ cheb_step_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict_
         const T lt = si * own[w] - acc[w];               // (L T_s)[i]
         tn[w] = a * lt + bc * own[w] + bp * prv[w];      // T_{s+1}[i]
       }
-      if (tnext) Vec<T>::st(tnext + row * p.ld_next + c, tn);   // T_{s+1} is gathered next step: normal L2 policy
+      if (tnext) {   // T_{s+1} is gathered next step: normal L2 policy by default
+        if (next_c == 0) Vec<T>::st(tnext + row * p.ld_next + c, tn);
+        else Stream<T>::st(tnext + row * p.ld_next + c, tn, pol_next);
+      }
       if (p.p2p && tnext && row >= p.p2p->row0) {
         // fused halo exchange: the peers that read this row get it straight into their halo
         // (NVLink stores from the epilogue, no pack / send / receive)
@@ -680,6 +567,24 @@ size_t persist_bytes() {
 }
 size_t persist_max_window() { return g_persist_max_window; }
 
+// SC_L2_SETASIDE_MB > 0 (experiment): L2 set-aside for persisting (evict_last) lines, no window
+void setaside_once() {
+  static const bool done = [] {
+    const int mb = env_int("SC_L2_SETASIDE_MB", 0);
+    if (mb > 0) {
+      int dev = 0, maxp = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)mb << 20, (size_t)maxp));
+      size_t got = 0;
+      cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+      std::fprintf(stderr, "[sc] L2 set-aside %zu B (max %d)\n", got, maxp);
+    }
+    return true;
+  }();
+  (void)done;
+}
+
 // dynamic tile scheduling of the step kernel (env SC_DYN_TILES=0 disables)
 bool dyn_tiles_on() {
   static const bool v = env_int("SC_DYN_TILES", 1) != 0;
@@ -691,11 +596,12 @@ unsigned* next_tile_ctr(const sc_graph* g, cudaStream_t s) {
   if (!g->tile_ctr_ring.ptr) {
     if (g->tile_ctr_ring.ensure(sizeof(unsigned) * kTileCtrRing) != SC_OK) return nullptr;
     if (cudaMemsetAsync(g->tile_ctr_ring.ptr, 0, sizeof(unsigned) * kTileCtrRing, s) != cudaSuccess) return nullptr;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return nullptr;   // zeroed before any stream uses it
   }
+  // every slot is reset to 0 by the last tile request of the launch that used it (the step
+  // kernels' producers), so the ring needs no re-zeroing when it wraps; kTileCtrRing
+  // launches in flight at once would be needed to reuse a slot early
   const int idx = static_cast<int>(g->tile_ctr_seq++ % kTileCtrRing);
-  if (idx == 0 && g->tile_ctr_seq > 1 &&
-      cudaMemsetAsync(g->tile_ctr_ring.ptr, 0, sizeof(unsigned) * kTileCtrRing, s) != cudaSuccess)
-    return nullptr;
   return g->tile_ctr_ring.as<unsigned>() + idx;
 }
 
@@ -810,7 +716,11 @@ int launch_step_impl(const sc_graph* g, const StepParams& p, cudaStream_t s, boo
   const uint16_t* order = tile_order(g, tr, p.row_begin, p.row_end, s);
   if (!order) return fail(SC_ERR_NOMEM, "tile order allocation failed");
   StepParams q = p;
-  q.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
+  // moments: static round-robin tiles, so each CTA's partial sums cover the same tiles in the
+  // same order on every run (deterministic moments -> deterministic lambda_k)
+  q.tile_ctr = (dyn_tiles_on() && !moments) ? next_tile_ctr(g, s) : nullptr;
+  q.l2pol = static_cast<unsigned>(env_int("SC_L2POL", 0));
+  setaside_once();
   const size_t persist = persist_bytes();
   if (persist) {
     // experiment (SC_PERSIST_MB): an L2 persisting window over the gathered table T_s
@@ -1021,8 +931,9 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
   const std::vector<int> chunks = chunk_plan<T>(Rp, g->n_cols);
   int cwmax = 0;
   for (int w : chunks) cwmax = std::max(cwmax, w);
-  SC_TRY(g->ws_a.ensure((size_t)g->n_cols * cwmax * sizeof(T)));
-  SC_TRY(g->ws_b.ensure((size_t)g->n_cols * cwmax * sizeof(T)));
+  // + one row: the all-zero row n_cols that the SELL padding gathers
+  SC_TRY(g->ws_a.ensure((size_t)(g->n_cols + 1) * cwmax * sizeof(T)));
+  SC_TRY(g->ws_b.ensure((size_t)(g->n_cols + 1) * cwmax * sizeof(T)));
 
   int col0 = 0;
   for (int w : chunks) {
@@ -1037,6 +948,64 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
         col0 += w;
         continue;
       }
+    }
+    bool use_sell = false;
+    if (sell_enabled()) SC_TRY(sell_usable<T>(g, w, 0, n, s, &use_sell));
+    if (use_sell) {
+      // SELL path: T_0 = the X chunk copied into bufs[0] (row stride w), zero row n_cols in
+      // both buffers (the sentinel of the padded slices)
+      SC_CUDA_TRY(cudaMemsetAsync(bufs[0] + (size_t)g->n_cols * w, 0, sizeof(T) * w, s));
+      SC_CUDA_TRY(cudaMemsetAsync(bufs[1] + (size_t)g->n_cols * w, 0, sizeof(T) * w, s));
+      copy_cols_kernel<T><<<g->num_sms * 8, 256, 0, s>>>(Xc, Rp, bufs[0], w, n, w);
+      SC_CUDA_TRY(cudaGetLastError());
+      if (g_prof.on) g_prof.launches += 1;
+      int added = -1;
+      for (int st = 0; st < order; ++st) {
+        StepParams p{};
+        p.row_begin = 0;
+        p.row_end = n;
+        p.width = w;
+        p.total_width = Rp;
+        p.tcur = bufs[st & 1];
+        p.ld_cur = w;
+        p.tprev = st == 0 ? nullptr : (const void*)bufs[(st - 1) & 1];
+        p.ld_prev = w;
+        const bool last = st == order - 1;
+        p.tnext = last ? nullptr : (void*)bufs[(st + 1) & 1];
+        p.ld_next = w;
+        p.a = (st == 0 ? 2.0 : 4.0) / lambda_max;
+        p.b_cur = st == 0 ? -1.0 : -2.0;
+        p.b_prev = st == 0 ? 0.0 : -1.0;
+        p.y = Yc;
+        p.ld_y = Rp;
+        const int pending = (st + 1) - added;
+        if (last || pending == 3) {
+          p.cy_prev = (st >= 1 && added < st - 1) ? d[st - 1] : 0.0;
+          p.cy_cur = (added < st) ? d[st] : 0.0;
+          p.cy_next = d[st + 1];
+          p.y_mode = added == -1 ? 1 : 2;
+          added = st + 1;
+        }
+        p.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
+        p.l2pol = static_cast<unsigned>(env_int("SC_L2POL", 0));
+        cudaEvent_t e0 = nullptr;
+        if (g_prof.on) {
+          e0 = g_prof.get();
+          cudaEventRecord(e0, s);
+        }
+        double ab = 0.0;
+        SC_TRY(launch_sell_step<T>(g, p, s, g_prof.on ? &ab : nullptr));
+        if (g_prof.on) {
+          cudaEvent_t e1 = g_prof.get();
+          cudaEventRecord(e1, s);
+          g_prof.ev.emplace_back(e0, e1);
+          g_prof.launches += 1;
+          g_prof.step_launches += 1;
+          g_prof.algo_bytes += ab;
+        }
+      }
+      col0 += w;
+      continue;
     }
     int added = -1;
     for (int st = 0; st < order; ++st) {

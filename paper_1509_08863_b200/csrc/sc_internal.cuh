@@ -170,7 +170,7 @@ struct sc_graph {
   std::map<std::pair<int, int>, std::unique_ptr<sc::DevBuf>> resident_tiles;
   sc::DevBuf resident_coef;
   // dynamic tile scheduling of the step kernel: one tile counter per launch from a ring of
-  // kTileCtrRing slots, re-zeroed (stream-ordered memset) each time the ring wraps
+  // kTileCtrRing slots, zeroed once; the last tile request of a launch resets its slot
   mutable sc::DevBuf tile_ctr_ring;
   mutable int64_t tile_ctr_seq = 0;
   mutable std::mutex tile_ctr_mu;
@@ -223,11 +223,25 @@ struct StepParams {
   int64_t p2p_signal;
   // dynamic tile scheduling (nullptr: static round-robin): tiles are taken from this counter
   unsigned* tile_ctr;
+  // L2 eviction policies of the dense streams (experiment knob SC_L2POL, 0 = default):
+  // bits 0-1 own row T_s[i] (0 evict_first, 1 evict_normal, 2 evict_last),
+  // bits 2-3 T_{s+1} store (0 no hint, 1 evict_first, 2 evict_last, 3 evict_normal),
+  // bits 4-5 T_{s-1} row (0 evict_first, 1 evict_normal)
+  unsigned l2pol;
 };
 
 // launch one fused step for `width` columns starting at the given pointers
 template <typename T>
 int launch_step(const sc_graph* g, const StepParams& p, cudaStream_t s);
+
+// one fused step over the sliced padded CSR (sc_sell.cu); T_s needs a zero row at n_cols.
+// *algo_bytes (optional): the step's algorithmic bytes
+template <typename T>
+int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, double* algo_bytes);
+bool sell_enabled();                       // env SC_SELL (default 1)
+template <typename T>
+int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end, cudaStream_t s, bool* ok);
+void sell_release(const sc_graph* g);      // drop the graph's cached SELL plans
 
 // degree-sorted row order of every tile of tr rows over [row_begin, row_end) (cached on g)
 const uint16_t* tile_order(const sc_graph* g, int tr, int64_t row_begin, int64_t row_end, cudaStream_t s);

@@ -316,8 +316,18 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, g->device);
     (void)0;
+    // a graph whose CSR cannot fit the aggregate shared memory at one CTA per SM is never
+    // resident: decide that before touching row_ptr (no device->host copy for c3 / c4)
+    const size_t need = (size_t)g->nnz * (g->unit_weights ? 4 : 8) + (size_t)n * 6;
+    std::vector<int64_t> rph;   // row_ptr on the host, copied once per plan
+    if (coop && need <= (size_t)g->num_sms * kRSmemMax) {
+      rph.resize(n + 1);
+      SC_CUDA_TRY(cudaMemcpyAsync(rph.data(), g->row_ptr.as<int64_t>(), sizeof(int64_t) * (n + 1),
+                                  cudaMemcpyDeviceToHost, s));
+      SC_CUDA_TRY(cudaStreamSynchronize(s));
+    }
     // two CTAs per SM when their slices fit (more warps to hide gather latency), else one
-    for (int per_sm = 2; per_sm >= 1 && !plan[0]; --per_sm) {
+    for (int per_sm = 2; per_sm >= 1 && !plan[0] && !rph.empty(); --per_sm) {
       const int grid = (int)std::min<int64_t>((int64_t)g->num_sms * per_sm, ntiles);
       if (!coop || grid <= 0) break;
       std::vector<int64_t> tb(grid + 1), rpb(grid + 1);
@@ -325,9 +335,7 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
       // balance the CTAs' step work (every step waits for the slowest CTA): boundaries where the
       // cumulative nnz + 2 x rows crosses b / grid of the total (SC_RESIDENT_BALANCE=0: equal
       // tile counts)
-      if (env_int_r("SC_RESIDENT_BALANCE", 1) && n <= (int64_t)1 << 24) {
-        std::vector<int64_t> rph(n + 1);
-        SC_CUDA_TRY(cudaMemcpy(rph.data(), g->row_ptr.as<int64_t>(), sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+      if (env_int_r("SC_RESIDENT_BALANCE", 1)) {
         auto cost = [&](int64_t t) {   // cost of tiles [0, t)
           const int64_t r = std::min(t * tr, n);
           return (double)rph[r] + 2.0 * (double)r;
@@ -341,10 +349,7 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
         }
         tb[grid] = ntiles;
       }
-      for (int b = 0; b <= grid; ++b) {
-        const int64_t r = std::min(tb[b] * tr, n);
-        SC_CUDA_TRY(cudaMemcpy(&rpb[b], g->row_ptr.as<int64_t>() + r, sizeof(int64_t), cudaMemcpyDeviceToHost));
-      }
+      for (int b = 0; b <= grid; ++b) rpb[b] = rph[std::min(tb[b] * tr, n)];
       int64_t cap_rows = 0, cap_nnz = 0;
       for (int b = 0; b < grid; ++b) {
         cap_rows = std::max<int64_t>(cap_rows, (tb[b + 1] - tb[b]) * tr);

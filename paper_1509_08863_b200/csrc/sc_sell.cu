@@ -1,0 +1,700 @@
+// Fused Chebyshev recurrence step over a sliced, padded copy of the CSR (SELL layout).
+//
+// PAPER.md §2.4 Eq. (3) (lines 135-147) and §4.1 step 5 Eq. (10) (line 321): the filter is
+// p sparse products with L = S - W, run as the Chebyshev three-term recurrence
+// (R1).  One launch = one step over one column chunk:
+//     T_{s+1}[i] = a (s_i T_s[i] - sum_k W_ik T_s[k]) + b_cur T_s[i] + b_prev T_{s-1}[i]
+//     Y[i]      (=|+=) cy_prev T_{s-1}[i] + cy_cur T_s[i] + cy_next T_{s+1}[i]
+// (same arithmetic as cheb_step_kernel in sc_filter.cu, which stays for the moments and
+// row-partitioned paths).
+//
+// Why a second layout.  cheb_step_kernel walks the plain CSR: every gathered 16-byte
+// vector costs ~19 SASS instructions per lane (bounds tests per window slot, zero fills
+// for lanes whose row ended, one index load per edge, four scalar adds), and on configs[3]
+// the launch is issue-bound (ncu: issue active 74 %, 190 M warp instructions per launch).
+// Here each tile's rows are cut into slices of RPW rows (the rows one warp processes
+// together, already degree-sorted by tile_order), every row of a slice is padded to the
+// slice's longest row rounded up to 4 with a sentinel column index that points at an
+// all-zero row appended to the gathered block (row n_cols), and the indices are stored
+// 4-edge-chunk-interleaved so one 16-byte shared-memory load gives a lane the next four
+// column indices of its row without bank conflicts:
+//     slice entry (row r of the slice, edge e) at  off + (e / 4) * 4 * RPW + 4 r + e % 4.
+// The gather loop then has no per-edge predicate, no zero fill and a warp-uniform trip
+// count; each gathered vector is one IMAD.WIDE + one LDG.E.128 + two packed FADD2
+// (add.rn.f32x2), i.e. ~5 instructions per edge per lane.  Adding the padding's zero
+// rows changes nothing (x + 0 = x), so the per-element sums are the CSR-order sums of
+// cheb_step_kernel exactly.
+//
+// Build (once per graph and tile shape, cached on the handle): sell_len_kernel (padded
+// slice lengths), a host prefix over tiles, sell_fill_kernel (slice metadata + entries).
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "sc_internal.cuh"
+#include "sc_ptx.cuh"
+
+namespace sc {
+namespace {
+
+#ifndef SC_SELL_NC
+#define SC_SELL_NC 16       // consumer warps per CTA (= slices per tile)
+#endif
+#ifndef SC_SELL_MIN_CTAS
+#define SC_SELL_MIN_CTAS 2  // resident CTAs per SM the register budget is sized for
+#endif
+#ifndef SC_SELL_NB
+#define SC_SELL_NB 1        // 4-edge batches in flight per lane (configs[3], 32-column chunks:
+#endif                      // 1 -> 97.1 ms per pass, 2 -> 107.1 ms; profiles/r02_sell.md)
+#ifndef SC_SELL_NB_W
+#define SC_SELL_NB_W 1      // weighted graphs
+#endif
+#ifndef SC_SELL_NB_F64
+#define SC_SELL_NB_F64 1    // fp64 (configs[3], 16-double chunks: 1 -> 198.5 ms, 2 -> 219.6 ms)
+#endif
+#ifndef SC_SELL_STAGES
+#define SC_SELL_STAGES 3
+#endif
+#ifndef SC_SELL_GATHER_L1
+#define SC_SELL_GATHER_L1 0   // gathers: 0 ld.global.nc, 1 ld.global.nc.L1::no_allocate, 2 ld.global.cg
+#endif
+#ifndef SC_SELL_SMEM_KB
+#define SC_SELL_SMEM_KB 113   // most shared memory per CTA (2 CTAs per SM); a plan takes only
+#endif                        // what its largest tile needs, the rest of the SM's 228 KB is L1
+#if SC_SELL_GATHER_L1 == 1
+#define SC_GLD "ld.global.nc.L1::no_allocate"
+#elif SC_SELL_GATHER_L1 == 2
+#define SC_GLD "ld.global.cg"
+#else
+#define SC_GLD "ld.global.nc"
+#endif
+constexpr int kNC = SC_SELL_NC;
+constexpr int kThreads = (kNC + 1) * 32;
+constexpr int kStages = SC_SELL_STAGES;
+static_assert(kStages <= 4, "header holds at most 4 stages");
+
+struct SellTileMeta {
+  int64_t r0, r1;     // rows [r0, r1); r0 < 0: no more tiles
+  int64_t e0;         // first SELL entry of the tile
+  int32_t overflow;   // 1: the tile's entries did not fit the stage, read them from global
+  int32_t tile;
+};
+
+__host__ __device__ constexpr int sell_tile_rows(int vpr) { return kNC * (32 / vpr); }
+
+struct SellLayout {
+  int cap;   // SELL entries per stage
+  size_t meta_off, ord_off, idx_off, val_off, stage_bytes, dense_off, total;
+  __host__ __device__ SellLayout(int tr, int cap_, bool unit) {
+    cap = cap_;
+    meta_off = 0;
+    ord_off = (size_t)kNC * 8;
+    idx_off = ord_off + (((size_t)tr * 2 + 15) & ~(size_t)15);
+    val_off = idx_off + (size_t)cap * 4;
+    stage_bytes = val_off + (unit ? 0 : (size_t)cap * 4);
+    stage_bytes = (stage_bytes + 127) & ~(size_t)127;
+    dense_off = 256 + (size_t)kStages * stage_bytes;
+    total = dense_off + (size_t)kNC * 3 * 32 * 16;
+  }
+};
+
+struct SellDev {
+  const int64_t* tile_ptr;   // [ntiles + 1] first entry of each tile (multiple of 4)
+  const int2* meta;          // [ntiles * kNC] {offset in the tile, padded length} per slice
+  const int32_t* idx;        // column indices (sentinel n_cols = the zero row)
+  const float* val;          // weights (0 on padding), nullptr for unit weights
+  const uint16_t* order;     // [ntiles * tr] degree-sorted row order inside each tile
+};
+
+// 16-byte gathers as two packed fp32 pairs (for add.rn.f32x2)
+__device__ __forceinline__ void ldg_pair2(const void* p, uint64_t& a, uint64_t& b) {
+  asm volatile(SC_GLD ".v2.b64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+__device__ __forceinline__ void add_f32x2(uint64_t& acc, uint64_t v) {
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(v));
+}
+__device__ __forceinline__ void ldg_d2(const void* p, double& a, double& b) {
+  asm volatile(SC_GLD ".v2.f64 {%0,%1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+}
+__device__ __forceinline__ void ldg_f4(const void* p, float& a, float& b, float& c, float& d) {
+  asm volatile(SC_GLD ".v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "l"(p));
+}
+
+// Sum of the gathered rows of one lane's row: acc[w] += T_s[k][c + w] (x weight), over the
+// padded slice row, NB 4-edge batches in flight.  `ci` / `cw`: this lane's first 4-index
+// chunk (chunk b at ci + b * 4 * RPW).  Warp-uniform trip count nb = padded length / 4.
+// Loads are unconditional (a conditional load would keep the slot's previous value live
+// across it); a lane without a row passes ldb = 0, so its loads all hit one L1 line.
+template <typename T, int RPW, int NB, bool UNIT> struct Gather;
+
+template <int RPW, int NB> struct Gather<float, RPW, NB, true> {
+  static __device__ __forceinline__ void run(const int32_t* __restrict__ ci, const float* __restrict__,
+                                             int nb, const char* gbase, uint32_t ldb, float (&acc)[4]) {
+    constexpr int CS = 4 * RPW;
+    uint64_t a0 = 0, a1 = 0;
+    uint64_t g[NB][4][2];
+    auto issue = [&](int slot, int b) {
+      const int4 k = *reinterpret_cast<const int4*>(ci + b * CS);
+      {
+        ldg_pair2(gbase + (uint64_t)(uint32_t)k.x * ldb, g[slot][0][0], g[slot][0][1]);
+        ldg_pair2(gbase + (uint64_t)(uint32_t)k.y * ldb, g[slot][1][0], g[slot][1][1]);
+        ldg_pair2(gbase + (uint64_t)(uint32_t)k.z * ldb, g[slot][2][0], g[slot][2][1]);
+        ldg_pair2(gbase + (uint64_t)(uint32_t)k.w * ldb, g[slot][3][0], g[slot][3][1]);
+      }
+    };
+#pragma unroll
+    for (int s = 0; s < NB; ++s)
+      if (s < nb) issue(s, s);
+    for (int b0 = 0; b0 < nb; b0 += NB) {
+#pragma unroll
+      for (int s = 0; s < NB; ++s) {
+        if (b0 + s < nb) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            add_f32x2(a0, g[s][e][0]);
+            add_f32x2(a1, g[s][e][1]);
+          }
+          if (b0 + s + NB < nb) issue(s, b0 + s + NB);
+        }
+      }
+    }
+    acc[0] = __uint_as_float(static_cast<uint32_t>(a0));
+    acc[1] = __uint_as_float(static_cast<uint32_t>(a0 >> 32));
+    acc[2] = __uint_as_float(static_cast<uint32_t>(a1));
+    acc[3] = __uint_as_float(static_cast<uint32_t>(a1 >> 32));
+  }
+};
+
+template <int RPW, int NB> struct Gather<float, RPW, NB, false> {
+  static __device__ __forceinline__ void run(const int32_t* __restrict__ ci, const float* __restrict__ cw,
+                                             int nb, const char* gbase, uint32_t ldb, float (&acc)[4]) {
+    constexpr int CS = 4 * RPW;
+    float g[NB][4][4];
+    acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+    auto issue = [&](int slot, int b) {
+      const int4 k = *reinterpret_cast<const int4*>(ci + b * CS);
+      {
+        ldg_f4(gbase + (uint64_t)(uint32_t)k.x * ldb, g[slot][0][0], g[slot][0][1], g[slot][0][2], g[slot][0][3]);
+        ldg_f4(gbase + (uint64_t)(uint32_t)k.y * ldb, g[slot][1][0], g[slot][1][1], g[slot][1][2], g[slot][1][3]);
+        ldg_f4(gbase + (uint64_t)(uint32_t)k.z * ldb, g[slot][2][0], g[slot][2][1], g[slot][2][2], g[slot][2][3]);
+        ldg_f4(gbase + (uint64_t)(uint32_t)k.w * ldb, g[slot][3][0], g[slot][3][1], g[slot][3][2], g[slot][3][3]);
+      }
+    };
+#pragma unroll
+    for (int s = 0; s < NB; ++s)
+      if (s < nb) issue(s, s);
+    for (int b0 = 0; b0 < nb; b0 += NB) {
+#pragma unroll
+      for (int s = 0; s < NB; ++s) {
+        if (b0 + s < nb) {
+          // weights read from the staged segment when consumed (no registers held)
+          const float4 wv = *reinterpret_cast<const float4*>(cw + (b0 + s) * CS);
+          const float w4[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fmaf(w4[e], g[s][e][q], acc[q]);
+          if (b0 + s + NB < nb) issue(s, b0 + s + NB);
+        }
+      }
+    }
+  }
+};
+
+template <int RPW, int NB, bool UNIT> struct Gather<double, RPW, NB, UNIT> {
+  static __device__ __forceinline__ void run(const int32_t* __restrict__ ci, const float* __restrict__ cw,
+                                             int nb, const char* gbase, uint32_t ldb, double (&acc)[2]) {
+    constexpr int CS = 4 * RPW;
+    double g[NB][4][2];
+    acc[0] = acc[1] = 0.0;
+    auto issue = [&](int slot, int b) {
+      const int4 k = *reinterpret_cast<const int4*>(ci + b * CS);
+      {
+        ldg_d2(gbase + (uint64_t)(uint32_t)k.x * ldb, g[slot][0][0], g[slot][0][1]);
+        ldg_d2(gbase + (uint64_t)(uint32_t)k.y * ldb, g[slot][1][0], g[slot][1][1]);
+        ldg_d2(gbase + (uint64_t)(uint32_t)k.z * ldb, g[slot][2][0], g[slot][2][1]);
+        ldg_d2(gbase + (uint64_t)(uint32_t)k.w * ldb, g[slot][3][0], g[slot][3][1]);
+      }
+    };
+#pragma unroll
+    for (int s = 0; s < NB; ++s)
+      if (s < nb) issue(s, s);
+    for (int b0 = 0; b0 < nb; b0 += NB) {
+#pragma unroll
+      for (int s = 0; s < NB; ++s) {
+        if (b0 + s < nb) {
+          if (UNIT) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              acc[0] += g[s][e][0];
+              acc[1] += g[s][e][1];
+            }
+          } else {
+            const float4 wv = *reinterpret_cast<const float4*>(cw + (b0 + s) * CS);
+            const double w4[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              acc[0] = fma(w4[e], g[s][e][0], acc[0]);
+              acc[1] = fma(w4[e], g[s][e][1], acc[1]);
+            }
+          }
+          if (b0 + s + NB < nb) issue(s, b0 + s + NB);
+        }
+      }
+    }
+  }
+};
+
+template <typename T, int VPR, int NB, bool UNIT>
+__global__ void __launch_bounds__(kThreads, SC_SELL_MIN_CTAS)
+cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int cap) {
+  constexpr int W = Vec<T>::W;
+  constexpr int SW = VPR;          // lanes per row (one 16-byte vector each)
+  constexpr int RPW = 32 / SW;     // rows per warp = rows per slice
+  constexpr int TR = sell_tile_rows(VPR);
+  constexpr int S = kStages;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  const SellLayout lay(TR, cap, UNIT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 4;
+  SellTileMeta* meta = reinterpret_cast<SellTileMeta*>(smem + 64);
+  unsigned char* stages = smem + 256;
+  unsigned char* dense = smem + lay.dense_off;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nrows = p.row_end - p.row_begin;
+  const int64_t ntiles = (nrows + TR - 1) / TR;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == kNC) {
+    // ------------------------------------------------------------- producer
+    // tiles from the launch's counter (dynamic) or round-robin; a stage with r0 = -1 stops
+    // the consumers.  The producer that makes the counter's last increment of the launch
+    // (value ntiles + gridDim.x - 1) resets it to 0, so a counter slot is reusable by a
+    // later launch (or a CUDA graph replay) without a host-side memset.
+    int i = 0;
+    if (lane == 0) {
+      for (;; ++i) {
+        const int s = i % S;
+        int64_t t;
+        if (p.tile_ctr) {
+          const unsigned v = atomicAdd(p.tile_ctr, 1u);
+          if ((int64_t)v == ntiles + gridDim.x - 1) atomicExch(p.tile_ctr, 0u);
+          t = v;
+        } else {
+          t = blockIdx.x + (int64_t)i * gridDim.x;
+        }
+        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+        SellTileMeta& m = meta[s];
+        if (t >= ntiles) {
+          m.r0 = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        const int64_t r0 = p.row_begin + t * TR;
+        const int64_t r1 = min(r0 + TR, p.row_end);
+        const int64_t e0 = __ldg(sd.tile_ptr + t), e1 = __ldg(sd.tile_ptr + t + 1);
+        const int64_t ncol = e1 - e0;
+        const int overflow = ncol > lay.cap;
+        m.r0 = r0; m.r1 = r1; m.e0 = e0; m.overflow = overflow; m.tile = (int32_t)t;
+        unsigned char* st = stages + (size_t)s * lay.stage_bytes;
+        uint32_t tx = (uint32_t)(kNC * 8) + (uint32_t)(TR * 2);
+        const bool cp_col = !overflow && ncol > 0;
+        if (cp_col) tx += (uint32_t)(ncol * 4 * (UNIT ? 1 : 2));
+        mbar_arrive_expect_tx(&full[s], tx);
+        const uint64_t pol_stream = policy_evict_first();
+        bulk_g2s(st + lay.meta_off, sd.meta + t * kNC, (uint32_t)(kNC * 8), &full[s], pol_stream);
+        bulk_g2s(st + lay.ord_off, sd.order + t * TR, (uint32_t)(TR * 2), &full[s], pol_stream);
+        if (cp_col) {
+          bulk_g2s(st + lay.idx_off, sd.idx + e0, (uint32_t)(ncol * 4), &full[s], pol_stream);
+          if (!UNIT) bulk_g2s(st + lay.val_off, sd.val + e0, (uint32_t)(ncol * 4), &full[s], pol_stream);
+        }
+      }
+      // drain: wait until the consumers released every real tile's stage still in use
+      for (int j = max(0, i - S); j < i; ++j) mbar_wait(&empty[j % S], (j / S) & 1);
+    }
+    __syncwarp();
+    return;
+  }
+
+  // --------------------------------------------------------------- consumers
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous step has completed
+  const int sub = lane / SW;
+  const int sl = lane % SW;
+  const int c = sl * W;
+  const T* tprev = static_cast<const T*>(p.tprev);   // may alias tnext (same row, read before write)
+  const T* __restrict__ tcur = static_cast<const T*>(p.tcur);
+  T* tnext = static_cast<T*>(p.tnext);
+  T* y = static_cast<T*>(p.y);
+  const char* gbase = reinterpret_cast<const char*>(tcur + c);
+  const uint32_t ldb = static_cast<uint32_t>(p.ld_cur * sizeof(T));
+  T* d_own = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 0) * 32 + lane) * 16);
+  T* d_prv = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 1) * 32 + lane) * 16);
+  T* d_y = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 2) * 32 + lane) * 16);
+
+  for (int i = 0;; ++i) {
+    const int s = i % S;
+    mbar_wait(&full[s], (i / S) & 1);
+    const SellTileMeta m = meta[s];
+    if (m.r0 < 0) break;
+    const int64_t t = m.tile;
+    const unsigned char* st = stages + (size_t)s * lay.stage_bytes;
+    // this warp's slice: one block of RPW consecutive degree ranks, the block index rotating
+    // with the tile so every warp sees every degree class
+    const int j = (warp + static_cast<int>(t % kNC)) % kNC;
+    const int2 mj = reinterpret_cast<const int2*>(st + lay.meta_off)[j];
+    const uint16_t* ord = reinterpret_cast<const uint16_t*>(st + lay.ord_off);
+    const int rank = j * RPW + sub;
+    const bool valid = sub < RPW && rank < static_cast<int>(m.r1 - m.r0);
+    const int32_t row = static_cast<int32_t>(m.r0) + (valid ? ord[rank] : 0);   // rows < 2^31
+    if (valid) {
+      // own row, T_{s-1} and Y rows land in shared memory while the gathers run; streaming
+      // operands carry an L2 evict-first policy so the gathered block T_s stays in L2
+      const uint64_t pol = policy_evict_first();
+      cp_async16(d_own, tcur + (int64_t)row * p.ld_cur + c, pol);
+      if (tprev) cp_async16(d_prv, tprev + (int64_t)row * p.ld_prev + c, pol);
+      if (p.y_mode == 2) cp_async16(d_y, y + (int64_t)row * p.ld_y + c, pol);
+    }
+    const int lsub = sub < RPW ? sub : 0;
+    T acc[W];
+    {
+      // every tile fits a stage (launch_sell_step checks the plan's largest tile)
+      const int32_t* ci = reinterpret_cast<const int32_t*>(st + lay.idx_off) + mj.x + 4 * lsub;
+      const float* cw = reinterpret_cast<const float*>(st + lay.val_off) + mj.x + 4 * lsub;
+      Gather<T, RPW, NB, UNIT>::run(ci, cw, mj.y >> 2, gbase, valid ? ldb : 0u, acc);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+
+    if (valid) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      T own[W], prv[W], yv[W];
+      Vec<T>::ld(d_own, own);
+      if (tprev) Vec<T>::ld(d_prv, prv);
+      else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) prv[w] = T(0);
+      }
+      if (p.y_mode == 2) Vec<T>::ld(d_y, yv);
+      else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) yv[w] = T(0);
+      }
+      const T si = strength[row];
+      const T a = static_cast<T>(p.a), bc = static_cast<T>(p.b_cur), bp = static_cast<T>(p.b_prev);
+      T tn[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const T lt = si * own[w] - acc[w];               // (L T_s)[i]
+        tn[w] = a * lt + bc * own[w] + bp * prv[w];      // T_{s+1}[i]
+      }
+      if (tnext) Vec<T>::st(tnext + (int64_t)row * p.ld_next + c, tn);   // gathered next step: normal L2 policy
+      if (p.y_mode) {
+        const T cyp = static_cast<T>(p.cy_prev), cyc = static_cast<T>(p.cy_cur), cyn = static_cast<T>(p.cy_next);
+#pragma unroll
+        for (int w = 0; w < W; ++w) yv[w] += cyp * prv[w] + cyc * own[w] + cyn * tn[w];
+        Stream<T>::st(y + (int64_t)row * p.ld_y + c, yv, policy_evict_first());
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SELL build
+// ---------------------------------------------------------------------------
+// padded length of every slice (max degree of its rows rounded up to 4) and entries per tile
+__global__ void sell_len_kernel(const int64_t* __restrict__ row_ptr, int64_t row_begin, int64_t row_end, int tr,
+                                int rpw, const uint16_t* __restrict__ order, int32_t* __restrict__ slice_len,
+                                int64_t* __restrict__ tile_entries) {
+  const int64_t t = blockIdx.x;
+  const int64_t r0 = row_begin + t * tr;
+  const int cnt = static_cast<int>(min((int64_t)tr, row_end - r0));
+  __shared__ int len[64];
+  for (int j = threadIdx.x; j < kNC; j += blockDim.x) {
+    int maxd = 0;
+    for (int q = 0; q < rpw; ++q) {
+      const int rank = j * rpw + q;
+      if (rank < cnt) {
+        const int64_t row = r0 + order[t * tr + rank];
+        maxd = max(maxd, static_cast<int>(row_ptr[row + 1] - row_ptr[row]));
+      }
+    }
+    len[j] = (maxd + 3) & ~3;
+    slice_len[t * kNC + j] = len[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t tot = 0;
+    for (int j = 0; j < kNC; ++j) tot += (int64_t)len[j] * rpw;
+    tile_entries[t] = tot;
+  }
+}
+
+__global__ void sell_fill_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                 const float* __restrict__ val, int64_t row_begin, int64_t row_end, int tr, int rpw,
+                                 const uint16_t* __restrict__ order, const int32_t* __restrict__ slice_len,
+                                 const int64_t* __restrict__ tile_ptr, int32_t sentinel, int2* __restrict__ meta,
+                                 int32_t* __restrict__ idx, float* __restrict__ sval) {
+  const int64_t t = blockIdx.x;
+  const int64_t r0 = row_begin + t * tr;
+  const int cnt = static_cast<int>(min((int64_t)tr, row_end - r0));
+  __shared__ int off[65];
+  __shared__ int64_t rb[1024];
+  __shared__ int deg[1024];
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int j = 0; j < kNC; ++j) {
+      off[j] = o;
+      o += slice_len[t * kNC + j] * rpw;
+    }
+    off[kNC] = o;
+  }
+  for (int r = threadIdx.x; r < tr; r += blockDim.x) {
+    if (r < cnt) {
+      const int64_t row = r0 + order[t * tr + r];
+      rb[r] = row_ptr[row];
+      deg[r] = static_cast<int>(row_ptr[row + 1] - rb[r]);
+    } else {
+      rb[r] = 0;
+      deg[r] = 0;
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < kNC; j += blockDim.x) meta[t * kNC + j] = make_int2(off[j], slice_len[t * kNC + j]);
+  const int64_t base = tile_ptr[t];
+  const int total = off[kNC];
+  for (int q = threadIdx.x; q < total; q += blockDim.x) {
+    int j = 0;
+    while (off[j + 1] <= q) ++j;
+    const int rel = q - off[j];
+    const int chunk = rel / (4 * rpw), rem = rel % (4 * rpw);
+    const int r = rem / 4;
+    const int e = chunk * 4 + rem % 4;
+    const int rank = j * rpw + r;
+    const bool real = rank < cnt && e < deg[rank];
+    idx[base + q] = real ? col[rb[rank] + e] : sentinel;
+    if (sval) sval[base + q] = real ? val[rb[rank] + e] : 0.f;
+  }
+}
+
+struct SellPlan {
+  int tr = 0, rpw = 0;
+  int64_t ntiles = 0, entries = 0, max_tile = 0;
+  DevBuf tile_ptr, meta, idx, val;
+  const uint16_t* order = nullptr;
+};
+
+std::mutex g_sell_mu;
+std::map<std::tuple<const sc_graph*, int, int64_t, int64_t>, std::unique_ptr<SellPlan>> g_sell_plans;
+
+int env_int_s(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+int sell_plan(const sc_graph* g, int vpr, int64_t row_begin, int64_t row_end, cudaStream_t s, SellPlan** out) {
+  const int tr = sell_tile_rows(vpr), rpw = 32 / vpr;
+  std::lock_guard<std::mutex> lock(g_sell_mu);
+  auto key = std::make_tuple(g, tr, row_begin, row_end);
+  auto it = g_sell_plans.find(key);
+  if (it != g_sell_plans.end()) {
+    *out = it->second.get();
+    return SC_OK;
+  }
+  auto pl = std::make_unique<SellPlan>();
+  pl->tr = tr;
+  pl->rpw = rpw;
+  pl->ntiles = (row_end - row_begin + tr - 1) / tr;
+  pl->order = tile_order(g, tr, row_begin, row_end, s);
+  if (!pl->order) return fail(SC_ERR_NOMEM, "tile order allocation failed");
+  const int64_t nt = pl->ntiles;
+  DevBuf slen, tent;
+  SC_TRY(slen.ensure(sizeof(int32_t) * std::max<int64_t>(1, nt * kNC)));
+  SC_TRY(tent.ensure(sizeof(int64_t) * std::max<int64_t>(1, nt)));
+  if (nt > 0) {
+    sell_len_kernel<<<(unsigned)nt, 64, 0, s>>>(g->row_ptr.as<int64_t>(), row_begin, row_end, tr, rpw, pl->order,
+                                                slen.as<int32_t>(), tent.as<int64_t>());
+    SC_CUDA_TRY(cudaGetLastError());
+  }
+  std::vector<int64_t> h(nt), ptr(nt + 1, 0);
+  if (nt > 0) {
+    SC_CUDA_TRY(cudaMemcpyAsync(h.data(), tent.ptr, sizeof(int64_t) * nt, cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  for (int64_t t = 0; t < nt; ++t) {
+    ptr[t + 1] = ptr[t] + h[t];
+    pl->max_tile = std::max(pl->max_tile, h[t]);
+  }
+  pl->entries = ptr[nt];
+  SC_TRY(pl->tile_ptr.ensure(sizeof(int64_t) * (nt + 1)));
+  SC_CUDA_TRY(cudaMemcpyAsync(pl->tile_ptr.ptr, ptr.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, s));
+  SC_TRY(pl->meta.ensure(sizeof(int2) * std::max<int64_t>(1, nt * kNC)));
+  SC_TRY(pl->idx.ensure(sizeof(int32_t) * std::max<int64_t>(4, pl->entries)));
+  if (!g->unit_weights) SC_TRY(pl->val.ensure(sizeof(float) * std::max<int64_t>(4, pl->entries)));
+  if (nt > 0) {
+    sell_fill_kernel<<<(unsigned)nt, 256, 0, s>>>(
+        g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(), g->unit_weights ? nullptr : g->values.as<float>(),
+        row_begin, row_end, tr, rpw, pl->order, slen.as<int32_t>(), pl->tile_ptr.as<int64_t>(),
+        static_cast<int32_t>(g->n_cols), pl->meta.as<int2>(), pl->idx.as<int32_t>(),
+        g->unit_weights ? nullptr : pl->val.as<float>());
+    SC_CUDA_TRY(cudaGetLastError());
+  }
+  SC_CUDA_TRY(cudaStreamSynchronize(s));   // slen / tent are freed on return
+  *out = pl.get();
+  g_sell_plans[key] = std::move(pl);
+  return SC_OK;
+}
+
+template <typename T>
+using SellFn = void (*)(SellDev, const T*, StepParams, int);
+
+template <typename T, int VPR>
+SellFn<T> pick_sell_unit(bool unit) {
+  if constexpr (sizeof(T) == 4) {
+    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB, true>;
+    return cheb_sell_kernel<T, VPR, SC_SELL_NB_W, false>;
+  } else {
+    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, true>;
+    return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, false>;
+  }
+}
+
+template <typename T>
+SellFn<T> pick_sell(int vpr, bool unit) {
+  switch (vpr) {
+    case 1: return pick_sell_unit<T, 1>(unit);
+    case 2: return pick_sell_unit<T, 2>(unit);
+    case 3: return pick_sell_unit<T, 3>(unit);
+    case 4: return pick_sell_unit<T, 4>(unit);
+    case 6: return pick_sell_unit<T, 6>(unit);
+    case 8: return pick_sell_unit<T, 8>(unit);
+    case 12: return pick_sell_unit<T, 12>(unit);
+    case 16: return pick_sell_unit<T, 16>(unit);
+    case 24: return pick_sell_unit<T, 24>(unit);
+    case 32: return pick_sell_unit<T, 32>(unit);
+    default: return nullptr;
+  }
+}
+
+// stage capacity (SELL entries) for a plan: its largest tile rounded up to 64 entries, so
+// the CTA takes no more shared memory than it needs (the rest of the SM's 228 KB is L1,
+// which holds the gathers in flight); 0 if that does not fit SC_SELL_SMEM_KB
+int sell_cap(int tr, bool unit, int64_t max_tile) {
+  const int per_entry = unit ? 4 : 8;
+  const int64_t cap = std::max<int64_t>(64, (max_tile + 63) & ~int64_t(63));
+  const SellLayout lay(tr, (int)std::min<int64_t>(cap, INT_MAX / 8), unit);
+  return lay.total <= (size_t)SC_SELL_SMEM_KB * 1024 && cap * per_entry < INT_MAX / 4 ? (int)cap : 0;
+}
+
+}  // namespace
+
+bool sell_enabled() {
+  static const bool v = env_int_s("SC_SELL", 1) != 0;
+  return v;
+}
+
+void sell_release(const sc_graph* g) {
+  std::lock_guard<std::mutex> lock(g_sell_mu);
+  for (auto it = g_sell_plans.begin(); it != g_sell_plans.end();) {
+    if (std::get<0>(it->first) == g) it = g_sell_plans.erase(it);
+    else ++it;
+  }
+}
+
+// Can the SELL kernel run this (graph, chunk width, row range)?  Builds (and caches) the
+// plan; false when a supported width has a tile whose padded entries exceed a stage (very
+// high-degree rows: the CSR kernel handles those graphs).
+template <typename T>
+int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end, cudaStream_t s, bool* ok) {
+  constexpr int W = Vec<T>::W;
+  *ok = false;
+  if (width % W || !pick_sell<T>(width / W, g->unit_weights) || row_end - row_begin >= INT_MAX) return SC_OK;
+  const int vpr = width / W;
+  if ((sell_tile_rows(vpr) * 2) % 16) return SC_OK;   // the tile's order segment must be a 16-byte bulk copy
+  SellPlan* pl = nullptr;
+  SC_TRY(sell_plan(g, vpr, row_begin, row_end, s, &pl));
+  *ok = sell_cap(sell_tile_rows(vpr), g->unit_weights, pl->max_tile) > 0;
+  return SC_OK;
+}
+template int sell_usable<float>(const sc_graph*, int, int64_t, int64_t, cudaStream_t, bool*);
+template int sell_usable<double>(const sc_graph*, int, int64_t, int64_t, cudaStream_t, bool*);
+
+// One fused step over the SELL layout.  Requirements: T_s (p.tcur) has a zero row at index
+// g->n_cols (the sentinel of the padding); rows [row_begin, row_end) of one graph.
+template <typename T>
+int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, double* algo_bytes) {
+  constexpr int W = Vec<T>::W;
+  if (p.width % W) return fail(SC_ERR_ARG, "unsupported chunk width " + std::to_string(p.width));
+  const int vpr = p.width / W;
+  SellFn<T> k = pick_sell<T>(vpr, g->unit_weights);
+  if (!k) return fail(SC_ERR_ARG, "unsupported chunk width " + std::to_string(p.width));
+  const int tr = sell_tile_rows(vpr);
+  SellPlan* pl = nullptr;
+  SC_TRY(sell_plan(g, vpr, p.row_begin, p.row_end, s, &pl));
+  const int cap = sell_cap(tr, g->unit_weights, pl->max_tile);
+  if (cap <= 0) return fail(SC_ERR_STATE, "SELL tile exceeds the stage capacity");
+  const SellLayout lay(tr, cap, g->unit_weights);
+  const int smem = static_cast<int>(lay.total);
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> occ_cache;
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = occ_cache.find({(const void*)k, smem});
+    if (it == occ_cache.end()) {
+      SC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+      occ_cache[{(const void*)k, smem}] = occ;
+    } else {
+      occ = it->second;
+    }
+  }
+  const int64_t rows = p.row_end - p.row_begin;
+  if (rows <= 0) return SC_OK;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(pl->ntiles, (int64_t)g->num_sms * occ)));
+  SellDev sd{pl->tile_ptr.as<int64_t>(), pl->meta.as<int2>(), pl->idx.as<int32_t>(),
+             g->unit_weights ? nullptr : pl->val.as<float>(), pl->order};
+  const T* strength = sizeof(T) == 4 ? reinterpret_cast<const T*>(g->strength32.ptr)
+                                     : reinterpret_cast<const T*>(g->strength64.ptr);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, sd, strength, p, cap));
+  if (algo_bytes) {
+    // algorithmic bytes of the step: the CSR share of this chunk (row
+    // pointers + column indices [+ weights], not the padding) + dense operands touched once
+    const double csr = (double)rows * 8.0 + (double)g->nnz * (g->unit_weights ? 4.0 : 8.0) * rows / g->n_rows;
+    const double dense_rows = (1.0 + (p.tprev ? 1.0 : 0.0) + (p.tnext ? 1.0 : 0.0) +
+                               (p.y_mode == 2 ? 2.0 : (p.y_mode == 1 ? 1.0 : 0.0)));
+    const double frac = (double)p.width / (p.total_width > 0 ? p.total_width : p.width);
+    *algo_bytes = csr * frac + dense_rows * (double)rows * p.width * sizeof(T);
+  }
+  return SC_OK;
+}
+template int launch_sell_step<float>(const sc_graph*, const StepParams&, cudaStream_t, double*);
+template int launch_sell_step<double>(const sc_graph*, const StepParams&, cudaStream_t, double*);
+
+}  // namespace sc

@@ -254,6 +254,36 @@ def gmm_knn(n: int = 20_000, dim: int = 10, n_comp: int = 10, knn: int = 10, sig
     return _connect_components(g, rng)
 
 
+def permute(g: CSRGraph, perm: np.ndarray) -> CSRGraph:
+    """Relabel node perm[i] as i (new CSR, columns sorted per row); labels follow."""
+    n = g.n
+    inv = np.empty(n, dtype=np.int64)
+    inv[perm] = np.arange(n, dtype=np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(g.row_ptr))
+    a, b = inv[rows], inv[g.col_idx.astype(np.int64)]
+    order = np.lexsort((b, a))
+    a, b = a[order], b[order]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(row_ptr, a + 1, 1)
+    row_ptr = np.cumsum(row_ptr)
+    vals = None if g.values is None else g.values[order]
+    labels = None if g.labels is None else g.labels[perm]
+    return CSRGraph(n=n, row_ptr=row_ptr, col_idx=b.astype(np.int32), values=vals, labels=labels,
+                    meta=dict(g.meta, permuted=True))
+
+
+def rcm_order(g: CSRGraph) -> CSRGraph:
+    """Reverse Cuthill-McKee relabelling (scipy.sparse.csgraph): neighbours get nearby
+    indices, so the rows a tile gathers are close together in memory."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+    A = sp.csr_matrix((np.ones(g.nnz, dtype=np.int8), g.col_idx, g.row_ptr), shape=(g.n, g.n))
+    perm = np.asarray(reverse_cuthill_mckee(A, symmetric_mode=True), dtype=np.int64)
+    out = permute(g, perm)
+    out.meta["order"] = "rcm"
+    return out
+
+
 # ----------------------------------------------------------------------------
 # Small fixtures with closed-form spectra (tests)
 # ----------------------------------------------------------------------------

@@ -48,22 +48,24 @@ def _key(seed: int, stream: int) -> np.uint64:
 
 
 def gaussian_block(seed: int, n: int, eta: int, row0: int = 0, dtype=np.float32,
-                   variance: float | None = None, stream: int = 0) -> np.ndarray:
+                   variance: float | None = None, stream: int = 0, cols=None) -> np.ndarray:
     """Rows [row0, row0+n) of the N x eta Gaussian block for ``seed``.
 
     ``variance`` defaults to 1/eta.  ``row0`` lets a rank
     of a row-partitioned run generate exactly its own rows of the global block.
+    ``cols`` (optional): only these columns of the eta-wide block (same values).
     """
     if variance is None:
         variance = 1.0 / eta
     key = _key(seed, stream)
-    out = np.empty((n, eta), dtype=dtype)
+    qs = np.arange(eta, dtype=np.uint64) if cols is None else np.asarray(cols, dtype=np.uint64)
+    out = np.empty((n, len(qs)), dtype=dtype)
     scale = np.sqrt(np.float64(variance))
-    chunk = max(1, (1 << 22) // max(eta, 1))
+    chunk = max(1, (1 << 22) // max(len(qs), 1))
     for r0 in range(0, n, chunk):
         r1 = min(n, r0 + chunk)
         ctr = (np.arange(row0 + r0, row0 + r1, dtype=np.uint64)[:, None] * np.uint64(eta)
-               + np.arange(eta, dtype=np.uint64)[None, :])
+               + qs[None, :])
         with np.errstate(over="ignore"):
             h1 = splitmix64(key + np.uint64(2) * ctr)
             h2 = splitmix64(key + np.uint64(2) * ctr + np.uint64(1))

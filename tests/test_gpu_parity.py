@@ -314,6 +314,30 @@ def test_full_size_c4_properties(sc):
     assert rel(a, b.astype(np.float64)) <= 1e-6
 
 
+@pytest.mark.slow
+def test_full_size_c4_oracle_columns(sc):
+    """configs[4] (SBM N=10^7, 2e8 nonzeros, R=96, p=300) at full size in bench.py's launch
+    configuration (96 columns, chunk plan 64 + 32): two sampled columns, one from each chunk,
+    against the oracle's plain-C fp64 filter (oracle/cfilter.c, every host core)."""
+    from oracle import cfilter
+    from scinputs import configs
+    w = configs.WORKLOADS["c4_sbm10m"]
+    g = configs.build_graph("c4_sbm10m")
+    G = sc.Graph.from_csr(g)
+    n, R, p = g.n, w.R, w.order
+    lmax = sc.sc_lambda_max(G.handle, 40, 0.01, 3)
+    lc = 0.05 * lmax
+    Y = torch.empty((n, R), dtype=torch.float32, device="cuda")
+    sc.sc_filter_lowpass_f32(G.handle, lc, lmax, p, w.jackson, R, 81, None, Y)
+    cols = [7, 90]
+    Yg = Y[:, cols].cpu().numpy()
+    del Y
+    G.close()
+    X = scinputs.gaussian_block(81, n, R, cols=cols).astype(np.float64)
+    Yo = cfilter.cheb_filter(g, X, chebyshev.filter_coeffs(lc, lmax, p, w.jackson), lmax)
+    assert rel(Yg, Yo) <= F32_TOL
+
+
 # ---------------------------------------------------------------------------
 # eigencount moments and lambda_k dichotomy
 # ---------------------------------------------------------------------------
@@ -522,6 +546,46 @@ def test_cluster_pipeline_recovers_planted_sbm(sc):
     assert 4.5 <= info[2] <= 5.5
     ev = np.linalg.eigvalsh(laplacian.laplacian_dense(g))
     assert ev[-1] <= info[0] <= 1.02 * ev[-1]
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+def test_cluster_matches_oracle_pipeline(sc, normalize):
+    """sc_cluster (§4.1 steps 1-6, l.303-329) against oracle.pipeline.accelerated_sc
+    fed the same inputs: the GPU's lambda_max bound (two estimators of one bound, R3), the
+    eigencount probes (stream 2, seed ^ 0x5e5e5e5e, variance 1/n_probe), the signal block
+    (stream 0, fp32-rounded), the k-means++ uniforms (stream 1).  Checked stage by stage:
+    lambda~_k equal (or the dichotomy decision within rounding of k - 1/2), the features at
+    the fp32 tolerance, k-means labels bit-exact on the oracle's fp32-rounded features, and
+    the end-to-end labels (ARI >= 0.99)."""
+    g = scinputs.sbm(2000, 5, 20, 0.05, seed=1234)
+    k, R, order, npr, seed, restarts, max_iter = 5, 32, 60, 32, 2024, 10, 100
+    G = sc.Graph.from_csr(g)
+    lab = np.zeros(g.n, dtype=np.int32)
+    info = sc.sc_cluster(G.handle, k, R, order, True, npr, seed, restarts, max_iter, normalize, lab)
+    lmax, lk = float(info[0]), float(info[1])
+    X = scinputs.gaussian_block(seed, g.n, R).astype(np.float64)
+    P = scinputs.gaussian_block(seed ^ 0x5E5E5E5E, g.n, npr, dtype=np.float64, stream=2)
+    u = np.stack([scinputs.uniforms(seed, k, offset=k * r) for r in range(restarts)])
+    out = pipeline.accelerated_sc(g, k, X, P, order, True, u, lambda_max_value=lmax, normalize=normalize,
+                                  max_iter=max_iter, bisect_iter=40, bisect_rtol=1e-4)
+    L = laplacian.laplacian(g)
+    if lk != out["lambda_k"]:
+        _, _, trace = eigencount.estimate_lambda_k(L, k, lmax, order, P, True, 40, 1e-4)
+        assert min(abs(c - (k - 0.5)) for _, c in trace) < 1e-8 * np.sum(P * P)
+    # features: the filter call sc_cluster makes (seeded signals, lambda~_k, Jackson)
+    Yd = torch.empty((g.n, R), dtype=torch.float32, device="cuda")
+    sc.sc_filter_lowpass_f32(G.handle, lk, lmax, order, True, R, seed, None, Yd)
+    Yo = chebyshev.lowpass_filter(L, X, lk, lmax, order, True)
+    assert rel(Yd.cpu().numpy(), Yo) <= F32_TOL
+    # k-means on the oracle's features, rounded to fp32 once: labels bit-exact
+    F = (pipeline.normalize_rows(Yo) if normalize else Yo).astype(np.float32)
+    lab2 = np.zeros(g.n, dtype=np.int32)
+    _, it2, best2 = sc.sc_kmeans(F, g.n, R, k, restarts, max_iter, seed, None, lab2)
+    lo, _, _, ito, ro, _ = kmeans.kmeans(F, k, u, max_iter)
+    assert np.array_equal(lab2, lo) and best2 == ro and it2 == ito
+    # end to end
+    assert oari.ari(lab, out["labels"]) >= 0.99
+    assert oari.ari(lab, g.labels) > 0.95
 
 
 # ---------------------------------------------------------------------------

@@ -163,24 +163,34 @@ def _path_eigs(n):
     return lam, V
 
 
+def _cheb_filter_impl(impl, g, R, coeffs, lmax):
+    """The two oracle implementations of the same definition: numpy (chebyshev.cheb_filter
+    on L) and plain C with OpenMP rows (cfilter.cheb_filter on W's CSR)."""
+    if impl == "numpy":
+        return chebyshev.cheb_filter(laplacian.laplacian(g), R, coeffs, lmax)
+    from oracle import cfilter
+    return cfilter.cheb_filter(g, R, coeffs, lmax, nthreads=3)
+
+
+@pytest.mark.parametrize("impl", ["numpy", "c"])
 @pytest.mark.parametrize("damping", [False, True])
-def test_filter_recurrence_vs_closed_form_path_eigenbasis(damping):
+def test_filter_recurrence_vs_closed_form_path_eigenbasis(damping, impl):
     """F R = V diag(p(lambda)) V^T R with the DCT-II eigenbasis of the path graph
     (closed form) and p evaluated by numpy's chebval (independent of the recurrence)."""
     n, order = 40, 60
     lam, V = _path_eigs(n)
     assert np.allclose(V.T @ V, np.eye(n), atol=1e-12)
-    L = laplacian.laplacian(scinputs.path(n))
     lmax, lc = 4.0, 0.6
     coeffs = chebyshev.filter_coeffs(lc, lmax, order, damping)
     R = np.random.default_rng(5).standard_normal((n, 7))
-    Y = chebyshev.cheb_filter(L, R, coeffs, lmax)
+    Y = _cheb_filter_impl(impl, scinputs.path(n), R, coeffs, lmax)
     pl = npcheb.chebval(2 * lam / lmax - 1, coeffs)
     Yex = V @ (pl[:, None] * (V.T @ R))
     assert np.linalg.norm(Y - Yex) <= 1e-11 * np.linalg.norm(Yex)
 
 
-def test_filter_recurrence_vs_dense_eig_random_weighted():
+@pytest.mark.parametrize("impl", ["numpy", "c"])
+def test_filter_recurrence_vs_dense_eig_random_weighted(impl):
     for s in range(4):
         g = scinputs.random_connected(50, 0.15, seed=10 + s)
         L = laplacian.laplacian(g)
@@ -188,10 +198,28 @@ def test_filter_recurrence_vs_dense_eig_random_weighted():
         lmax = 1.01 * lam[-1]
         coeffs = chebyshev.filter_coeffs(0.3 * lmax, lmax, 45, s % 2 == 0)
         R = np.random.default_rng(s).standard_normal((g.n, 5))
-        Y = chebyshev.cheb_filter(L, R, coeffs, lmax)
+        Y = _cheb_filter_impl(impl, g, R, coeffs, lmax)
         pl = npcheb.chebval(2 * lam / lmax - 1, coeffs)
         Yex = chi @ (pl[:, None] * (chi.T @ R))
         assert np.linalg.norm(Y - Yex) <= 1e-10 * np.linalg.norm(Yex)
+
+
+def test_c_oracle_matches_numpy_oracle_and_constant_vector():
+    """The C oracle against the numpy one (same definition, different summation order:
+    agreement to rounding) on an unweighted SBM and a weighted kNN graph, plus the
+    constant-vector identity F 1 = p(0) 1 (L 1 = 0) and thread-count independence."""
+    from oracle import cfilter
+    for g in (scinputs.sbm(800, 4, 12, 0.1, seed=3), scinputs.gmm_knn(600, 3, 4, 6, seed=2)):
+        lmax = 2.0 * g.degrees().max() if g.values is None else 2.0 * np.max(
+            np.add.reduceat(g.weights(), g.row_ptr[:-1]))
+        coeffs = chebyshev.filter_coeffs(0.15 * lmax, lmax, 70, True)
+        R = np.random.default_rng(1).standard_normal((g.n, 6))
+        Yn = chebyshev.cheb_filter(laplacian.laplacian(g), R, coeffs, lmax)
+        Yc = cfilter.cheb_filter(g, R, coeffs, lmax, nthreads=4)
+        assert np.linalg.norm(Yc - Yn) <= 1e-12 * np.linalg.norm(Yn)
+        assert np.array_equal(Yc, cfilter.cheb_filter(g, R, coeffs, lmax, nthreads=1))
+        y1 = cfilter.cheb_filter(g, np.ones(g.n), coeffs, lmax)
+        assert np.allclose(y1, npcheb.chebval(-1.0, coeffs), atol=1e-11)
 
 
 def test_filter_approximates_ideal_projector_within_polynomial_error():
@@ -349,6 +377,58 @@ def test_kmeanspp_hand_example():
     assert list(kmeans.kmeanspp(X, 2, np.array([0.0, 0.5]))) == [0, 2]     # 50.5 -> idx 2
     assert list(kmeans.kmeanspp(X, 2, np.array([0.0, 0.005]))) == [0, 1]   # 0.505 -> idx 1
     assert list(kmeans.kmeanspp(X, 2, np.array([0.99, 0.0]))) == [2, 0]    # D^2 = (100, 81, 0)
+
+
+def test_kmeans_best_replicate_rule_hand_example():
+    """Replicate selection (oracle/kmeans.py kmeans(): lowest inertia wins, ties -> lowest
+    replicate index; R8, §5 l.404 'replicates').  1-D points
+    A = {0, 1}, B = {10, 11}, C = {100, 120}, k = 3, four restarts whose seeds (chosen by
+    hand through the D^2 cumulative sums) converge to two different local optima:
+      r0, r3: seeds 0, 10, 100 -> {A}, {B}, {C}:   inertia 4 * 0.25 + 2 * 100   = 201
+      r1:     seeds 100, 120, 0 -> {100}, {120}, {A u B}: 2 * 5.5^2 + 2 * 4.5^2 = 101
+      r2:     seeds 120, 100, 1 -> {120}, {100}, {A u B}: 101 (an exact tie with r1,
+              different label numbering)
+    Expected: replicate 1 (not 2: ties go to the lowest index; not 0 or 3: the minimum)."""
+    X = np.array([[0.0], [1.0], [10.0], [11.0], [100.0], [120.0]])
+    u = np.array([[0.0, 0.002, 0.2],      # seeds 0, 2, 4 (hand cumsums in the docstring)
+                  [0.7, 0.995, 0.1],      # seeds 4, 5, 0
+                  [0.9, 0.995, 0.4],      # seeds 5, 4, 1
+                  [0.0, 0.002, 0.2]])
+    assert list(kmeans.kmeanspp(X, 3, u[0])) == [0, 2, 4]
+    assert list(kmeans.kmeanspp(X, 3, u[1])) == [4, 5, 0]
+    assert list(kmeans.kmeanspp(X, 3, u[2])) == [5, 4, 1]
+    labels, C, inertia, it, r, seeds = kmeans.kmeans(X, 3, u, 50)
+    assert r == 1 and inertia == 101.0
+    assert list(labels) == [2, 2, 2, 2, 0, 1]
+    assert np.array_equal(C[:, 0], [100.0, 120.0, 5.5])
+    # the single-restart results the rule chooses among
+    assert kmeans.kmeans(X, 3, u[:1], 50)[2] == 201.0
+    assert list(kmeans.kmeans(X, 3, u[2:3], 50)[0]) == [2, 2, 2, 2, 1, 0]
+    # order matters only through the index: the tie goes to whichever comes first
+    assert kmeans.kmeans(X, 3, u[[2, 1]], 50)[4] == 0
+    assert list(kmeans.kmeans(X, 3, u[[0, 3]], 50)[0]) == [0, 0, 1, 1, 2, 2]
+
+
+def test_poly_eval_against_chebval_and_hand_values():
+    """oracle/chebyshev.py poly_eval: p(lambda) = sum_j c_j T_j(x), x = 2 lambda / lambda_max - 1
+    (R1).  Pinned to hand values of T_0..T_3 and to numpy's Clenshaw evaluation
+    (numpy.polynomial.chebyshev.chebval), an independent routine."""
+    lmax = 4.0
+    # x = -1, -0.5, 0, 0.5, 1 at lambda = 0, 1, 2, 3, 4
+    lam = np.array([0.0, 1.0, 2.0, 3.0, 4.0])
+    assert np.allclose(chebyshev.poly_eval(lam, np.array([1.0]), lmax), 1.0)
+    assert np.allclose(chebyshev.poly_eval(lam, np.array([0.0, 1.0]), lmax), [-1, -0.5, 0, 0.5, 1])
+    assert np.allclose(chebyshev.poly_eval(lam, np.array([0.0, 0.0, 1.0]), lmax), [1, -0.5, -1, -0.5, 1])
+    assert np.allclose(chebyshev.poly_eval(lam, np.array([0.0, 0.0, 0.0, 1.0]), lmax), [-1, 1, 0, -1, 1])
+    rng = np.random.default_rng(5)
+    for p in (1, 7, 50, 300):
+        c = rng.standard_normal(p + 1)
+        lam = rng.uniform(0.0, lmax, 64)
+        want = npcheb.chebval(2.0 * lam / lmax - 1.0, c)
+        assert np.allclose(chebyshev.poly_eval(lam, c, lmax), want, rtol=1e-10, atol=1e-10 * np.abs(c).sum())
+    # the filter's polynomial at 0 (the value F 1 = p(0) 1 uses) for the damped step
+    d = chebyshev.filter_coeffs(0.3, 4.0, 40, True)
+    assert chebyshev.poly_eval(0.0, d, 4.0) == pytest.approx(npcheb.chebval(-1.0, d), rel=1e-12)
 
 
 def test_kmeans_inertia_monotone():

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--tag", default="")
+    ap.add_argument("--pols", default="", help="comma list of SC_L2POL values to sweep (experiment knob)")
     a = ap.parse_args()
     w = configs.WORKLOADS[a.workload]
     g = configs.build_graph(a.workload, cache=True)
@@ -43,9 +44,11 @@ def main():
     Y = torch.empty_like(X)
     f = sc.sc_filter_apply_f32 if a.dtype == "f32" else sc.sc_filter_apply_f64
     nnz_l = g.nnz + n
+    pols = a.pols.split(",") if a.pols else [os.environ.get("SC_L2POL", "0")]
     for ch in a.chunks.split(","):
-        for fl in a.l2flags.split(","):
+        for fl in pols:
             os.environ["SC_CHUNK"] = ch
+            os.environ["SC_L2POL"] = fl
             f(G.handle, d, order, lmax, R, X, Y)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -58,7 +61,7 @@ def main():
             launches, steps, kms, abytes = sc.sc_profile_end()
             ms = e0.elapsed_time(e1) / a.reps
             print(json.dumps({"tag": a.tag, "workload": a.workload, "dtype": a.dtype, "chunk": int(ch),
-                              "l2flags": int(fl), "ms_per_pass": round(ms, 3),
+                              "l2pol": int(fl), "ms_per_pass": round(ms, 3),
                               "value": nnz_l * R * order / (ms / 1e3),
                               "algo_GBps": abytes / (kms / 1e3) / 1e9, "step_launches": steps // a.reps}),
                   flush=True)
