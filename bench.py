@@ -279,9 +279,6 @@ def run_ours(args):
         handle = G.handle
     else:
         from paper_1509_08863_b200 import dist as pdist
-        # lambda bounds on rank-local copies are not needed: Gershgorin bound + fixed cut
-        lmax = 2.0 * float(g.degrees().max())
-        lam_k, count_k = 0.25 * lmax, None
         # 2-D decomposition: column group cgrp filters columns [c0, c1) of every row; its
         # n_row ranks row-partition the graph and exchange halos among themselves only
         n_cg, n_row = pdist.grid_shape(world, R, col_groups=args.col_groups or None)
@@ -294,6 +291,12 @@ def run_ours(args):
                 else pdist.send_lists_from_halos(part, [part.halo_gid]))
         Gl = sc.Graph(part.n_local, part.row_ptr, part.col_idx, part.values, n_cols=part.n_local + part.n_halo)
         handle = Gl.handle
+        # PAPER.md §4.1 steps 1-2 on the partition: Lanczos lambda_N and the eigencount
+        # dichotomy, halo exchange before every SpMV, inner products all-reduced over the
+        # row group (every column group holds the whole graph: same estimates)
+        est = pdist.NcclFilter(part, handle, group=rgroup)
+        lmax = est.lambda_max(60, 0.01, args.seed)
+        lam_k, count_k = est.estimate_lambda_k(w.k, lmax, min(order, 150), True, 32, args.seed + 1, 40, 1e-4)
     d = sc.sc_cheby_coeffs(lam_k, lmax, order, w.jackson)
 
     if not partitioned:
@@ -316,12 +319,13 @@ def run_ours(args):
         if exchange == "p2p":
             try:
                 nf = pdist.P2PFilter(part, handle, n, c1 - c0, group=rgroup)
+                est.close()
             except Exception as e:   # IPC mapping unavailable: the NCCL schedule instead
                 print(f"[bench] p2p exchange setup failed ({e}); using NCCL", file=sys.stderr)
                 exchange = f"nccl (p2p setup failed: {str(e)[:80]})"
-                nf = pdist.NcclFilter(part, handle, group=rgroup)
+                nf = est
         else:
-            nf = pdist.NcclFilter(part, handle, group=rgroup)
+            nf = est
         if n_row == 1:
             exchange = "none (one row block per column group: no halo)"
 

@@ -297,6 +297,10 @@ int sc_nccl_unique_id(void* id);
 
 /* Communicator of `world` ranks on the current device.  Errors: SC_ERR_CUDA from NCCL. */
 int sc_comm_init(const void* id, int world, int rank, sc_comm** out);
+/* Communicator without NCCL for rank `rank` of `world` (<= 8): the single-process emulation
+ * in which one process holds every rank's plan on one GPU (sc_dist_lambda_max and friends
+ * with nheld == world).  Errors: SC_ERR_ARG for world outside [1, 8] or a bad rank. */
+int sc_comm_local(int world, int rank, sc_comm** out);
 int sc_comm_free(sc_comm* c);
 
 /*
@@ -321,6 +325,31 @@ int sc_dist_free(sc_dist* d);
  */
 int sc_dist_filter_f32(sc_dist* d, const double* coeffs, int order, double lambda_max, int R, const float* X,
                        float* Y, void* stream);
+
+/*
+ * Row-partitioned lambda estimates (§4.1 steps 1-2, l.309-311; §3.2 l.269-275):
+ * the single-GPU estimators (sc_lambda_max, sc_cheb_moments, sc_estimate_lambda_k) on the
+ * partition, every SpMV preceded by the halo exchange of its vector and every inner product
+ * summed over the ranks.  ds / nheld: the plans this process holds -- nheld = 1 (one process
+ * per GPU; a multi-rank plan needs an NCCL communicator: halos by send/recv, sums by
+ * ncclAllReduce) or nheld = world (all ranks of the partition in this process on one GPU,
+ * created with sc_comm_local: halos copied, sums in rank order; ds[r] is rank r).
+ * row0 (host int64 [nheld] or NULL = 0): counter offset of each held rank's first local row
+ * for the start vector (stream 0) and the probes (stream 2, variance 1/n_probe, counters
+ * (row0 + i) * n_probe + q).  All ranks must call collectively with the same arguments.
+ * sc_dist_lambda_max: min((1 + margin) theta, 2 max_i s_i) as sc_lambda_max.
+ * sc_dist_cheb_moments: moments[0..2 order] (host) of the probes, as sc_cheb_moments.
+ * sc_dist_estimate_lambda_k: dichotomy on those moments, as sc_estimate_lambda_k.
+ * Errors: SC_ERR_ARG (bad sizes, plans not ranks 0..world-1, disagreeing send/receive
+ * counts), SC_ERR_CUDA (CUDA or NCCL).
+ */
+int sc_dist_lambda_max(sc_dist* const* ds, int nheld, int iters, double margin, uint64_t seed, const int64_t* row0,
+                       double* out, void* stream);
+int sc_dist_cheb_moments(sc_dist* const* ds, int nheld, double lambda_max, int order, int n_probe, uint64_t seed,
+                         const int64_t* row0, double* moments, void* stream);
+int sc_dist_estimate_lambda_k(sc_dist* const* ds, int nheld, int k, double lambda_max, int order, int jackson,
+                              int n_probe, uint64_t seed, const int64_t* row0, int max_iter, double rtol,
+                              double* lambda_k, double* count_k, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Row-partitioned filter with the halo exchange fused into the step kernel */

@@ -75,7 +75,29 @@ def build(verbose_ptxas: bool = False, defs=(), out: str = LIB) -> str:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    check_sass(out)
     return out
+
+
+def check_sass(lib: str) -> None:
+    """Reject SASS whose 64-bit memory descriptor sits in an odd uniform register pair
+    (desc[UR1], desc[UR3], ...): a misaligned wide operand that faults at run time with
+    cudaErrorIllegalInstruction.  ptxas 12.9 emitted it once for cp.async with an L2 cache
+    hint (round 2, SELL kernel)."""
+    import re
+    cuobjdump = os.path.join(os.path.dirname(NVCC), "cuobjdump")
+    r = subprocess.run([cuobjdump, "-sass", lib], capture_output=True, text=True)
+    if r.returncode != 0:
+        return
+    bad, fn = [], ""
+    for ln in r.stdout.splitlines():
+        if "Function :" in ln:
+            fn = ln.split("Function :")[1].strip()
+        elif re.search(r"desc\[UR\d*[13579]\]", ln):
+            bad.append(fn)
+    if bad:
+        os.remove(lib)
+        raise RuntimeError("SASS with a misaligned (odd) uniform descriptor register in: " + ", ".join(sorted(set(bad))))
 
 
 if __name__ == "__main__":

@@ -75,10 +75,15 @@ _F = {
                          c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp),
     "sc_nccl_unique_id": _sig("sc_nccl_unique_id", c_vp),
     "sc_comm_init": _sig("sc_comm_init", c_vp, c_i32, c_i32, P(c_vp)),
+    "sc_comm_local": _sig("sc_comm_local", c_i32, c_i32, P(c_vp)),
     "sc_comm_free": _sig("sc_comm_free", c_vp),
     "sc_dist_create": _sig("sc_dist_create", c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, P(c_vp)),
     "sc_dist_free": _sig("sc_dist_free", c_vp),
     "sc_dist_filter_f32": _sig("sc_dist_filter_f32", c_vp, c_vp, c_i32, c_dbl, c_i32, c_vp, c_vp, c_vp),
+    "sc_dist_lambda_max": _sig("sc_dist_lambda_max", c_vp, c_i32, c_i32, c_dbl, c_u64, c_vp, P(c_dbl), c_vp),
+    "sc_dist_cheb_moments": _sig("sc_dist_cheb_moments", c_vp, c_i32, c_dbl, c_i32, c_i32, c_u64, c_vp, c_vp, c_vp),
+    "sc_dist_estimate_lambda_k": _sig("sc_dist_estimate_lambda_k", c_vp, c_i32, c_i32, c_dbl, c_i32, c_i32, c_i32,
+                                      c_u64, c_vp, c_i32, c_dbl, P(c_dbl), P(c_dbl), c_vp),
     "sc_p2p_create": _sig("sc_p2p_create", c_vp, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i32,
                           P(c_vp)),
     "sc_p2p_free": _sig("sc_p2p_free", c_vp),
@@ -292,6 +297,12 @@ def sc_comm_init(uid: bytes, world, rank):
     return h.value
 
 
+def sc_comm_local(world, rank):
+    h = c_vp()
+    _check(_F["sc_comm_local"](world, rank, ctypes.byref(h)))
+    return h.value
+
+
 def sc_comm_free(c):
     _check(_F["sc_comm_free"](c))
 
@@ -313,6 +324,46 @@ def sc_dist_free(d):
 def sc_dist_filter_f32(d, coeffs, order, lambda_max, R, X, Y, stream=None):
     coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
     _check(_F["sc_dist_filter_f32"](d, coeffs.ctypes.data, order, lambda_max, R, _ptr(X), _ptr(Y), _stream(stream)))
+
+
+def _plans(ds):
+    ds = [ds] if isinstance(ds, int) else list(ds)
+    arr = (c_vp * len(ds))(*ds)
+    return arr, len(ds)
+
+
+def _row0(row0, n):
+    if row0 is None:
+        return None, None
+    r = np.ascontiguousarray(row0, dtype=np.int64).reshape(-1)
+    assert r.size == n
+    return r, r.ctypes.data
+
+
+def sc_dist_lambda_max(ds, iters=60, margin=0.01, seed=0, row0=None, stream=None) -> float:
+    arr, n = _plans(ds)
+    keep, r0 = _row0(row0, n)
+    out = c_dbl()
+    _check(_F["sc_dist_lambda_max"](arr, n, iters, margin, seed, r0, ctypes.byref(out), _stream(stream)))
+    return out.value
+
+
+def sc_dist_cheb_moments(ds, lambda_max, order, n_probe, seed, row0=None, stream=None) -> np.ndarray:
+    arr, n = _plans(ds)
+    keep, r0 = _row0(row0, n)
+    mu = np.zeros(2 * order + 1, dtype=np.float64)
+    _check(_F["sc_dist_cheb_moments"](arr, n, lambda_max, order, n_probe, seed, r0, mu.ctypes.data, _stream(stream)))
+    return mu
+
+
+def sc_dist_estimate_lambda_k(ds, k, lambda_max, order, jackson, n_probe, seed, row0=None, max_iter=40, rtol=1e-4,
+                              stream=None):
+    arr, n = _plans(ds)
+    keep, r0 = _row0(row0, n)
+    lk, ck = c_dbl(), c_dbl()
+    _check(_F["sc_dist_estimate_lambda_k"](arr, n, k, lambda_max, order, int(jackson), n_probe, seed, r0, max_iter,
+                                           rtol, ctypes.byref(lk), ctypes.byref(ck), _stream(stream)))
+    return lk.value, ck.value
 
 
 def sc_p2p_create(g, world, rank, n_global, sd_ptr, sd_row, sd_peer, sd_slot, peer_n_local, max_R):

@@ -46,6 +46,7 @@ struct sc_dist {
   std::vector<int64_t> send_counts, recv_counts, send_off, recv_off;
   sc::DevBuf send_idx;           // int64 [n_send] local (permuted) row positions, grouped by peer
   sc::DevBuf tA, tB, tC, sendbuf, xpad;
+  sc::DevBuf lz, probes, mpart, msums;   // partitioned lambda estimates (Lanczos, moments)
 };
 
 namespace sc {
@@ -76,6 +77,7 @@ __global__ void take_cols_kernel(const float* __restrict__ src, int64_t lds, int
 int exchange(sc_dist* d, float* T, int w, cudaStream_t cs) {
   sc_comm* c = d->c;
   if (c->world == 1 || (d->n_send == 0 && d->n_halo == 0)) return SC_OK;
+  if (!c->comm) return fail(SC_ERR_ARG, "a local (emulation) communicator has no NCCL exchange");
   if (d->n_send) {
     pack_rows_kernel<<<d->g->num_sms * 4, 256, 0, cs>>>(T, d->send_idx.as<int64_t>(), d->n_send, w,
                                                          d->sendbuf.as<float>());
@@ -98,6 +100,287 @@ int exchange(sc_dist* d, float* T, int w, cudaStream_t cs) {
   return SC_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Row-partitioned lambda estimates (§4.1 steps 1-2, l.309-311): Lanczos for
+// lambda_N and the Chebyshev moments of the eigencount (§3.2 l.269-275) on the partition.
+// The same SpMV / fused-step kernels as one GPU, with (a) the halo of the vector filled
+// before every product and (b) every inner product summed over the ranks.  `Ranks` are the
+// plans this process holds: one (one process per GPU: NCCL send/recv halos, NCCL all-reduce)
+// or all of them (the single-GPU emulation the tests use: halo rows copied between the ranks'
+// buffers, sums taken in rank order).
+// ---------------------------------------------------------------------------
+struct Ranks {
+  std::vector<sc_dist*> d;
+  int world() const { return d[0]->c->world; }
+  bool nccl() const { return d.size() == 1 && world() > 1; }
+};
+
+struct DPtrs {
+  double* p[kP2PMaxWorld];
+};
+
+// x[r][0..count) = sum over ranks in rank order, written back to every rank
+__global__ void sum_ranks_kernel(DPtrs x, int world, int count) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    double acc = 0.0;
+    for (int r = 0; r < world; ++r) acc += x.p[r][i];
+    for (int r = 0; r < world; ++r) x.p[r][i] = acc;
+  }
+}
+
+int allreduce_sum(const Ranks& R, const std::vector<double*>& x, int count, cudaStream_t s) {
+  if (R.world() == 1) return SC_OK;
+  if (R.nccl()) {
+    SC_NCCL_TRY(ncclAllReduce(x[0], x[0], count, ncclDouble, ncclSum, R.d[0]->c->comm, s));
+    return SC_OK;
+  }
+  DPtrs dp{};
+  for (size_t r = 0; r < x.size(); ++r) dp.p[r] = x[r];
+  sum_ranks_kernel<<<1, 256, 0, s>>>(dp, static_cast<int>(x.size()), count);
+  SC_CUDA_TRY(cudaGetLastError());
+  return SC_OK;
+}
+
+// halo rows of every held rank's buffer (row stride w floats; fp64 rows travel as 2 floats
+// per double, bit for bit)
+int halo_fill(const Ranks& R, const std::vector<float*>& T, int w, cudaStream_t s) {
+  if (R.world() == 1) return SC_OK;
+  if (R.nccl()) {
+    sc_dist* d = R.d[0];
+    SC_TRY(d->sendbuf.ensure(sizeof(float) * std::max<int64_t>(1, d->n_send) * w));
+    SC_TRY(exchange(d, T[0], w, s));
+    if (d->n_send || d->n_halo) SC_CUDA_TRY(cudaStreamWaitEvent(s, d->c->ev_comm, 0));
+    return SC_OK;
+  }
+  const int world = R.world();
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q) {
+      if (q == r) continue;
+      sc_dist* dr = R.d[r];
+      sc_dist* dq = R.d[q];
+      const int64_t cnt = dr->recv_counts[q];
+      if (cnt != dq->send_counts[r]) return fail(SC_ERR_ARG, "send / receive counts of two ranks disagree");
+      if (!cnt) continue;
+      pack_rows_kernel<<<dr->g->num_sms * 2, 256, 0, s>>>(T[q], dq->send_idx.as<int64_t>() + dq->send_off[r], cnt, w,
+                                                           T[r] + (dr->n_local + dr->recv_off[q]) * w);
+      SC_CUDA_TRY(cudaGetLastError());
+    }
+  return SC_OK;
+}
+
+int ranks_of(sc_dist* const* ds, int nheld, Ranks* R) {
+  SC_CHECK_ARG(ds && nheld >= 1, "null plans");
+  R->d.assign(ds, ds + nheld);
+  const int world = ds[0]->c->world;
+  if (nheld == 1) {
+    SC_CHECK_ARG(world == 1 || ds[0]->c->comm, "one held rank of a multi-rank partition needs an NCCL communicator");
+    return SC_OK;
+  }
+  SC_CHECK_ARG(nheld == world && world <= kP2PMaxWorld, "hold one rank or all ranks of the partition");
+  for (int r = 0; r < nheld; ++r)
+    SC_CHECK_ARG(ds[r] && ds[r]->c->world == world && ds[r]->c->rank == r, "plans must be ranks 0..world-1 in order");
+  return SC_OK;
+}
+
+// Lanczos (fp64) on the partition: theta = largest Ritz value of L after `iters` steps.  The
+// start vector of rank r's local row i is the counter generator's (seed, stream 0) entry
+// row0[r] + i.
+int dist_lanczos(const Ranks& R, int iters, uint64_t seed, const int64_t* row0, double* theta, cudaStream_t s) {
+  const int nh = static_cast<int>(R.d.size());
+  struct Buf { double *v, *vprev, *w, *tmp, *part, *alpha, *b2, *beta; };
+  std::vector<Buf> b(nh);
+  for (int r = 0; r < nh; ++r) {
+    sc_dist* d = R.d[r];
+    const size_t nc = (size_t)(d->n_local + d->n_halo), nl = (size_t)d->n_local;
+    SC_TRY(d->lz.ensure(sizeof(double) * (2 * nc + 2 * nl + lz::kDotBlocks + 3 * (size_t)(iters + 2))));
+    double* base = d->lz.as<double>();
+    b[r].v = base;
+    b[r].vprev = b[r].v + nc;
+    b[r].w = b[r].vprev + nc;
+    b[r].tmp = b[r].w + nl;
+    b[r].part = b[r].tmp + nl;
+    b[r].alpha = b[r].part + lz::kDotBlocks;
+    b[r].b2 = b[r].alpha + (iters + 2);
+    b[r].beta = b[r].b2 + (iters + 2);
+    SC_CUDA_TRY(cudaMemsetAsync(b[r].v, 0, sizeof(double) * 2 * nc, s));
+  }
+  auto scal = [&](double* Buf::*field, int j) {
+    std::vector<double*> x(nh);
+    for (int r = 0; r < nh; ++r) x[r] = (b[r].*field) + j;
+    return x;
+  };
+  auto vecs = [&](double* Buf::*field) {
+    std::vector<float*> x(nh);
+    for (int r = 0; r < nh; ++r) x[r] = reinterpret_cast<float*>(b[r].*field);
+    return x;
+  };
+  // v_0 = r / ||r||
+  for (int r = 0; r < nh; ++r) {
+    sc_dist* d = R.d[r];
+    SC_TRY(random_signals<double>(d->n_local, 1, row0 ? row0[r] : 0, seed, 0, 1.0, b[r].tmp, s));
+    SC_TRY(lz::dot_local(b[r].tmp, b[r].tmp, d->n_local, b[r].part, b[r].b2, s));
+  }
+  SC_TRY(allreduce_sum(R, scal(&Buf::b2, 0), 1, s));
+  for (int r = 0; r < nh; ++r) {
+    SC_TRY(lz::scale_inv_sqrt(b[r].v, b[r].tmp, b[r].b2, nullptr, R.d[r]->n_local, s));
+    SC_CUDA_TRY(cudaMemsetAsync(b[r].beta, 0, sizeof(double), s));
+  }
+  for (int j = 0; j < iters; ++j) {
+    SC_TRY(halo_fill(R, vecs(&Buf::v), 2, s));
+    for (int r = 0; r < nh; ++r) {
+      SC_TRY(lz::spmv(R.d[r]->g, b[r].v, j ? b[r].vprev : nullptr, b[r].beta + j, b[r].w, s));
+      SC_TRY(lz::dot_local(b[r].w, b[r].v, R.d[r]->n_local, b[r].part, b[r].alpha + j, s));
+    }
+    SC_TRY(allreduce_sum(R, scal(&Buf::alpha, j), 1, s));
+    for (int r = 0; r < nh; ++r) {
+      SC_TRY(lz::axpy_neg(b[r].w, b[r].v, b[r].alpha + j, R.d[r]->n_local, s));
+      SC_TRY(lz::dot_local(b[r].w, b[r].w, R.d[r]->n_local, b[r].part, b[r].b2 + j + 1, s));
+    }
+    SC_TRY(allreduce_sum(R, scal(&Buf::b2, j + 1), 1, s));
+    for (int r = 0; r < nh; ++r) {
+      std::swap(b[r].vprev, b[r].v);
+      SC_TRY(lz::scale_inv_sqrt(b[r].v, b[r].w, b[r].b2 + j + 1, b[r].beta + j + 1, R.d[r]->n_local, s));
+    }
+  }
+  std::vector<double> ha(iters), hb(iters + 1);
+  SC_CUDA_TRY(cudaMemcpyAsync(ha.data(), b[0].alpha, sizeof(double) * iters, cudaMemcpyDeviceToHost, s));
+  SC_CUDA_TRY(cudaMemcpyAsync(hb.data(), b[0].beta, sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost, s));
+  SC_CUDA_TRY(cudaStreamSynchronize(s));
+  *theta = lz::theta_from(ha, hb);
+  return SC_OK;
+}
+
+// max over ranks of the local strengths (Gershgorin: lambda_N <= 2 max_i s_i)
+int dist_max_strength(const Ranks& R, double* out, cudaStream_t s) {
+  double m = 0.0;
+  for (sc_dist* d : R.d) m = std::max(m, d->g->max_strength);
+  if (R.nccl()) {
+    sc_dist* d = R.d[0];
+    SC_TRY(d->msums.ensure(sizeof(double)));
+    SC_CUDA_TRY(cudaMemcpyAsync(d->msums.ptr, &m, sizeof(double), cudaMemcpyHostToDevice, s));
+    SC_NCCL_TRY(ncclAllReduce(d->msums.ptr, d->msums.ptr, 1, ncclDouble, ncclMax, d->c->comm, s));
+    SC_CUDA_TRY(cudaMemcpyAsync(&m, d->msums.ptr, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  *out = m;
+  return SC_OK;
+}
+
+// dst[r][c] = c < cols_left ? src[r * lds + col0 + c] : 0   (fp64, w columns)
+__global__ void take_cols_d_kernel(const double* __restrict__ src, int64_t lds, int col0, int cols_left, int64_t n,
+                                   int w, double* __restrict__ dst) {
+  const int64_t total = n * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / w;
+    const int c = static_cast<int>(e - r * w);
+    dst[e] = c < cols_left ? src[r * lds + col0 + c] : 0.0;
+  }
+}
+
+// Chebyshev moments mu_0..mu_{2p} of the probes X (n_probe columns, N(0, 1/n_probe) entries
+// from the counter generator, stream 2, counters (row0[r] + i) * n_probe + q) on the partition;
+// the same identity as cheb_moments (sc_filter.cu) on the sums over all ranks
+int dist_moments(const Ranks& R, double lambda_max, int order, int np, uint64_t seed, const int64_t* row0,
+                 std::vector<double>& mu, cudaStream_t s) {
+  const int nh = static_cast<int>(R.d.size());
+  // fixed chunk plan, equal on every rank (the exchanges are collective): 16-double chunks
+  std::vector<int> chunks;
+  {
+    int rem = (np + 1) / 2;   // in 16-byte vectors of 2 doubles
+    const int set[] = {8, 6, 4, 3, 2, 1};
+    while (rem > 0) {
+      int v = 1;
+      for (int c : set)
+        if (c <= rem) { v = c; break; }
+      chunks.push_back(2 * v);
+      rem -= v;
+    }
+  }
+  int cwmax = 0;
+  for (int w : chunks) cwmax = std::max(cwmax, w);
+  const int max_grid = 148 * 32;
+  std::vector<double*> sums(nh);
+  for (int r = 0; r < nh; ++r) {
+    sc_dist* d = R.d[r];
+    const int64_t nc = d->n_local + d->n_halo;
+    SC_TRY(d->probes.ensure(sizeof(double) * std::max<int64_t>(1, d->n_local) * np));
+    SC_TRY(d->tA.ensure(sizeof(double) * nc * cwmax));
+    SC_TRY(d->tB.ensure(sizeof(double) * nc * cwmax));
+    SC_TRY(d->tC.ensure(sizeof(double) * nc * cwmax));
+    SC_TRY(d->mpart.ensure(sizeof(double) * 2 * max_grid * 3));
+    SC_TRY(d->msums.ensure(sizeof(double) * (size_t)order * 6));
+    SC_CUDA_TRY(cudaMemsetAsync(d->msums.ptr, 0, sizeof(double) * (size_t)order * 6, s));
+    if (d->n_local) SC_TRY(random_signals<double>(d->n_local, np, row0 ? row0[r] : 0, seed, 2, 1.0 / np,
+                                                  d->probes.as<double>(), s));
+    sums[r] = d->msums.as<double>();
+  }
+  std::vector<double> acc((size_t)order * 3, 0.0), h((size_t)order * 6);
+  int col0 = 0;
+  for (int w : chunks) {
+    std::vector<double*> A(nh), B(nh), C(nh);
+    for (int r = 0; r < nh; ++r) {
+      sc_dist* d = R.d[r];
+      A[r] = d->tA.as<double>();
+      B[r] = d->tB.as<double>();
+      C[r] = d->tC.as<double>();
+      SC_CUDA_TRY(cudaMemsetAsync(A[r], 0, sizeof(double) * (d->n_local + d->n_halo) * w, s));
+      if (d->n_local) {
+        take_cols_d_kernel<<<d->g->num_sms * 4, 256, 0, s>>>(d->probes.as<double>(), np, col0, np - col0, d->n_local,
+                                                             w, A[r]);
+        SC_CUDA_TRY(cudaGetLastError());
+      }
+      SC_CUDA_TRY(cudaMemsetAsync(sums[r], 0, sizeof(double) * (size_t)order * 6, s));
+    }
+    for (int st = 0; st < order; ++st) {
+      std::vector<float*> cur(nh);
+      for (int r = 0; r < nh; ++r) cur[r] = reinterpret_cast<float*>(st == 0 ? A[r] : ((st & 1) ? B[r] : C[r]));
+      SC_TRY(halo_fill(R, cur, 2 * w, s));
+      for (int r = 0; r < nh; ++r) {
+        sc_dist* d = R.d[r];
+        double* bufs[2] = {C[r], B[r]};   // T_j (j >= 1) in bufs[j & 1]
+        StepParams p{};
+        p.width = w;
+        p.total_width = w;
+        p.tcur = cur[r];
+        p.ld_cur = w;
+        p.tprev = st == 0 ? nullptr : (st == 1 ? (const void*)A[r] : (const void*)bufs[(st - 1) & 1]);
+        p.ld_prev = w;
+        p.tnext = st == order - 1 ? nullptr : (void*)bufs[(st + 1) & 1];
+        p.ld_next = w;
+        p.a = (st == 0 ? 2.0 : 4.0) / lambda_max;
+        p.b_cur = st == 0 ? -1.0 : -2.0;
+        p.b_prev = st == 0 ? 0.0 : -1.0;
+        const int64_t bounds[3] = {0, d->n_interior, d->n_local};
+        for (int part = 0; part < 2; ++part) {
+          if (bounds[part + 1] <= bounds[part]) continue;
+          p.row_begin = bounds[part];
+          p.row_end = bounds[part + 1];
+          p.part = d->mpart.as<double>() + (size_t)part * max_grid * 3;
+          int grid = 0;
+          SC_TRY(launch_moments_step(d->g, p, s, &grid));
+          if (grid > max_grid) return fail(SC_ERR_STATE, "moment partial buffer too small");
+          SC_TRY(reduce_moment_partials(p.part, grid, sums[r] + (size_t)st * 6 + 3 * part, s));
+        }
+      }
+    }
+    SC_TRY(allreduce_sum(R, sums, order * 6, s));
+    SC_CUDA_TRY(cudaMemcpyAsync(h.data(), sums[0], sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int st = 0; st < order; ++st)
+      for (int c = 0; c < 3; ++c) acc[(size_t)st * 3 + c] += h[(size_t)st * 6 + c] + h[(size_t)st * 6 + 3 + c];
+    col0 += w;
+  }
+  mu.assign((size_t)2 * order + 1, 0.0);
+  mu[0] = acc[0];
+  mu[1] = acc[1];
+  for (int st = 1; st < order; ++st) {
+    mu[2 * st] = 2.0 * acc[3 * st + 0] - mu[0];
+    mu[2 * st + 1] = 2.0 * acc[3 * st + 1] - mu[1];
+  }
+  mu[2 * order] = 2.0 * acc[3 * (order - 1) + 2] - mu[0];
+  return SC_OK;
+}
 }  // namespace
 }  // namespace sc
 
@@ -135,6 +418,16 @@ int sc_comm_init(const void* id, int world, int rank, sc_comm** out) {
     delete c;
     return fail(SC_ERR_CUDA, "stream/event creation failed");
   }
+  *out = c;
+  return SC_OK;
+}
+
+int sc_comm_local(int world, int rank, sc_comm** out) {
+  SC_CHECK_ARG(out && world >= 1 && world <= kP2PMaxWorld && rank >= 0 && rank < world, "bad arguments");
+  auto* c = new sc_comm();
+  c->world = world;
+  c->rank = rank;
+  cudaGetDevice(&c->device);
   *out = c;
   return SC_OK;
 }
@@ -184,12 +477,13 @@ int sc_dist_create(sc_graph* g, sc_comm* c, int64_t n_interior, const int64_t* s
   // The step kernels are persistent (grid = SMs x resident CTAs); leave a few SMs free so
   // that NCCL's send/recv kernels on the communication stream can run concurrently with
   // the interior step instead of queueing behind it.
-  if (c->world > 1) g->num_sms = std::max(1, g->num_sms - kNcclReservedSms);
+  if (c->world > 1 && c->comm) g->num_sms = std::max(1, g->num_sms - kNcclReservedSms);
   *out = d;
   return SC_OK;
 }
 
 int sc_dist_free(sc_dist* d) {
+  if (d && d->g && d->c && d->c->world > 1 && d->c->comm) d->g->num_sms += kNcclReservedSms;   // as before create
   delete d;
   return SC_OK;
 }
@@ -281,6 +575,43 @@ int sc_dist_filter_f32(sc_dist* d, const double* coeffs, int order, double lambd
   }
   SC_TRY(ys_.out(Y, cs));
   return SC_OK;
+}
+
+int sc_dist_lambda_max(sc_dist* const* ds, int nheld, int iters, double margin, uint64_t seed, const int64_t* row0,
+                       double* out, void* stream) {
+  SC_CHECK_ARG(out && iters >= 1 && margin >= 0.0, "bad arguments");
+  Ranks R;
+  SC_TRY(ranks_of(ds, nheld, &R));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double theta = 0.0, smax = 0.0;
+  SC_TRY(dist_lanczos(R, iters, seed, row0, &theta, s));
+  SC_TRY(dist_max_strength(R, &smax, s));
+  const double gersh = 2.0 * smax;
+  double b = (1.0 + margin) * theta;
+  if (!(b > 0.0) || b > gersh) b = gersh;
+  if (!(b > 0.0)) b = 1.0;
+  *out = b;
+  return SC_OK;
+}
+
+int sc_dist_cheb_moments(sc_dist* const* ds, int nheld, double lambda_max, int order, int n_probe, uint64_t seed,
+                         const int64_t* row0, double* moments, void* stream) {
+  SC_CHECK_ARG(moments && order >= 1 && n_probe >= 1 && lambda_max > 0.0, "bad arguments");
+  Ranks R;
+  SC_TRY(ranks_of(ds, nheld, &R));
+  std::vector<double> mu;
+  SC_TRY(dist_moments(R, lambda_max, order, n_probe, seed, row0, mu, static_cast<cudaStream_t>(stream)));
+  std::memcpy(moments, mu.data(), sizeof(double) * mu.size());
+  return SC_OK;
+}
+
+int sc_dist_estimate_lambda_k(sc_dist* const* ds, int nheld, int k, double lambda_max, int order, int jackson,
+                              int n_probe, uint64_t seed, const int64_t* row0, int max_iter, double rtol,
+                              double* lambda_k, double* count_k, void* stream) {
+  SC_CHECK_ARG(lambda_k && count_k && k >= 1 && max_iter >= 1 && rtol > 0.0, "bad arguments");
+  std::vector<double> mu((size_t)2 * order + 1);
+  SC_TRY(sc_dist_cheb_moments(ds, nheld, lambda_max, order, n_probe, seed, row0, mu.data(), stream));
+  return lambda_k_dichotomy(mu.data(), order, k, lambda_max, jackson != 0, max_iter, rtol, lambda_k, count_k);
 }
 
 }  // extern "C"

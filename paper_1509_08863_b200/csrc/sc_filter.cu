@@ -891,6 +891,16 @@ int launch_step(const sc_graph* g, const StepParams& p, cudaStream_t s) {
 template int launch_step<float>(const sc_graph*, const StepParams&, cudaStream_t);
 template int launch_step<double>(const sc_graph*, const StepParams&, cudaStream_t);
 
+int launch_moments_step(const sc_graph* g, const StepParams& p, cudaStream_t s, int* grid) {
+  return launch_step_impl<double>(g, p, s, true, grid);
+}
+
+int reduce_moment_partials(const double* part, int grid, double* out, cudaStream_t s) {
+  reduce_partials_kernel<<<1, 256, 0, s>>>(part, grid, out);
+  SC_CUDA_TRY(cudaGetLastError());
+  return SC_OK;
+}
+
 // ---------------------------------------------------------------------------
 // whole filter on device buffers
 // ---------------------------------------------------------------------------

@@ -283,6 +283,22 @@ int random_signals(int64_t n, int R, int64_t row0, uint64_t seed, int stream_id,
 
 // Lanczos
 int lanczos_lambda_max(sc_graph* g, int iters, uint64_t seed, double* theta, cudaStream_t s);
+// its building blocks (sc_linalg.cu), for the row-partitioned version (sc_dist.cu):
+// w = L v - beta_j vprev over g's rows (v has g->n_cols entries: local rows + halo)
+namespace lz {
+constexpr int kDotBlocks = 296;   // partials per dot product (part must hold this many)
+int spmv(const sc_graph* g, const double* v, const double* vprev, const double* beta_j, double* w, cudaStream_t s);
+int dot_local(const double* a, const double* b, int64_t n, double* part, double* out, cudaStream_t s);
+int axpy_neg(double* w, const double* v, const double* alpha, int64_t n, cudaStream_t s);
+int scale_inv_sqrt(double* out, const double* w, const double* b2, double* beta, int64_t n, cudaStream_t s);
+double theta_from(const std::vector<double>& alpha, const std::vector<double>& beta);
+}  // namespace lz
+
+// one fused step in MOMENTS mode (fp64, static tile schedule): per-CTA partial sums of
+// <T_s,T_s>, <T_{s+1},T_s>, <T_{s+1},T_{s+1}> into p.part[grid][3]; *grid = CTAs launched
+int launch_moments_step(const sc_graph* g, const StepParams& p, cudaStream_t s, int* grid);
+// out[0..2] = sum of the grid partials, fixed order
+int reduce_moment_partials(const double* part, int grid, double* out, cudaStream_t s);
 
 // host math (sc_host.cpp)
 void cheby_lowpass_coeffs(double lambda_c, double lambda_max, int order, bool jackson, double* out);

@@ -147,6 +147,39 @@ int dot(const double* a, const double* b, int64_t n, double* part, double* out, 
 
 }  // namespace
 
+// building blocks of the row-partitioned Lanczos (sc_dist.cu)
+namespace lz {
+int spmv(const sc_graph* g, const double* v, const double* vprev, const double* beta_j, double* w, cudaStream_t s) {
+  const float* val = g->unit_weights ? nullptr : g->values.as<float>();
+  lanczos_spmv<<<g->num_sms * 8, 256, 0, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(), val,
+                                                g->strength64.as<double>(), g->n_rows, v, vprev, beta_j, w);
+  SC_CUDA_TRY(cudaGetLastError());
+  return SC_OK;
+}
+int dot_local(const double* a, const double* b, int64_t n, double* part, double* out, cudaStream_t s) {
+  return dot(a, b, n, part, out, s);
+}
+int axpy_neg(double* w, const double* v, const double* alpha, int64_t n, cudaStream_t s) {
+  ::sc::axpy_neg<<<148 * 8, 256, 0, s>>>(w, v, alpha, n);
+  SC_CUDA_TRY(cudaGetLastError());
+  return SC_OK;
+}
+int scale_inv_sqrt(double* out, const double* w, const double* b2, double* beta, int64_t n, cudaStream_t s) {
+  ::sc::scale_inv_sqrt<<<148 * 8, 256, 0, s>>>(out, w, b2, beta, n);
+  SC_CUDA_TRY(cudaGetLastError());
+  return SC_OK;
+}
+double theta_from(const std::vector<double>& ha, const std::vector<double>& hb) {
+  const int iters = static_cast<int>(ha.size());
+  int m = iters;
+  for (int j = 1; j < iters; ++j) {
+    if (!(hb[j] > 1e-12 * (std::fabs(ha[j - 1]) + 1e-300))) { m = j; break; }
+  }
+  std::vector<double> a(ha.begin(), ha.begin() + m), b(hb.begin() + 1, hb.begin() + m);
+  return tridiag_max_eig(a, b);
+}
+}  // namespace lz
+
 int lanczos_lambda_max(sc_graph* g, int iters, uint64_t seed, double* theta, cudaStream_t s) {
   const int64_t n = g->n_rows;
   // workspace: 3 vectors + w + partials + scalars (alpha[iters], b2[iters+1], beta[iters+1])

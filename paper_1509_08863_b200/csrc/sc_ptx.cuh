@@ -98,6 +98,9 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t 
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16_nohint(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 // global -> shared bulk copy completing on `bar` (bytes and both addresses 16-byte multiples)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(

@@ -63,6 +63,11 @@ namespace {
 #ifndef SC_SELL_GATHER_L1
 #define SC_SELL_GATHER_L1 0   // gathers: 0 ld.global.nc, 1 ld.global.nc.L1::no_allocate, 2 ld.global.cg
 #endif
+#ifndef SC_SELL_SMEM_TARGET_KB
+#define SC_SELL_SMEM_TARGET_KB 80   // a plan's shared memory per CTA should stay at or below this:
+#endif                              // the rest of the SM's 228 KB is L1, which holds the gathers in
+                                    // flight (configs[3]: 16-column chunks 215 ms with 105 KB per
+                                    // CTA, 123 ms with 54 KB; profiles/r02_sell.md)
 #ifndef SC_SELL_SMEM_KB
 #define SC_SELL_SMEM_KB 113   // most shared memory per CTA (2 CTAs per SM); a plan takes only
 #endif                        // what its largest tile needs, the rest of the SM's 228 KB is L1
@@ -75,7 +80,7 @@ namespace {
 #endif
 constexpr int kNC = SC_SELL_NC;
 constexpr int kThreads = (kNC + 1) * 32;
-constexpr int kStages = SC_SELL_STAGES;
+constexpr int kStages = SC_SELL_STAGES;   // most stages a plan uses
 static_assert(kStages <= 4, "header holds at most 4 stages");
 
 struct SellTileMeta {
@@ -90,22 +95,27 @@ __host__ __device__ constexpr int sell_tile_rows(int vpr) { return kNC * (32 / v
 struct SellLayout {
   int cap;   // SELL entries per stage
   size_t meta_off, ord_off, idx_off, val_off, stage_bytes, dense_off, total;
-  __host__ __device__ SellLayout(int tr, int cap_, bool unit) {
+  // stages: CSR ring depth (2..kStages); dense: own / T_{s-1} / Y rows staged with cp.async
+  // during the gathers (else plain loads after the gather loop: less shared memory)
+  __host__ __device__ SellLayout(int tr, int cap_, bool unit, int stages, bool dense) {
     cap = cap_;
     meta_off = 0;
-    ord_off = (size_t)kNC * 8;
+    ord_off = (size_t)kNC * 16;
     idx_off = ord_off + (((size_t)tr * 2 + 15) & ~(size_t)15);
     val_off = idx_off + (size_t)cap * 4;
     stage_bytes = val_off + (unit ? 0 : (size_t)cap * 4);
     stage_bytes = (stage_bytes + 127) & ~(size_t)127;
-    dense_off = 256 + (size_t)kStages * stage_bytes;
-    total = dense_off + (size_t)kNC * 3 * 32 * 16;
+    dense_off = 256 + (size_t)stages * stage_bytes;
+    total = dense_off + (dense ? (size_t)kNC * 3 * 32 * 16 : 0);
   }
 };
 
 struct SellDev {
   const int64_t* tile_ptr;   // [ntiles + 1] first entry of each tile (multiple of 4)
-  const int2* meta;          // [ntiles * kNC] {offset in the tile, padded length} per slice
+  const int4* meta;          // [ntiles * kNC] per slice: {offset in the tile, padded length,
+                             //   hub mask (bit r: slice row r is a hub), first hub id}
+  const int32_t* hub_chunk_ptr;   // [n_hubs + 1] chunks of each hub row (split-row path)
+  const void* hubpart;            // [n_chunks][width] partial sums of the hub chunks (type T)
   const int32_t* idx;        // column indices (sentinel n_cols = the zero row)
   const float* val;          // weights (0 on padding), nullptr for unit weights
   const uint16_t* order;     // [ntiles * tr] degree-sorted row order inside each tile
@@ -252,15 +262,16 @@ template <int RPW, int NB, bool UNIT> struct Gather<double, RPW, NB, UNIT> {
 
 template <typename T, int VPR, int NB, bool UNIT>
 __global__ void __launch_bounds__(kThreads, SC_SELL_MIN_CTAS)
-cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int cap) {
+cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int cap, int cfg) {
   constexpr int W = Vec<T>::W;
   constexpr int SW = VPR;          // lanes per row (one 16-byte vector each)
   constexpr int RPW = 32 / SW;     // rows per warp = rows per slice
   constexpr int TR = sell_tile_rows(VPR);
-  constexpr int S = kStages;
+  const int S = cfg & 15;                  // CSR ring stages
+  const bool dense_stage = (cfg >> 4) & 1;  // cp.async staging of the dense rows
 
   extern __shared__ __align__(128) unsigned char smem[];
-  const SellLayout lay(TR, cap, UNIT);
+  const SellLayout lay(TR, cap, UNIT, S, dense_stage);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 4;
   SellTileMeta* meta = reinterpret_cast<SellTileMeta*>(smem + 64);
@@ -314,12 +325,12 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
         const int overflow = ncol > lay.cap;
         m.r0 = r0; m.r1 = r1; m.e0 = e0; m.overflow = overflow; m.tile = (int32_t)t;
         unsigned char* st = stages + (size_t)s * lay.stage_bytes;
-        uint32_t tx = (uint32_t)(kNC * 8) + (uint32_t)(TR * 2);
+        uint32_t tx = (uint32_t)(kNC * 16) + (uint32_t)(TR * 2);
         const bool cp_col = !overflow && ncol > 0;
         if (cp_col) tx += (uint32_t)(ncol * 4 * (UNIT ? 1 : 2));
         mbar_arrive_expect_tx(&full[s], tx);
         const uint64_t pol_stream = policy_evict_first();
-        bulk_g2s(st + lay.meta_off, sd.meta + t * kNC, (uint32_t)(kNC * 8), &full[s], pol_stream);
+        bulk_g2s(st + lay.meta_off, sd.meta + t * kNC, (uint32_t)(kNC * 16), &full[s], pol_stream);
         bulk_g2s(st + lay.ord_off, sd.order + t * TR, (uint32_t)(TR * 2), &full[s], pol_stream);
         if (cp_col) {
           bulk_g2s(st + lay.idx_off, sd.idx + e0, (uint32_t)(ncol * 4), &full[s], pol_stream);
@@ -358,18 +369,19 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
     // this warp's slice: one block of RPW consecutive degree ranks, the block index rotating
     // with the tile so every warp sees every degree class
     const int j = (warp + static_cast<int>(t % kNC)) % kNC;
-    const int2 mj = reinterpret_cast<const int2*>(st + lay.meta_off)[j];
+    const int4 mj = reinterpret_cast<const int4*>(st + lay.meta_off)[j];
     const uint16_t* ord = reinterpret_cast<const uint16_t*>(st + lay.ord_off);
     const int rank = j * RPW + sub;
     const bool valid = sub < RPW && rank < static_cast<int>(m.r1 - m.r0);
     const int32_t row = static_cast<int32_t>(m.r0) + (valid ? ord[rank] : 0);   // rows < 2^31
-    if (valid) {
-      // own row, T_{s-1} and Y rows land in shared memory while the gathers run; streaming
-      // operands carry an L2 evict-first policy so the gathered block T_s stays in L2
-      const uint64_t pol = policy_evict_first();
-      cp_async16(d_own, tcur + (int64_t)row * p.ld_cur + c, pol);
-      if (tprev) cp_async16(d_prv, tprev + (int64_t)row * p.ld_prev + c, pol);
-      if (p.y_mode == 2) cp_async16(d_y, y + (int64_t)row * p.ld_y + c, pol);
+    if (dense_stage && valid) {
+      // own row, T_{s-1} and Y rows land in shared memory while the gathers run.  No L2
+      // cache hint here: with one, ptxas 12.9 allocated the hint's 64-bit descriptor to an
+      // odd uniform register (desc[UR1]) in the unit-weight instantiations, which faults with
+      // cudaErrorIllegalInstruction (native_build.py now rejects such SASS)
+      cp_async16_nohint(d_own, tcur + (int64_t)row * p.ld_cur + c);
+      if (tprev) cp_async16_nohint(d_prv, tprev + (int64_t)row * p.ld_prev + c);
+      if (p.y_mode == 2) cp_async16_nohint(d_y, y + (int64_t)row * p.ld_y + c);
     }
     const int lsub = sub < RPW ? sub : 0;
     T acc[W];
@@ -382,17 +394,40 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
+    if (valid && ((mj.z >> sub) & 1)) {
+      // a hub row (degree above the plan's threshold): its slice entries are empty and its
+      // neighbour sum was split over warps by hub_chunk_kernel (launched just before, so
+      // griddepcontrol.wait covered it); add the chunk partials in chunk order
+      const int h = mj.w + __popc(static_cast<unsigned>(mj.z) & ((1u << sub) - 1u));
+      const int c0 = sd.hub_chunk_ptr[h], c1 = sd.hub_chunk_ptr[h + 1];
+      const T* hp = static_cast<const T*>(sd.hubpart) + c;
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc[w] = T(0);
+      for (int q = c0; q < c1; ++q) {
+        T v[W];
+        Vec<T>::ld(hp + (int64_t)q * p.width, v);
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[w] += v[w];
+      }
+    }
     if (valid) {
-      asm volatile("cp.async.wait_all;" ::: "memory");
       T own[W], prv[W], yv[W];
-      Vec<T>::ld(d_own, own);
-      if (tprev) Vec<T>::ld(d_prv, prv);
-      else {
+      if (dense_stage) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        Vec<T>::ld(d_own, own);
+        if (tprev) Vec<T>::ld(d_prv, prv);
+        if (p.y_mode == 2) Vec<T>::ld(d_y, yv);
+      } else {
+        const uint64_t pol = policy_evict_first();
+        Vec<T>::ldg(tcur + (int64_t)row * p.ld_cur + c, own);
+        if (tprev) Stream<T>::ld(tprev + (int64_t)row * p.ld_prev + c, prv, pol);
+        if (p.y_mode == 2) Stream<T>::ld(y + (int64_t)row * p.ld_y + c, yv, pol);
+      }
+      if (!tprev) {
 #pragma unroll
         for (int w = 0; w < W; ++w) prv[w] = T(0);
       }
-      if (p.y_mode == 2) Vec<T>::ld(d_y, yv);
-      else {
+      if (p.y_mode != 2) {
 #pragma unroll
         for (int w = 0; w < W; ++w) yv[w] = T(0);
       }
@@ -416,41 +451,109 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
 }
 
 // ---------------------------------------------------------------------------
+// Split rows (degree-adaptive traversal, north_star "chosen for the degree distribution";
+// PAPER.md l.147 cost O(m(|E| + N))): a row whose degree exceeds the plan's threshold would
+// pad its whole slice to its degree and be walked by one lane group (a straggler).  Its edges
+// are cut into chunks of kHubChunk; one warp sums a chunk (its RPW lane groups take every
+// RPW-th edge, then the groups are added in group order), the SELL kernel's epilogue adds the
+// row's chunk partials in chunk order -- deterministic, and a hub costs as many warps as it
+// has chunks.
+// ---------------------------------------------------------------------------
+constexpr int kHubChunk = 512;
+
+struct HubChunk {
+  int64_t e0;     // first edge (CSR position)
+  int32_t len;    // edges in the chunk
+  int32_t pad;
+};
+
+template <typename T, int VPR, bool UNIT>
+__global__ void __launch_bounds__(256)
+hub_chunk_kernel(const HubChunk* __restrict__ chunks, int n_chunks, const int32_t* __restrict__ col,
+                 const float* __restrict__ val, StepParams p, T* __restrict__ hubpart) {
+  constexpr int W = Vec<T>::W;
+  constexpr int SW = VPR;
+  constexpr int RPW = 32 / SW;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / SW, sl = lane % SW, c = sl * W;
+  const T* tcur = static_cast<const T*>(p.tcur);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < n_chunks; q += (gridDim.x * blockDim.x) >> 5) {
+    const HubChunk ch = chunks[q];
+    T acc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) acc[w] = T(0);
+    if (sub < RPW) {
+      for (int e = sub; e < ch.len; e += RPW) {
+        const int64_t k = col[ch.e0 + e];
+        T v[W];
+        Vec<T>::ldg(tcur + k * p.ld_cur + c, v);
+        const T wt = UNIT ? T(1) : static_cast<T>(val[ch.e0 + e]);
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[w] = UNIT ? acc[w] + v[w] : fma(wt, v[w], acc[w]);
+      }
+    }
+    // groups added in group order by the lanes of group 0
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      T tot = acc[w];
+      for (int g = 1; g < RPW; ++g) {
+        const T o = __shfl_sync(FULL, acc[w], sl + g * SW);
+        tot += o;
+      }
+      acc[w] = tot;
+    }
+    if (sub == 0) Vec<T>::st(hubpart + (int64_t)q * p.width + c, acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // SELL build
 // ---------------------------------------------------------------------------
 // padded length of every slice (max degree of its rows rounded up to 4) and entries per tile
+// (rows of degree > hub_deg are hubs: no slice entries, split-row path)
 __global__ void sell_len_kernel(const int64_t* __restrict__ row_ptr, int64_t row_begin, int64_t row_end, int tr,
-                                int rpw, const uint16_t* __restrict__ order, int32_t* __restrict__ slice_len,
-                                int64_t* __restrict__ tile_entries) {
+                                int rpw, const uint16_t* __restrict__ order, int64_t hub_deg,
+                                int32_t* __restrict__ slice_len, int64_t* __restrict__ tile_entries,
+                                int32_t* __restrict__ tile_hubs) {
   const int64_t t = blockIdx.x;
   const int64_t r0 = row_begin + t * tr;
   const int cnt = static_cast<int>(min((int64_t)tr, row_end - r0));
-  __shared__ int len[64];
+  __shared__ int len[64], hubs[64];
   for (int j = threadIdx.x; j < kNC; j += blockDim.x) {
-    int maxd = 0;
+    int maxd = 0, nh = 0;
     for (int q = 0; q < rpw; ++q) {
       const int rank = j * rpw + q;
       if (rank < cnt) {
         const int64_t row = r0 + order[t * tr + rank];
-        maxd = max(maxd, static_cast<int>(row_ptr[row + 1] - row_ptr[row]));
+        const int64_t d = row_ptr[row + 1] - row_ptr[row];
+        if (d > hub_deg) ++nh;
+        else maxd = max(maxd, static_cast<int>(d));
       }
     }
     len[j] = (maxd + 3) & ~3;
+    hubs[j] = nh;
     slice_len[t * kNC + j] = len[j];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     int64_t tot = 0;
-    for (int j = 0; j < kNC; ++j) tot += (int64_t)len[j] * rpw;
+    int nh = 0;
+    for (int j = 0; j < kNC; ++j) {
+      tot += (int64_t)len[j] * rpw;
+      nh += hubs[j];
+    }
     tile_entries[t] = tot;
+    tile_hubs[t] = nh;
   }
 }
 
 __global__ void sell_fill_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                                  const float* __restrict__ val, int64_t row_begin, int64_t row_end, int tr, int rpw,
                                  const uint16_t* __restrict__ order, const int32_t* __restrict__ slice_len,
-                                 const int64_t* __restrict__ tile_ptr, int32_t sentinel, int2* __restrict__ meta,
-                                 int32_t* __restrict__ idx, float* __restrict__ sval) {
+                                 const int64_t* __restrict__ tile_ptr, int32_t sentinel, int64_t hub_deg,
+                                 const int32_t* __restrict__ tile_hub_base, int4* __restrict__ meta,
+                                 int32_t* __restrict__ idx, float* __restrict__ sval, int32_t* __restrict__ hub_rows) {
   const int64_t t = blockIdx.x;
   const int64_t r0 = row_begin + t * tr;
   const int cnt = static_cast<int>(min((int64_t)tr, row_end - r0));
@@ -465,18 +568,37 @@ __global__ void sell_fill_kernel(const int64_t* __restrict__ row_ptr, const int3
     }
     off[kNC] = o;
   }
+  __shared__ int hub[1024];
   for (int r = threadIdx.x; r < tr; r += blockDim.x) {
     if (r < cnt) {
       const int64_t row = r0 + order[t * tr + r];
       rb[r] = row_ptr[row];
-      deg[r] = static_cast<int>(row_ptr[row + 1] - rb[r]);
+      const int64_t d = row_ptr[row + 1] - rb[r];
+      hub[r] = d > hub_deg;
+      deg[r] = hub[r] ? 0 : static_cast<int>(d);
     } else {
       rb[r] = 0;
       deg[r] = 0;
+      hub[r] = 0;
     }
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < kNC; j += blockDim.x) meta[t * kNC + j] = make_int2(off[j], slice_len[t * kNC + j]);
+  if (threadIdx.x == 0) {
+    // hub ids in (tile, slice, slice row) order
+    int h = tile_hub_base[t];
+    for (int j = 0; j < kNC; ++j) {
+      int mask = 0;
+      const int base = h;
+      for (int q = 0; q < rpw; ++q) {
+        const int rank = j * rpw + q;
+        if (rank < cnt && hub[rank]) {
+          mask |= 1 << q;
+          hub_rows[h++] = static_cast<int32_t>(r0 - row_begin + order[t * tr + rank]);
+        }
+      }
+      meta[t * kNC + j] = make_int4(off[j], slice_len[t * kNC + j], mask, base);
+    }
+  }
   const int64_t base = tile_ptr[t];
   const int total = off[kNC];
   for (int q = threadIdx.x; q < total; q += blockDim.x) {
@@ -498,7 +620,27 @@ struct SellPlan {
   int64_t ntiles = 0, entries = 0, max_tile = 0;
   DevBuf tile_ptr, meta, idx, val;
   const uint16_t* order = nullptr;
+  // split rows
+  int64_t hub_deg = 0;
+  int n_hubs = 0, n_chunks = 0;
+  DevBuf hub_rows, hub_chunk_ptr, chunks, hubpart;
 };
+
+// split-row threshold: a row of degree > this is cut into chunks (env SC_SELL_HUB_DEG)
+int64_t hub_threshold() {
+  const char* v = std::getenv("SC_SELL_HUB_DEG");
+  return v ? std::atoll(v) : 512;
+}
+
+// hub rows' CSR ranges (device) -> host
+__global__ void hub_range_kernel(const int64_t* __restrict__ row_ptr, int64_t row_begin, const int32_t* __restrict__ rows,
+                                 int n, int64_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int64_t r = row_begin + rows[i];
+    out[2 * i] = row_ptr[r];
+    out[2 * i + 1] = row_ptr[r + 1];
+  }
+}
 
 std::mutex g_sell_mu;
 std::map<std::tuple<const sc_graph*, int, int64_t, int64_t>, std::unique_ptr<SellPlan>> g_sell_plans;
@@ -524,45 +666,102 @@ int sell_plan(const sc_graph* g, int vpr, int64_t row_begin, int64_t row_end, cu
   pl->order = tile_order(g, tr, row_begin, row_end, s);
   if (!pl->order) return fail(SC_ERR_NOMEM, "tile order allocation failed");
   const int64_t nt = pl->ntiles;
-  DevBuf slen, tent;
+  pl->hub_deg = hub_threshold();
+  DevBuf slen, tent, thub;
   SC_TRY(slen.ensure(sizeof(int32_t) * std::max<int64_t>(1, nt * kNC)));
   SC_TRY(tent.ensure(sizeof(int64_t) * std::max<int64_t>(1, nt)));
+  SC_TRY(thub.ensure(sizeof(int32_t) * std::max<int64_t>(1, nt)));
   if (nt > 0) {
     sell_len_kernel<<<(unsigned)nt, 64, 0, s>>>(g->row_ptr.as<int64_t>(), row_begin, row_end, tr, rpw, pl->order,
-                                                slen.as<int32_t>(), tent.as<int64_t>());
+                                                pl->hub_deg, slen.as<int32_t>(), tent.as<int64_t>(),
+                                                thub.as<int32_t>());
     SC_CUDA_TRY(cudaGetLastError());
   }
   std::vector<int64_t> h(nt), ptr(nt + 1, 0);
+  std::vector<int32_t> th(nt), thb(nt + 1, 0);
   if (nt > 0) {
     SC_CUDA_TRY(cudaMemcpyAsync(h.data(), tent.ptr, sizeof(int64_t) * nt, cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaMemcpyAsync(th.data(), thub.ptr, sizeof(int32_t) * nt, cudaMemcpyDeviceToHost, s));
     SC_CUDA_TRY(cudaStreamSynchronize(s));
   }
   for (int64_t t = 0; t < nt; ++t) {
     ptr[t + 1] = ptr[t] + h[t];
     pl->max_tile = std::max(pl->max_tile, h[t]);
+    thb[t + 1] = thb[t] + th[t];
   }
+  pl->n_hubs = thb[nt];
+  SC_TRY(pl->hub_rows.ensure(sizeof(int32_t) * std::max(1, pl->n_hubs)));
+  DevBuf thbase;
+  SC_TRY(thbase.ensure(sizeof(int32_t) * (nt + 1)));
+  SC_CUDA_TRY(cudaMemcpyAsync(thbase.ptr, thb.data(), sizeof(int32_t) * (nt + 1), cudaMemcpyHostToDevice, s));
   pl->entries = ptr[nt];
   SC_TRY(pl->tile_ptr.ensure(sizeof(int64_t) * (nt + 1)));
   SC_CUDA_TRY(cudaMemcpyAsync(pl->tile_ptr.ptr, ptr.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, s));
-  SC_TRY(pl->meta.ensure(sizeof(int2) * std::max<int64_t>(1, nt * kNC)));
+  SC_TRY(pl->meta.ensure(sizeof(int4) * std::max<int64_t>(1, nt * kNC)));
   SC_TRY(pl->idx.ensure(sizeof(int32_t) * std::max<int64_t>(4, pl->entries)));
   if (!g->unit_weights) SC_TRY(pl->val.ensure(sizeof(float) * std::max<int64_t>(4, pl->entries)));
   if (nt > 0) {
     sell_fill_kernel<<<(unsigned)nt, 256, 0, s>>>(
         g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(), g->unit_weights ? nullptr : g->values.as<float>(),
         row_begin, row_end, tr, rpw, pl->order, slen.as<int32_t>(), pl->tile_ptr.as<int64_t>(),
-        static_cast<int32_t>(g->n_cols), pl->meta.as<int2>(), pl->idx.as<int32_t>(),
-        g->unit_weights ? nullptr : pl->val.as<float>());
+        static_cast<int32_t>(g->n_cols), pl->hub_deg, thbase.as<int32_t>(), pl->meta.as<int4>(),
+        pl->idx.as<int32_t>(), g->unit_weights ? nullptr : pl->val.as<float>(), pl->hub_rows.as<int32_t>());
     SC_CUDA_TRY(cudaGetLastError());
   }
-  SC_CUDA_TRY(cudaStreamSynchronize(s));   // slen / tent are freed on return
+  // split rows: chunks of kHubChunk edges per hub, in hub order
+  std::vector<int32_t> cptr(pl->n_hubs + 1, 0);
+  if (pl->n_hubs > 0) {
+    DevBuf rng;
+    SC_TRY(rng.ensure(sizeof(int64_t) * 2 * pl->n_hubs));
+    hub_range_kernel<<<std::min(1024, (pl->n_hubs + 255) / 256), 256, 0, s>>>(
+        g->row_ptr.as<int64_t>(), row_begin, pl->hub_rows.as<int32_t>(), pl->n_hubs, rng.as<int64_t>());
+    SC_CUDA_TRY(cudaGetLastError());
+    std::vector<int64_t> hr(2 * (size_t)pl->n_hubs);
+    SC_CUDA_TRY(cudaMemcpyAsync(hr.data(), rng.ptr, sizeof(int64_t) * hr.size(), cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<HubChunk> ch;
+    for (int hI = 0; hI < pl->n_hubs; ++hI) {
+      for (int64_t e = hr[2 * hI]; e < hr[2 * hI + 1]; e += kHubChunk)
+        ch.push_back(HubChunk{e, (int32_t)std::min<int64_t>(kHubChunk, hr[2 * hI + 1] - e), 0});
+      cptr[hI + 1] = (int32_t)ch.size();
+    }
+    pl->n_chunks = (int)ch.size();
+    SC_TRY(pl->chunks.ensure(sizeof(HubChunk) * std::max<size_t>(1, ch.size())));
+    SC_CUDA_TRY(cudaMemcpyAsync(pl->chunks.ptr, ch.data(), sizeof(HubChunk) * ch.size(), cudaMemcpyHostToDevice, s));
+  }
+  SC_TRY(pl->hub_chunk_ptr.ensure(sizeof(int32_t) * (pl->n_hubs + 1)));
+  SC_CUDA_TRY(cudaMemcpyAsync(pl->hub_chunk_ptr.ptr, cptr.data(), sizeof(int32_t) * (pl->n_hubs + 1),
+                              cudaMemcpyHostToDevice, s));
+  SC_CUDA_TRY(cudaStreamSynchronize(s));   // build temporaries are freed on return
   *out = pl.get();
   g_sell_plans[key] = std::move(pl);
   return SC_OK;
 }
 
 template <typename T>
-using SellFn = void (*)(SellDev, const T*, StepParams, int);
+using SellFn = void (*)(SellDev, const T*, StepParams, int, int);
+template <typename T>
+using HubFn = void (*)(const HubChunk*, int, const int32_t*, const float*, StepParams, T*);
+
+template <typename T, int VPR>
+HubFn<T> pick_hub_unit(bool unit) {
+  return unit ? hub_chunk_kernel<T, VPR, true> : hub_chunk_kernel<T, VPR, false>;
+}
+template <typename T>
+HubFn<T> pick_hub(int vpr, bool unit) {
+  switch (vpr) {
+    case 1: return pick_hub_unit<T, 1>(unit);
+    case 2: return pick_hub_unit<T, 2>(unit);
+    case 3: return pick_hub_unit<T, 3>(unit);
+    case 4: return pick_hub_unit<T, 4>(unit);
+    case 6: return pick_hub_unit<T, 6>(unit);
+    case 8: return pick_hub_unit<T, 8>(unit);
+    case 12: return pick_hub_unit<T, 12>(unit);
+    case 16: return pick_hub_unit<T, 16>(unit);
+    case 24: return pick_hub_unit<T, 24>(unit);
+    default: return pick_hub_unit<T, 32>(unit);
+  }
+}
 
 template <typename T, int VPR>
 SellFn<T> pick_sell_unit(bool unit) {
@@ -592,22 +791,42 @@ SellFn<T> pick_sell(int vpr, bool unit) {
   }
 }
 
-// stage capacity (SELL entries) for a plan: its largest tile rounded up to 64 entries, so
-// the CTA takes no more shared memory than it needs (the rest of the SM's 228 KB is L1,
-// which holds the gathers in flight); 0 if that does not fit SC_SELL_SMEM_KB
-int sell_cap(int tr, bool unit, int64_t max_tile) {
-  const int per_entry = unit ? 4 : 8;
+// Launch configuration of a plan: stage capacity = its largest tile rounded up to 64
+// entries; then the deepest CSR ring and the cp.async staging of the dense rows, in this order
+// of preference, that keep the CTA at or below SC_SELL_SMEM_TARGET_KB (the rest of the SM's
+// shared memory / L1 carve-out is L1, which holds the gathers in flight), else the smallest
+// footprint; cap = 0 when even that exceeds SC_SELL_SMEM_KB.
+struct SellCfg {
+  int cap = 0, stages = 0;
+  bool dense = false;
+  size_t smem = 0;
+  int packed() const { return stages | (dense ? 16 : 0); }
+};
+SellCfg sell_config(int tr, bool unit, int64_t max_tile) {
+  SellCfg c;
   const int64_t cap = std::max<int64_t>(64, (max_tile + 63) & ~int64_t(63));
-  const SellLayout lay(tr, (int)std::min<int64_t>(cap, INT_MAX / 8), unit);
-  return lay.total <= (size_t)SC_SELL_SMEM_KB * 1024 && cap * per_entry < INT_MAX / 4 ? (int)cap : 0;
+  if (cap > (int64_t)1 << 24) return c;
+  const size_t target = (size_t)env_int_s("SC_SELL_SMEM_TARGET_KB", SC_SELL_SMEM_TARGET_KB) * 1024;
+  const int forced_st = env_int_s("SC_SELL_FORCE_STAGES", 0), forced_dense = env_int_s("SC_SELL_FORCE_DENSE", -1);
+  const struct { int st; bool dense; } order[] = {{3, true}, {2, true}, {3, false}, {2, false}};
+  for (const auto& o : order) {
+    if (o.st > kStages) continue;
+    if (forced_st && o.st != forced_st) continue;
+    if (forced_dense >= 0 && o.dense != (forced_dense != 0)) continue;
+    const SellLayout lay(tr, (int)cap, unit, o.st, o.dense);
+    if (lay.total > (size_t)SC_SELL_SMEM_KB * 1024) continue;
+    c.cap = (int)cap;
+    c.stages = o.st;
+    c.dense = o.dense;
+    c.smem = lay.total;
+    if (lay.total <= target) break;   // first that meets the target; else keep the smallest
+  }
+  return c;
 }
 
 }  // namespace
 
-bool sell_enabled() {
-  static const bool v = env_int_s("SC_SELL", 1) != 0;
-  return v;
-}
+bool sell_enabled() { return env_int_s("SC_SELL", 1) != 0; }   // read per call (tests switch it)
 
 void sell_release(const sc_graph* g) {
   std::lock_guard<std::mutex> lock(g_sell_mu);
@@ -629,7 +848,7 @@ int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end
   if ((sell_tile_rows(vpr) * 2) % 16) return SC_OK;   // the tile's order segment must be a 16-byte bulk copy
   SellPlan* pl = nullptr;
   SC_TRY(sell_plan(g, vpr, row_begin, row_end, s, &pl));
-  *ok = sell_cap(sell_tile_rows(vpr), g->unit_weights, pl->max_tile) > 0;
+  *ok = sell_config(sell_tile_rows(vpr), g->unit_weights, pl->max_tile).cap > 0;
   return SC_OK;
 }
 template int sell_usable<float>(const sc_graph*, int, int64_t, int64_t, cudaStream_t, bool*);
@@ -647,10 +866,10 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
   const int tr = sell_tile_rows(vpr);
   SellPlan* pl = nullptr;
   SC_TRY(sell_plan(g, vpr, p.row_begin, p.row_end, s, &pl));
-  const int cap = sell_cap(tr, g->unit_weights, pl->max_tile);
-  if (cap <= 0) return fail(SC_ERR_STATE, "SELL tile exceeds the stage capacity");
-  const SellLayout lay(tr, cap, g->unit_weights);
-  const int smem = static_cast<int>(lay.total);
+  const SellCfg cf = sell_config(tr, g->unit_weights, pl->max_tile);
+  if (cf.cap <= 0) return fail(SC_ERR_STATE, "SELL tile exceeds the stage capacity");
+  const int cap = cf.cap;
+  const int smem = static_cast<int>(cf.smem);
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> occ_cache;
   int occ = 0;
@@ -668,8 +887,23 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
   const int64_t rows = p.row_end - p.row_begin;
   if (rows <= 0) return SC_OK;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(pl->ntiles, (int64_t)g->num_sms * occ)));
-  SellDev sd{pl->tile_ptr.as<int64_t>(), pl->meta.as<int2>(), pl->idx.as<int32_t>(),
-             g->unit_weights ? nullptr : pl->val.as<float>(), pl->order};
+  SellDev sd{};
+  sd.tile_ptr = pl->tile_ptr.as<int64_t>();
+  sd.meta = pl->meta.as<int4>();
+  sd.idx = pl->idx.as<int32_t>();
+  sd.val = g->unit_weights ? nullptr : pl->val.as<float>();
+  sd.order = pl->order;
+  sd.hub_chunk_ptr = pl->hub_chunk_ptr.as<int32_t>();
+  if (pl->n_chunks > 0) {
+    // split rows first: one warp per chunk of a hub row's edges -> hubpart
+    SC_TRY(pl->hubpart.ensure(sizeof(T) * (size_t)pl->n_chunks * p.width));
+    sd.hubpart = pl->hubpart.ptr;
+    HubFn<T> hk = pick_hub<T>(vpr, g->unit_weights);
+    const int hgrid = (int)std::min<int64_t>((pl->n_chunks + 7) / 8, (int64_t)g->num_sms * 8);
+    hk<<<hgrid, 256, 0, s>>>(pl->chunks.as<HubChunk>(), pl->n_chunks, g->col_idx.as<int32_t>(),
+                             g->unit_weights ? nullptr : g->values.as<float>(), p, static_cast<T*>(pl->hubpart.ptr));
+    SC_CUDA_TRY(cudaGetLastError());
+  }
   const T* strength = sizeof(T) == 4 ? reinterpret_cast<const T*>(g->strength32.ptr)
                                      : reinterpret_cast<const T*>(g->strength64.ptr);
   cudaLaunchConfig_t cfg{};
@@ -682,7 +916,7 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  SC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, sd, strength, p, cap));
+  SC_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, sd, strength, p, cap, cf.packed()));
   if (algo_bytes) {
     // algorithmic bytes of the step: the CSR share of this chunk (row
     // pointers + column indices [+ weights], not the padding) + dense operands touched once

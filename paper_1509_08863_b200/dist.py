@@ -304,9 +304,19 @@ class NcclFilter:
         self.plan = _lib.sc_dist_create(graph_handle, self.comm, part.n_interior, part.send_idx,
                                         np.asarray(part.send_counts, dtype=np.int64),
                                         np.asarray(part.recv_counts, dtype=np.int64))
+        self.r0 = int(part.r0)   # counter offset of the rank's rows (start vector, probes)
 
     def filter(self, d, order: int, lambda_max: float, X, Y):
         self._lib.sc_dist_filter_f32(self.plan, d, order, lambda_max, X.shape[1], X, Y)
+
+    # PAPER.md §4.1 steps 1-2 on the partition (sc_dist_lambda_max / sc_dist_estimate_lambda_k):
+    # halo exchange before every SpMV, inner products all-reduced; collective over the ranks
+    def lambda_max(self, iters=60, margin=0.01, seed=0) -> float:
+        return self._lib.sc_dist_lambda_max(self.plan, iters, margin, seed, [self.r0])
+
+    def estimate_lambda_k(self, k, lambda_max, order, jackson=True, n_probe=32, seed=0, max_iter=40, rtol=1e-4):
+        return self._lib.sc_dist_estimate_lambda_k(self.plan, k, lambda_max, order, jackson, n_probe, seed,
+                                                   [self.r0], max_iter, rtol)
 
     def close(self):
         if getattr(self, "plan", None):

@@ -57,6 +57,11 @@ WORKLOADS = {
     "x_sbm1m_eps005": Workload("x_sbm1m_eps005", 1_000_000, 100, 64, 200, False,
                                dict(kind="sbm", n=1_000_000, k=100, avg_degree=20, eps=0.005,
                                     sizes="powerlaw", exponent=2.0, min_size=1000)),
+    # Power-law degrees (Chung-Lu, exponent 2.1, mean degree 20, N=10^6): the degree-adaptive
+    # traversal's bench graph (north_star "chosen for the degree
+    # distribution"); same R, p as configs[3].
+    "x_chunglu1m": Workload("x_chunglu1m", 1_000_000, 100, 64, 200, False,
+                            dict(kind="chung_lu", n=1_000_000, avg_degree=21.2, exponent=2.1)),   # realised mean ~20
 }
 
 ORDER = ["c0_sbm2k", "c1_gmm20k", "c2_sbm100k", "c3_sbm1m", "c4_sbm10m"]
@@ -90,6 +95,8 @@ def build_graph(name: str, seed: int = 1234, cache: bool = False) -> graphs.CSRG
         g = graphs.sbm(seed=seed, **spec)
     elif kind == "gmm_knn":
         g = graphs.gmm_knn(seed=seed, **spec)
+    elif kind == "chung_lu":
+        g = graphs.chung_lu(seed=seed, **spec)
     else:
         raise ValueError(kind)
     return graphs.rcm_order(g) if rcm else g

@@ -209,6 +209,40 @@ def sbm(n: int, k: int, avg_degree: float, eps: float, sizes: str = "equal",
     return g
 
 
+def chung_lu(n: int, avg_degree: float, exponent: float, seed: int = 0, max_degree: int | None = None) -> CSRGraph:
+    """Power-law-degree graph (Chung-Lu): node i has expected degree w_i proportional to
+    (i + i0)^(-1/(exponent - 1)), scaled to mean ``avg_degree`` (w_0 capped at ``max_degree``,
+    default sqrt(n) * avg_degree); the m = n * avg_degree / 2 edges join endpoints drawn
+    independently with probability w / sum(w), self loops dropped and duplicates merged (so
+    realised degrees of the largest hubs fall a little short of w).  Node ids are shuffled so
+    hubs are spread over the tiles.  Unit weights.  (North_star: the traversal must cope
+    with the degree distribution.)"""
+    rng = np.random.default_rng(np.random.PCG64(seed))
+    beta = 1.0 / (exponent - 1.0)
+    i = np.arange(n, dtype=np.float64)
+    w = (i + 1.0) ** (-beta)
+    w *= avg_degree * n / w.sum()
+    cap = float(max_degree if max_degree is not None else np.sqrt(n) * avg_degree)
+    for _ in range(20):                      # cap the largest weights, keep the mean
+        over = w > cap
+        if not over.any():
+            break
+        w[over] = cap
+        w *= avg_degree * n / w.sum()
+    p = w / w.sum()
+    m = int(round(n * avg_degree / 2.0))
+    cdf = np.cumsum(p)
+    a = np.searchsorted(cdf, rng.random(m) * cdf[-1], side="right")
+    b = np.searchsorted(cdf, rng.random(m) * cdf[-1], side="right")
+    a = np.minimum(a, n - 1)
+    b = np.minimum(b, n - 1)
+    keep = a != b
+    perm = rng.permutation(n)
+    g = from_edges(n, perm[a[keep]], perm[b[keep]], None,
+                   meta=dict(kind="chung_lu", avg_degree=avg_degree, exponent=exponent, seed=seed))
+    return g
+
+
 # ----------------------------------------------------------------------------
 # Gaussian-mixture kNN graph (PAPER.md §5; BASELINE.json config 1)
 # ----------------------------------------------------------------------------

@@ -136,15 +136,28 @@ CASES = [
         40001, np.concatenate([np.zeros(40000, np.int64), np.arange(1, 40000)]),
         np.concatenate([np.arange(1, 40001), np.arange(2, 40001)]), None), 16, 12, False, 0.3),
     ("path_tiny", lambda: scinputs.path(2), 4, 5, False, 0.5),
+    # power-law degrees (Chung-Lu, exponent 2.1): hundreds of rows above the split threshold
+    ("chung_lu", lambda: scinputs.chung_lu(30000, 20, 2.1, seed=3), 16, 30, True, 0.1),
 ]
 
+# streaming paths: "streaming" = the SELL kernel (large graphs' default; rows above the split
+# threshold of 512 go through hub_chunk_kernel), "split" = SELL with every row of degree > 4
+# split, "csr" = the plain-CSR step kernel (SC_SELL=0; moments and partitioned paths)
+PATHS = {"resident": {"SC_RESIDENT": "1"}, "streaming": {"SC_RESIDENT": "0"},
+         "split": {"SC_RESIDENT": "0", "SC_SELL_HUB_DEG": "4"}, "csr": {"SC_RESIDENT": "0", "SC_SELL": "0"}}
 
-@pytest.mark.parametrize("path", ["resident", "streaming"])
+
+def _path_env(monkeypatch, path):
+    for k, v in PATHS[path].items():
+        monkeypatch.setenv(k, v)
+
+
+@pytest.mark.parametrize("path", list(PATHS))
 @pytest.mark.parametrize("name,maker,R,order,jackson,ratio", CASES, ids=[c[0] for c in CASES])
 def test_filter_f32_parity(sc, name, maker, R, order, jackson, ratio, path, monkeypatch):
     # small graphs take the resident-CSR cooperative kernel by default; SC_RESIDENT=0 forces
-    # the streaming per-step kernel on the same inputs
-    monkeypatch.setenv("SC_RESIDENT", "1" if path == "resident" else "0")
+    # the streaming per-step kernels on the same inputs
+    _path_env(monkeypatch, path)
     g = maker()
     L = laplacian.laplacian(g)
     lmax = 2.0 * float(laplacian.strengths(laplacian.adjacency(g)).max())
@@ -154,10 +167,13 @@ def test_filter_f32_parity(sc, name, maker, R, order, jackson, ratio, path, monk
     assert rel(Y, Yo) <= F32_TOL
 
 
-@pytest.mark.parametrize("path", ["resident", "streaming"])
-@pytest.mark.parametrize("name,maker,R,order,jackson,ratio", CASES[:6], ids=[c[0] for c in CASES[:6]])
+F64_CASES = CASES[:6] + [c for c in CASES if c[0] in ("star_hub", "chung_lu")]
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+@pytest.mark.parametrize("name,maker,R,order,jackson,ratio", F64_CASES, ids=[c[0] for c in F64_CASES])
 def test_filter_f64_parity(sc, name, maker, R, order, jackson, ratio, path, monkeypatch):
-    monkeypatch.setenv("SC_RESIDENT", "1" if path == "resident" else "0")
+    _path_env(monkeypatch, path)
     g = maker()
     L = laplacian.laplacian(g)
     lmax = 2.0 * float(laplacian.strengths(laplacian.adjacency(g)).max())
@@ -691,6 +707,62 @@ def test_row_partitioned_steps_emulated_two_ranks(sc):
     assert rel(Yfull, Yo) <= F32_TOL
 
 
+def _dist_group(sc, g, world):
+    """All `world` ranks' partition plans held by this process (sc_comm_local: the library's
+    single-process emulation -- halo rows copied between the ranks' buffers, sums in rank
+    order)."""
+    from paper_1509_08863_b200 import dist as pdist
+    parts = [pdist.local_part(g.row_ptr, g.col_idx, g.values, g.n, r, world) for r in range(world)]
+    halos = [p.halo_gid for p in parts]
+    for p in parts:
+        pdist.send_lists_from_halos(p, halos)
+    Gs = [sc.Graph(p.n_local, p.row_ptr, p.col_idx, p.values, n_cols=p.n_local + p.n_halo) for p in parts]
+    comms = [sc.sc_comm_local(world, r) for r in range(world)]
+    plans = [sc.sc_dist_create(G.handle, c, p.n_interior, p.send_idx, np.asarray(p.send_counts, np.int64),
+                               np.asarray(p.recv_counts, np.int64)) for G, c, p in zip(Gs, comms, parts)]
+    return parts, Gs, comms, plans
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_partitioned_lambda_estimates_emulated(sc, world):
+    """PAPER.md §4.1 steps 1-2 on a row-partitioned graph (sc_dist_lambda_max,
+    sc_dist_cheb_moments, sc_dist_estimate_lambda_k): lambda^_N is a tight upper bound of the
+    exact lambda_N; the eigencounts of the moments and the dichotomy's lambda~_k match the
+    oracle on the probes the ranks drew (assembled in global row order)."""
+    g = scinputs.sbm(2000, 5, 10, 0.1, seed=1234)
+    parts, Gs, comms, plans = _dist_group(sc, g, world)
+    try:
+        if world > 1:
+            assert all(p.n_halo > 0 for p in parts)
+        row0 = [p.r0 for p in parts]
+        L = laplacian.laplacian(g)
+        lN = lambda_max.lambda_max_exact(L)
+        lm = sc.sc_dist_lambda_max(plans, 60, 0.01, 7, row0)
+        assert lN <= lm <= 1.02 * lN
+        lmax, order, npr, seed = 1.01 * lN, 50, 20, 4
+        mu = sc.sc_dist_cheb_moments(plans, lmax, order, npr, seed, row0)
+        P = np.zeros((g.n, npr))
+        for p in parts:
+            P[p.r0 + p.perm] = scinputs.gaussian_block(seed, p.n_local, npr, row0=p.r0, dtype=np.float64, stream=2)
+        assert mu[0] == pytest.approx(np.sum(P * P), rel=1e-12)
+        for ratio in [0.02, 0.07, 0.2, 0.5, 0.9]:
+            c = sc.sc_eigencount_from_moments(mu, order, ratio * lmax, lmax, True)
+            o = eigencount.count_below(L, ratio * lmax, lmax, order, P, True)
+            assert abs(c - o) <= 1e-9 * mu[0]
+        for k in [2, 5, 8]:
+            lk, ck = sc.sc_dist_estimate_lambda_k(plans, k, lmax, order, True, npr, seed, row0, 25, 1e-3)
+            lo, co, trace = eigencount.estimate_lambda_k(L, k, lmax, order, P, True, 25, 1e-3)
+            if lk != lo:
+                assert min(abs(c - (k - 0.5)) for _, c in trace) < 1e-8 * mu[0]
+            else:
+                assert abs(ck - co) <= 1e-9 * mu[0]
+    finally:
+        for pl in plans:
+            sc.sc_dist_free(pl)
+        for c in comms:
+            sc.sc_comm_free(c)
+
+
 @pytest.mark.parametrize("world,R,chunk,waits", [(2, 16, None, False), (3, 6, None, False), (4, 16, "8", False),
                                                  (2, 12, "4", False), (1, 8, None, False), (3, 16, "8", True)])
 def test_p2p_fused_exchange_emulated(sc, world, R, chunk, waits, monkeypatch):
@@ -875,10 +947,10 @@ def _random_case(i):
     return g, R, order, bool(rng.random() < 0.5), float(rng.uniform(0.01, 1.0))
 
 
-@pytest.mark.parametrize("path", ["resident", "streaming"])
+@pytest.mark.parametrize("path", list(PATHS))
 @pytest.mark.parametrize("i", range(16))
 def test_filter_random_cases(sc, i, path, monkeypatch):
-    monkeypatch.setenv("SC_RESIDENT", "1" if path == "resident" else "0")
+    _path_env(monkeypatch, path)
     g, R, order, jackson, ratio = _random_case(i)
     L = laplacian.laplacian(g)
     lmax = 2.0 * float(max(laplacian.strengths(laplacian.adjacency(g)).max(), 1e-12))
