@@ -418,7 +418,10 @@ def run_ours(args):
                            lambda_cut_count=count_k, **({"exchange": exchange} if partitioned else {})),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "cheb_step_kernel (fused SpMM + 3-term recurrence + Y accumulation)",
+                         "kernel": ("cheb_sell_kernel (fused sliced-CSR SpMM + 3-term recurrence + Y accumulation)"
+                                    if not partitioned else
+                                    "cheb_step_kernel (fused CSR SpMM + 3-term recurrence + Y accumulation, halo "
+                                    "exchange)"),
                          "avg_launch_us": avg_launch_s * 1e6, "algo_bytes_per_launch": bytes_per_launch,
                          "l2_gather_GBps": gather_gbps,
                          "l2_gather_ceiling_GBps": gceil, "l2_gather_ceiling_case": gcase,

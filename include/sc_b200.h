@@ -351,6 +351,28 @@ int sc_dist_estimate_lambda_k(sc_dist* const* ds, int nheld, int k, double lambd
                               int n_probe, uint64_t seed, const int64_t* row0, int max_iter, double rtol,
                               double* lambda_k, double* count_k, void* stream);
 
+/*
+ * sc_dist_kmeans -- sc_kmeans over the rows of a row partition (§4.1 step 6,
+ * l.323-328; BASELINE configs[4] "full pipeline including k-means" at 8 GPUs).  The points
+ * are the ranks' rows in rank-major order (rank 0's n_local[0] rows in its local order, then
+ * rank 1's, ...).  Lloyd runs data-parallel: every rank assigns its own rows with the
+ * single-GPU kernels; the exact fixed-point member sums and the member counts are summed over
+ * the ranks as integers (order independent: the centroids are bit-identical to sc_kmeans on
+ * the concatenated rows), the changed-label counts and the inertia likewise; the k-means++
+ * draw is made on the global D^2 prefix in rank order (R13).
+ * comms / nheld: nheld = 1 (one process per GPU, NCCL communicator from sc_comm_init; n_local
+ * = this rank's count) or nheld = world (all ranks in this process, communicators from
+ * sc_comm_local; one host thread per rank, reductions at a host rendezvous).
+ * F[r] (device, n_local[r] x d fp32), labels[r] (device int32 [n_local[r]]) per held rank;
+ * uniforms (host, restarts * k, or NULL = counter generator as sc_kmeans).  centroids (host,
+ * k * d, may be NULL), inertia, iters, best_restart (host, may be NULL): equal on every rank.
+ * Errors: SC_ERR_ARG (bad sizes, a rank with no rows, host buffers, total n >= 2^25),
+ * SC_ERR_CUDA, SC_ERR_STATE (ranks disagreeing on the result: a bug).
+ */
+int sc_dist_kmeans(sc_comm* const* comms, int nheld, const float* const* F, const int64_t* n_local, int d, int k,
+                   int restarts, int max_iter, uint64_t seed, const double* uniforms, int32_t* const* labels,
+                   double* centroids, double* inertia, int* iters, int* best_restart, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Row-partitioned filter with the halo exchange fused into the step kernel */
 /* (north_star: "exchanges the needed rows of T_j over NVLink ... overlapped */

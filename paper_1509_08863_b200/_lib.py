@@ -84,6 +84,8 @@ _F = {
     "sc_dist_cheb_moments": _sig("sc_dist_cheb_moments", c_vp, c_i32, c_dbl, c_i32, c_i32, c_u64, c_vp, c_vp, c_vp),
     "sc_dist_estimate_lambda_k": _sig("sc_dist_estimate_lambda_k", c_vp, c_i32, c_i32, c_dbl, c_i32, c_i32, c_i32,
                                       c_u64, c_vp, c_i32, c_dbl, P(c_dbl), P(c_dbl), c_vp),
+    "sc_dist_kmeans": _sig("sc_dist_kmeans", c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_u64, c_vp, c_vp,
+                           c_vp, P(c_dbl), P(c_i32), P(c_i32), c_vp),
     "sc_p2p_create": _sig("sc_p2p_create", c_vp, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i32,
                           P(c_vp)),
     "sc_p2p_free": _sig("sc_p2p_free", c_vp),
@@ -364,6 +366,23 @@ def sc_dist_estimate_lambda_k(ds, k, lambda_max, order, jackson, n_probe, seed, 
     _check(_F["sc_dist_estimate_lambda_k"](arr, n, k, lambda_max, order, int(jackson), n_probe, seed, r0, max_iter,
                                            rtol, ctypes.byref(lk), ctypes.byref(ck), _stream(stream)))
     return lk.value, ck.value
+
+
+def sc_dist_kmeans(comms, Fs, d, k, restarts, max_iter, seed, uniforms, labels, centroids=None, stream=None):
+    """Fs / labels: per held rank, device tensors (n_local x d fp32 / n_local int32)."""
+    comms = [comms] if isinstance(comms, int) else list(comms)
+    n = len(comms)
+    carr = (c_vp * n)(*comms)
+    farr = (c_vp * n)(*[_ptr(f) for f in Fs])
+    larr = (c_vp * n)(*[_ptr(x) for x in labels])
+    nl = np.ascontiguousarray([int(f.shape[0]) for f in Fs], dtype=np.int64)
+    u = None if uniforms is None else np.ascontiguousarray(uniforms, dtype=np.float64)
+    inertia, iters, best = c_dbl(), c_i32(), c_i32()
+    cp = None if centroids is None else centroids.ctypes.data
+    _check(_F["sc_dist_kmeans"](carr, n, farr, nl.ctypes.data, d, k, restarts, max_iter, seed,
+                                None if u is None else u.ctypes.data, larr, cp, ctypes.byref(inertia),
+                                ctypes.byref(iters), ctypes.byref(best), _stream(stream)))
+    return inertia.value, iters.value, best.value
 
 
 def sc_p2p_create(g, world, rank, n_global, sd_ptr, sd_row, sd_peer, sd_slot, peer_n_local, max_R):

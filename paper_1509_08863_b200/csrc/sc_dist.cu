@@ -17,7 +17,10 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "sc_internal.cuh"
@@ -381,6 +384,93 @@ int dist_moments(const Ranks& R, double lambda_max, int order, int np, uint64_t 
   mu[2 * order] = 2.0 * acc[3 * (order - 1) + 2] - mu[0];
   return SC_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Collectives of the distributed k-means (Coll, sc_internal.cuh)
+// ---------------------------------------------------------------------------
+struct NcclColl : Coll {
+  ncclComm_t comm;
+  NcclColl(ncclComm_t c, int r, int w) : comm(c) { rank = r; world = w; }
+  int red(void* p, size_t n, ncclDataType_t t, ncclRedOp_t op, cudaStream_t s) {
+    if (world == 1 || n == 0) return SC_OK;
+    SC_NCCL_TRY(ncclAllReduce(p, p, n, t, op, comm, s));
+    return SC_OK;
+  }
+  int sum_u64(unsigned long long* p, size_t n, cudaStream_t s) override { return red(p, n, ncclUint64, ncclSum, s); }
+  int sum_u32(unsigned* p, size_t n, cudaStream_t s) override { return red(p, n, ncclUint32, ncclSum, s); }
+  int sum_i32(int* p, size_t n, cudaStream_t s) override { return red(p, n, ncclInt32, ncclSum, s); }
+  int sum_f64(double* p, size_t n, cudaStream_t s) override { return red(p, n, ncclFloat64, ncclSum, s); }
+  int max_u32(unsigned* p, size_t n, cudaStream_t s) override { return red(p, n, ncclUint32, ncclMax, s); }
+};
+
+// Single-process emulation: one host thread per rank, each on its own stream of the one GPU.
+// A reduction synchronises the rank's stream, deposits its buffer in a host slot, meets the
+// other ranks at a host barrier, reduces the slots in rank order and copies the result back --
+// the ranks wait for each other on the host only (no kernel waits for another rank).
+struct LocalGroup {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  bool failed = false;
+  std::vector<std::vector<unsigned char>> slot;
+  explicit LocalGroup(int w) : world(w), slot(w) {}
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g || failed; });
+    }
+    return !failed;
+  }
+  void fail_all() {
+    std::lock_guard<std::mutex> lk(mu);
+    failed = true;
+    cv.notify_all();
+  }
+};
+
+struct LocalColl : Coll {
+  LocalGroup* grp;
+  LocalColl(LocalGroup* g, int r) : grp(g) { rank = r; world = g->world; }
+  template <typename T, typename Op>
+  int red(T* p, size_t n, cudaStream_t s, Op op) {
+    if (world == 1 || n == 0) return SC_OK;
+    std::vector<unsigned char>& mine = grp->slot[rank];
+    mine.resize(n * sizeof(T));
+    SC_CUDA_TRY(cudaMemcpyAsync(mine.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+    if (!grp->barrier()) return fail(SC_ERR_STATE, "another emulated rank failed");
+    std::vector<T> out(n);
+    std::memcpy(out.data(), grp->slot[0].data(), n * sizeof(T));
+    for (int r = 1; r < world; ++r) {
+      const T* x = reinterpret_cast<const T*>(grp->slot[r].data());
+      for (size_t i = 0; i < n; ++i) out[i] = op(out[i], x[i]);
+    }
+    if (!grp->barrier()) return fail(SC_ERR_STATE, "another emulated rank failed");
+    SC_CUDA_TRY(cudaMemcpyAsync(p, out.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+    return SC_OK;
+  }
+  int sum_u64(unsigned long long* p, size_t n, cudaStream_t s) override {
+    return red(p, n, s, [](unsigned long long a, unsigned long long b) { return a + b; });
+  }
+  int sum_u32(unsigned* p, size_t n, cudaStream_t s) override {
+    return red(p, n, s, [](unsigned a, unsigned b) { return a + b; });
+  }
+  int sum_i32(int* p, size_t n, cudaStream_t s) override { return red(p, n, s, [](int a, int b) { return a + b; }); }
+  int sum_f64(double* p, size_t n, cudaStream_t s) override {
+    return red(p, n, s, [](double a, double b) { return a + b; });
+  }
+  int max_u32(unsigned* p, size_t n, cudaStream_t s) override {
+    return red(p, n, s, [](unsigned a, unsigned b) { return a > b ? a : b; });
+  }
+};
 }  // namespace
 }  // namespace sc
 
@@ -612,6 +702,105 @@ int sc_dist_estimate_lambda_k(sc_dist* const* ds, int nheld, int k, double lambd
   std::vector<double> mu((size_t)2 * order + 1);
   SC_TRY(sc_dist_cheb_moments(ds, nheld, lambda_max, order, n_probe, seed, row0, mu.data(), stream));
   return lambda_k_dichotomy(mu.data(), order, k, lambda_max, jackson != 0, max_iter, rtol, lambda_k, count_k);
+}
+
+int sc_dist_kmeans(sc_comm* const* comms, int nheld, const float* const* F, const int64_t* n_local, int d, int k,
+                   int restarts, int max_iter, uint64_t seed, const double* uniforms, int32_t* const* labels,
+                   double* centroids, double* inertia, int* iters, int* best_restart, void* stream) {
+  SC_CHECK_ARG(comms && nheld >= 1 && F && n_local && labels, "null argument");
+  SC_CHECK_ARG(d >= 1 && k >= 1 && restarts >= 1 && max_iter >= 1, "bad arguments");
+  const int world = comms[0]->world;
+  SC_CHECK_ARG(nheld == 1 || nheld == world, "hold one rank or all ranks of the partition");
+  SC_CHECK_ARG(world <= kP2PMaxWorld, "world <= 8");
+  for (int r = 0; r < nheld; ++r) {
+    SC_CHECK_ARG(comms[r] && comms[r]->world == world && (nheld == 1 || comms[r]->rank == r),
+                 "communicators must be ranks 0..world-1 in order");
+    SC_CHECK_ARG(n_local[r] >= 1 && F[r] && labels[r] && is_device_ptr(F[r]) && is_device_ptr(labels[r]),
+                 "every rank needs >= 1 row; device features and labels required");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // the ranks' row counts -> each rank's global offset (rank-major point order)
+  std::vector<int64_t> counts(world, 0);
+  if (nheld == world) {
+    for (int r = 0; r < world; ++r) counts[r] = n_local[r];
+  } else if (world > 1) {
+    SC_CHECK_ARG(comms[0]->comm, "a multi-rank communicator without NCCL cannot run one held rank");
+    DevBuf cbuf;
+    SC_TRY(cbuf.ensure(sizeof(int64_t) * world));
+    SC_CUDA_TRY(cudaMemsetAsync(cbuf.ptr, 0, sizeof(int64_t) * world, s));
+    SC_CUDA_TRY(cudaMemcpyAsync(cbuf.as<int64_t>() + comms[0]->rank, n_local, sizeof(int64_t),
+                                cudaMemcpyHostToDevice, s));
+    SC_NCCL_TRY(ncclAllReduce(cbuf.ptr, cbuf.ptr, world, ncclInt64, ncclSum, comms[0]->comm, s));
+    SC_CUDA_TRY(cudaMemcpyAsync(counts.data(), cbuf.ptr, sizeof(int64_t) * world, cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+  } else {
+    counts[0] = n_local[0];
+  }
+  std::vector<int64_t> off(world + 1, 0);
+  for (int r = 0; r < world; ++r) off[r + 1] = off[r] + counts[r];
+  SC_CHECK_ARG(off[world] < (int64_t(1) << 25), "n must be < 2^25 for the exact centroid accumulator");
+  std::vector<double> u;
+  const double* uh = nullptr;
+  if (uniforms) {
+    u.assign(uniforms, uniforms + (size_t)restarts * k);
+    uh = u.data();
+  }
+  std::vector<double> C((size_t)k * d);
+  double in = 0.0;
+  int it = 0, best = 0;
+  if (nheld == 1) {
+    sc_comm* c = comms[0];
+    NcclColl coll(c->comm, c->rank, world);
+    SC_TRY(kmeans_run_dist(F[0], n_local[0], off[c->rank], off[world], d, k, restarts, max_iter, seed, uh, labels[0],
+                           C.data(), &in, &it, &best, &coll, s));
+  } else {
+    // emulation: one host thread and stream per rank
+    LocalGroup grp(world);
+    std::vector<int> rcs(world, SC_OK);
+    std::vector<std::string> msgs(world);
+    std::vector<double> ins(world);
+    std::vector<int> its(world), bests(world);
+    std::vector<std::vector<double>> Cs(world, std::vector<double>((size_t)k * d));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<std::thread> th;
+    for (int r = 0; r < world; ++r) {
+      th.emplace_back([&, r]() {
+        cudaSetDevice(dev);
+        cudaStream_t rs = nullptr;
+        int rc = cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking) == cudaSuccess ? SC_OK : SC_ERR_CUDA;
+        LocalColl coll(&grp, r);
+        if (rc == SC_OK)
+          rc = kmeans_run_dist(F[r], n_local[r], off[r], off[world], d, k, restarts, max_iter, seed, uh, labels[r],
+                               Cs[r].data(), &ins[r], &its[r], &bests[r], &coll, rs);
+        if (rc != SC_OK) {
+          rcs[r] = rc;
+          msgs[r] = sc_last_error();
+          grp.fail_all();
+        }
+        if (rs) {
+          cudaStreamSynchronize(rs);
+          cudaStreamDestroy(rs);
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int r = 0; r < world; ++r)
+      if (rcs[r] != SC_OK) return fail(rcs[r], "sc_dist_kmeans rank " + std::to_string(r) + ": " + msgs[r]);
+    for (int r = 1; r < world; ++r)
+      if (Cs[r] != Cs[0] || ins[r] != ins[0] || its[r] != its[0] || bests[r] != bests[0])
+        return fail(SC_ERR_STATE, "sc_dist_kmeans: ranks disagree on the result");
+    C = Cs[0];
+    in = ins[0];
+    it = its[0];
+    best = bests[0];
+  }
+  if (centroids) std::memcpy(centroids, C.data(), sizeof(double) * C.size());
+  if (inertia) *inertia = in;
+  if (iters) *iters = it;
+  if (best_restart) *best_restart = best;
+  return SC_OK;
 }
 
 }  // extern "C"

@@ -960,7 +960,16 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
       }
     }
     bool use_sell = false;
-    if (sell_enabled()) SC_TRY(sell_usable<T>(g, w, 0, n, s, &use_sell));
+    int64_t split_col = 0;
+    if (sell_enabled()) {
+      split_col = sell_split_col(g, w, sizeof(T));
+      if (split_col > 0) SC_TRY(sell_usable<T>(g, w, 0, n, s, &use_sell, split_col));
+      if (!use_sell) {
+        split_col = 0;
+        SC_TRY(sell_usable<T>(g, w, 0, n, s, &use_sell));
+      }
+    }
+    if (split_col > 0) SC_TRY(g->ws_split.ensure(sizeof(T) * (size_t)n * w));
     if (use_sell) {
       // SELL path: T_0 = the X chunk copied into bufs[0] (row stride w), zero row n_cols in
       // both buffers (the sentinel of the padded slices)
@@ -996,22 +1005,29 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
           p.y_mode = added == -1 ? 1 : 2;
           added = st + 1;
         }
-        p.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
         p.l2pol = static_cast<unsigned>(env_int("SC_L2POL", 0));
-        cudaEvent_t e0 = nullptr;
-        if (g_prof.on) {
-          e0 = g_prof.get();
-          cudaEventRecord(e0, s);
-        }
-        double ab = 0.0;
-        SC_TRY(launch_sell_step<T>(g, p, s, g_prof.on ? &ab : nullptr));
-        if (g_prof.on) {
-          cudaEvent_t e1 = g_prof.get();
-          cudaEventRecord(e1, s);
-          g_prof.ev.emplace_back(e0, e1);
-          g_prof.launches += 1;
-          g_prof.step_launches += 1;
-          g_prof.algo_bytes += ab;
+        p.split_col = split_col;
+        p.split_buf = split_col > 0 ? g->ws_split.ptr : nullptr;
+        // split gather: two launches per step (first half of the columns, then the second
+        // half + epilogue); the step's algorithmic bytes are counted once
+        for (int part = split_col > 0 ? 1 : 0; part <= (split_col > 0 ? 2 : 0); ++part) {
+          p.split_mode = part;
+          p.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
+          cudaEvent_t e0 = nullptr;
+          if (g_prof.on) {
+            e0 = g_prof.get();
+            cudaEventRecord(e0, s);
+          }
+          double ab = 0.0;
+          SC_TRY(launch_sell_step<T>(g, p, s, g_prof.on ? &ab : nullptr));
+          if (g_prof.on) {
+            cudaEvent_t e1 = g_prof.get();
+            cudaEventRecord(e1, s);
+            g_prof.ev.emplace_back(e0, e1);
+            g_prof.launches += 1;
+            g_prof.step_launches += 1;
+            g_prof.algo_bytes += part == 1 ? 0.0 : ab;
+          }
         }
       }
       col0 += w;

@@ -160,7 +160,7 @@ struct sc_graph {
   sc::DevBuf strength64;  // double [n_rows]
   sc::DevBuf strength32;  // float  [n_rows]
   // workspace (grow-only)
-  sc::DevBuf ws_a, ws_b, ws_sig, ws_part, ws_misc;
+  sc::DevBuf ws_a, ws_b, ws_sig, ws_part, ws_misc, ws_split;
   // per (tile rows, row_begin, row_end): degree-sorted row order inside each tile (uint16)
   mutable std::map<std::tuple<int, int64_t, int64_t>, std::unique_ptr<sc::DevBuf>> tile_orders;
   mutable std::mutex tile_orders_mu;
@@ -228,6 +228,12 @@ struct StepParams {
   // bits 2-3 T_{s+1} store (0 no hint, 1 evict_first, 2 evict_last, 3 evict_normal),
   // bits 4-5 T_{s-1} row (0 evict_first, 1 evict_normal)
   unsigned l2pol;
+  // split gather (SELL path): 0 none; 1 = columns [0, split_col) only, the row
+  // sums go to split_buf (row stride width) and there is no epilogue; 2 = columns
+  // [split_col, n_cols), split_buf added before the epilogue
+  int split_mode;
+  int64_t split_col;
+  void* split_buf;
 };
 
 // launch one fused step for `width` columns starting at the given pointers
@@ -240,7 +246,9 @@ template <typename T>
 int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, double* algo_bytes);
 bool sell_enabled();                       // env SC_SELL (default 1)
 template <typename T>
-int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end, cudaStream_t s, bool* ok);
+int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end, cudaStream_t s, bool* ok,
+                int64_t split_col = 0);
+int64_t sell_split_col(const sc_graph* g, int width, size_t elem);   // 0: no split gather
 void sell_release(const sc_graph* g);      // drop the graph's cached SELL plans
 
 // degree-sorted row order of every tile of tr rows over [row_begin, row_end) (cached on g)
@@ -309,6 +317,29 @@ double tridiag_max_eig(const std::vector<double>& alpha, const std::vector<doubl
 
 // k-means and friends
 int normalize_rows_f32(float* F, int64_t n, int d, cudaStream_t s);
+
+// Collective operations of one rank of a row partition (the distributed k-means): in-place
+// reductions of device buffers over the ranks, ordered on stream s.  Implementations: NCCL
+// (one process per GPU, sc_dist.cu) and the single-process emulation (one host thread per
+// rank on one GPU, host-side rendezvous: no kernel ever waits for another rank).
+struct Coll {
+  int rank = 0, world = 1;
+  virtual ~Coll() = default;
+  virtual int sum_u64(unsigned long long* p, size_t n, cudaStream_t s) = 0;   // wrap-around integer sums
+  virtual int sum_u32(unsigned* p, size_t n, cudaStream_t s) = 0;
+  virtual int sum_i32(int* p, size_t n, cudaStream_t s) = 0;
+  virtual int sum_f64(double* p, size_t n, cudaStream_t s) = 0;
+  virtual int max_u32(unsigned* p, size_t n, cudaStream_t s) = 0;
+};
+
+// k-means over the rows of every rank (distributed Lloyd): the points are the
+// ranks' local rows in rank-major order (rank 0's n_0 rows, then rank 1's ...); row_off = this
+// rank's first global index, n_global = all ranks' rows.  Every rank returns the same
+// centroids / inertia / iterations / restart and its own labels.
+int kmeans_run_dist(const float* F, int64_t n_local, int64_t row_off, int64_t n_global, int d, int k, int restarts,
+                    int max_iter, uint64_t seed, const double* uniforms_host, int32_t* labels_dev,
+                    double* centroids_host, double* inertia, int* iters, int* best_restart, Coll* coll,
+                    cudaStream_t s);
 int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_iter,
                uint64_t seed, const double* uniforms_host, int32_t* labels_dev,
                double* centroids_host, double* inertia, int* iters, int* best_restart,

@@ -303,6 +303,129 @@ __global__ void __launch_bounds__(kSel) seed_select_kernel(const double* __restr
   }
 }
 
+// ---- distributed k-means++ (kmeans_run_dist): the points are the ranks' rows in rank-major
+// order.  Each rank sums its D^2 in the same fixed order as seed_select_kernel (block sums,
+// then a block scan of them); the per-rank totals are summed over the ranks (S_all, every
+// entry but this rank's zero before the all-reduce), the draw's owner is the first rank whose
+// cumulative total exceeds u * total, and it selects its row exactly as seed_select_kernel does
+// with its local target; the other ranks write zeros and the row reaches every rank through
+// the sum all-reduce (x + 0 = x).  DESIGN.md R13: the global prefix is summed per rank here.
+__global__ void __launch_bounds__(kSel) local_total_kernel(const double* __restrict__ bsum, int G, int rank,
+                                                           double* __restrict__ s_all) {
+  __shared__ double s_w[64];
+  __shared__ double s_inc[kSel];
+  block_inclusive_scan(threadIdx.x < G ? bsum[threadIdx.x] : 0.0, s_w, s_inc);
+  if (threadIdx.x == 0) s_all[rank] = s_inc[kSel - 1];
+}
+
+struct DistDraw {
+  int rank, world;
+  int64_t row_off, n_global;
+};
+
+__global__ void __launch_bounds__(kSel) seed_select_dist_kernel(const double* __restrict__ bsum, int G,
+                                                                const double* __restrict__ v, int64_t n,
+                                                                int64_t chunk, double u,
+                                                                const double* __restrict__ s_all, DistDraw dd,
+                                                                const float* __restrict__ F, int d,
+                                                                double* __restrict__ c_out) {
+  __shared__ double s_w[64];
+  __shared__ double s_inc[kSel];
+  __shared__ int s_first;
+  __shared__ long long s_idx, s_last;
+  const int t = threadIdx.x;
+  double total = 0.0, pre = 0.0;
+  int owner = -1;
+  for (int q = 0; q < dd.world; ++q) total += s_all[q];
+  long long gidx = -1;   // uniform draw (all D^2 zero): global index
+  double target = 0.0;
+  if (!(total > 0.0)) {
+    const long long idx = (long long)floor(u * (double)dd.n_global);
+    gidx = idx < dd.n_global - 1 ? idx : dd.n_global - 1;
+    owner = (gidx >= dd.row_off && gidx < dd.row_off + n) ? dd.rank : -1;
+  } else {
+    target = u * total;
+    double cum = 0.0;
+    int last_pos = -1;
+    for (int q = 0; q < dd.world; ++q) {
+      if (s_all[q] > 0.0) last_pos = q;
+      if (owner < 0 && cum + s_all[q] > target) { owner = q; pre = cum; }
+      cum += s_all[q];
+    }
+    if (owner < 0) {   // rounding: the last rank holding positive D^2 takes the draw
+      owner = last_pos;
+      pre = 0.0;
+      for (int q = 0; q < last_pos; ++q) pre += s_all[q];
+    }
+  }
+  if (owner != dd.rank) {
+    for (int q = t; q < d; q += blockDim.x) c_out[q] = 0.0;
+    return;
+  }
+  if (gidx >= 0) {
+    const int64_t idx = gidx - dd.row_off;
+    for (int q = t; q < d; q += blockDim.x) c_out[q] = (double)F[idx * d + q];
+    return;
+  }
+  // this rank owns the draw: local target, then exactly seed_select_kernel's two-level search
+  const double ltarget = target - pre;
+  block_inclusive_scan(t < G ? bsum[t] : 0.0, s_w, s_inc);
+  if (t == 0) { s_first = INT_MAX; s_last = -1; }
+  __syncthreads();
+  if (t < G && s_inc[t] > ltarget) atomicMin(&s_first, t);
+  __syncthreads();
+  const int blk = s_first == INT_MAX ? G - 1 : s_first;
+  const double start = blk ? s_inc[blk - 1] : 0.0;
+  __syncthreads();
+  const int64_t b0 = (int64_t)blk * chunk, b1 = min(n, b0 + chunk);
+  const int64_t len = b1 - b0 > 0 ? b1 - b0 : 0;
+  const int64_t per = (len + kSel - 1) / kSel;
+  const int64_t s0 = min(b1, b0 + t * per), s1 = min(b1, s0 + per);
+  double sum = 0.0;
+  long long last_pos = -1;
+  for (int64_t i = s0; i < s1; ++i) {
+    const double vi = v[i];
+    sum += vi;
+    if (vi > 0.0) last_pos = i;
+  }
+  if (last_pos >= 0) atomicMax(&s_last, last_pos);
+  if (t == 0) s_first = INT_MAX;
+  block_inclusive_scan(sum, s_w, s_inc);
+  if (s1 > s0 && start + s_inc[t] > ltarget) atomicMin(&s_first, t);
+  __syncthreads();
+  if (s_first == INT_MAX) {
+    if (t == 0) s_idx = s_last >= 0 ? s_last : b1 - 1;
+  } else if (t == s_first) {
+    double acc = start + (t ? s_inc[t - 1] : 0.0);
+    long long pick = s1 - 1;
+    for (int64_t i = s0; i < s1; ++i) {
+      acc += v[i];
+      if (acc > ltarget) { pick = i; break; }
+    }
+    s_idx = pick;
+  }
+  __syncthreads();
+  const int64_t idx = s_idx;
+  for (int q = t; q < d; q += blockDim.x) c_out[q] = (double)F[idx * d + q];
+}
+
+// half distances from seed tseed to the earlier seeds (as seed_select_kernel computes them)
+__global__ void half_gap_kernel(const double* __restrict__ C, int d, int tseed, double* __restrict__ half_gap) {
+  const double* c_out = C + (int64_t)tseed * d;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < tseed; j += gridDim.x * blockDim.x) {
+    double s2 = 0.0;
+    for (int q = 0; q < d; ++q) {
+      const double df = c_out[q] - C[(int64_t)j * d + q];
+      s2 += df * df;
+    }
+    half_gap[j] = 0.5 * sqrt(s2) * (1.0 - 1e-9);
+  }
+}
+
+__global__ void row_or_zero_kernel(const float* __restrict__ F, int64_t idx_local, int d, double* __restrict__ c) {
+  for (int q = threadIdx.x; q < d; q += blockDim.x) c[q] = idx_local >= 0 ? (double)F[idx_local * d + q] : 0.0;
+}
+
 __global__ void row_to_centroid_kernel(const float* __restrict__ F, int64_t idx, int d, double* __restrict__ c) {
   for (int q = threadIdx.x; q < d; q += blockDim.x) c[q] = (double)F[idx * d + q];
 }
@@ -1220,7 +1343,11 @@ struct PinnedSlot {
 // ties -> lowest r) goes to *res and its labels to labels_dev.
 static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rstep, int restarts, int max_iter,
                          uint64_t seed, const double* uniforms_host, int32_t* labels_dev, KmResult* res,
-                         cudaStream_t s) {
+                         cudaStream_t s, Coll* coll = nullptr, int64_t row_off = 0, int64_t n_global = -1) {
+  // coll != nullptr: distributed over the ranks of a row partition (kmeans_run_dist) -- the
+  // same kernels on the local rows; the fixed-point scale, the changed-label counts, the exact
+  // member sums and counts, the inertia and the k-means++ draws are reduced over the ranks
+  if (n_global < 0) n_global = n;
   const int sms = num_sms_current();
   const int grid = sms * 8;
   const int G = std::min(sms * 2, 1024);                  // k-means++ range blocks (<= kSel)
@@ -1279,6 +1406,11 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_CUDA_TRY(cudaEventCreateWithFlags(&ev_chg[1], cudaEventDisableTiming));
   struct EvGuard { cudaEvent_t* e; ~EvGuard() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); } } ev_guard{ev_chg};
   SC_TRY(b_misc.ensure(64, s));
+  PoolBuf b_gcnt, b_sall;   // distributed: global member counts, per-rank D^2 totals (+ 1 scratch)
+  if (coll) {
+    SC_TRY(b_gcnt.ensure(sizeof(unsigned) * k, s));
+    SC_TRY(b_sall.ensure(sizeof(double) * (coll->world + 1), s));
+  }
   int32_t* lab = b_lab.as<int32_t>();
   int32_t* nw = b_new.as<int32_t>();
   double* C = b_C.as<double>();
@@ -1289,6 +1421,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_CUDA_TRY(cudaMemsetAsync(absmax, 0, sizeof(unsigned), s));
   absmax_bits_kernel<<<grid, kB, 0, s>>>(F, n * d, absmax);
   SC_CUDA_TRY(cudaGetLastError());
+  if (coll) SC_TRY(coll->max_u32(absmax, 1, s));   // one fixed-point scale on every rank
   unsigned amax_bits = 0;
   SC_CUDA_TRY(cudaMemcpyAsync(&amax_bits, absmax, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   SC_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1405,6 +1538,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
                                                        changed_dev + slot, cnt_of(slot),
                                                        b_chgl.as<int32_t>(), dcnt_of(slot));
     SC_CUDA_TRY(cudaGetLastError());
+    if (coll) SC_TRY(coll->sum_i32(changed_dev + slot, 1, s));   // labels changed on any rank
     return SC_OK;
   };
   auto read_inertia = [&](double* inertia) -> int {
@@ -1413,6 +1547,13 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     SC_CUDA_TRY(cudaStreamSynchronize(s));
     double tot = 0.0;
     for (double v : part) tot += v;   // fixed order: deterministic
+    if (coll) {   // + the other ranks' totals, in rank order
+      double* dv = b_sall.as<double>() + coll->world;
+      SC_CUDA_TRY(cudaMemcpyAsync(dv, &tot, sizeof(double), cudaMemcpyHostToDevice, s));
+      SC_TRY(coll->sum_f64(dv, 1, s));
+      SC_CUDA_TRY(cudaMemcpyAsync(&tot, dv, sizeof(double), cudaMemcpyDeviceToHost, s));
+      SC_CUDA_TRY(cudaStreamSynchronize(s));
+    }
     *inertia = tot;
     return SC_OK;
   };
@@ -1460,12 +1601,20 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     member_sum_kernel<<<(unsigned)max_items, slots * d, sizeof(unsigned long long) * 2 * slots * d, s>>>(
         F, d, b_perm.as<int32_t>(), d_off, d_item0, k, kChunk, d_total, shift, b_psum.as<unsigned long long>());
     SC_CUDA_TRY(cudaGetLastError());
+    const unsigned* counts = cnt_of(it - 1);
+    if (coll) {
+      // exact integer sums over the ranks (order independent), member counts likewise
+      SC_TRY(coll->sum_u64(b_psum.as<unsigned long long>(), (size_t)acc_elems, s));
+      SC_CUDA_TRY(cudaMemcpyAsync(b_gcnt.ptr, counts, sizeof(unsigned) * k, cudaMemcpyDeviceToDevice, s));
+      SC_TRY(coll->sum_u32(b_gcnt.as<unsigned>(), (size_t)k, s));
+      counts = b_gcnt.as<unsigned>();
+    }
     {
       // bounds wanted: 256 threads (power of two for the block reduction); else one warp-multiple
       const bool bounds = screen || prune;
       const int fin_threads = bounds ? 256 : std::min(256, (d + 31) / 32 * 32);
       member_finalize_kernel<<<(unsigned)k, fin_threads, 0, s>>>(
-          b_psum.as<unsigned long long>(), cnt_of(it - 1), k, d, shift, C, screen ? d_Cf : nullptr,
+          b_psum.as<unsigned long long>(), counts, k, d, shift, C, screen ? d_Cf : nullptr,
           screen ? d_cm : nullptr, prune ? b_dmax.as<double>() : nullptr);
     }
     SC_CUDA_TRY(cudaGetLastError());
@@ -1484,15 +1633,32 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     for (int t = 0; t < k; ++t)
       u[t] = uniforms_host ? uniforms_host[(size_t)r * k + t] : uniform_host(seed, 1, (uint64_t)r * k + t);
     // ---- k-means++ seeding (device-resident: block sums, then one selection kernel per draw)
-    int64_t idx = std::min<int64_t>((int64_t)std::floor(u[0] * n), n - 1);
-    row_to_centroid_kernel<<<1, 128, 0, s>>>(F, idx, d, C);
+    int64_t idx = std::min<int64_t>((int64_t)std::floor(u[0] * n_global), n_global - 1);
+    if (!coll) {
+      row_to_centroid_kernel<<<1, 128, 0, s>>>(F, idx, d, C);
+    } else {
+      row_or_zero_kernel<<<1, 128, 0, s>>>(F, (idx >= row_off && idx < row_off + n) ? idx - row_off : -1, d, C);
+      SC_TRY(coll->sum_f64(C, (size_t)d, s));
+    }
     d2_update_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_d2, s>>>(F, n, d, C, b_d2.as<double>(), 1,
                                                                           b_near.as<int32_t>());
     SC_CUDA_TRY(cudaGetLastError());
     for (int t = 1; t < k; ++t) {
       range_sums_kernel<<<G, kB, 0, s>>>(b_d2.as<double>(), n, chunk, b_part.as<double>());
-      seed_select_kernel<<<1, kSel, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk, u[t], F, d,
-                                          C + (size_t)t * d, t, b_gap.as<double>());
+      if (!coll) {
+        seed_select_kernel<<<1, kSel, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk, u[t], F, d,
+                                            C + (size_t)t * d, t, b_gap.as<double>());
+      } else {
+        SC_CUDA_TRY(cudaMemsetAsync(b_sall.ptr, 0, sizeof(double) * coll->world, s));
+        local_total_kernel<<<1, kSel, 0, s>>>(b_part.as<double>(), G, coll->rank, b_sall.as<double>());
+        SC_TRY(coll->sum_f64(b_sall.as<double>(), (size_t)coll->world, s));
+        seed_select_dist_kernel<<<1, kSel, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk, u[t],
+                                                 b_sall.as<double>(), DistDraw{coll->rank, coll->world, row_off,
+                                                                               n_global},
+                                                 F, d, C + (size_t)t * d);
+        SC_TRY(coll->sum_f64(C + (size_t)t * d, (size_t)d, s));
+        half_gap_kernel<<<1, 256, 0, s>>>(C, d, t, b_gap.as<double>());
+      }
       d2_update_skip_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_d2, s>>>(
           F, n, d, C + (size_t)t * d, t, b_gap.as<double>(), b_d2.as<double>(), b_near.as<int32_t>());
       SC_CUDA_TRY(cudaGetLastError());
@@ -1517,7 +1683,9 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     for (it = 1; it <= max_iter; ++it) {
       const bool try_check = !screen || use_check || it - last_check >= 8;
       if (try_check) last_check = it;
-      SC_TRY(update(lab, it >= 2 ? nw : nullptr, changed_dev + (it - 1), it));
+      // (distributed: full recompute every iteration -- the incremental update would keep
+      // per-rank running sums apart from the reduced ones)
+      SC_TRY(update(lab, (it >= 2 && !coll) ? nw : nullptr, changed_dev + (it - 1), it));
       SC_TRY(assign_all(nw, lab, it, try_check));
       SC_CUDA_TRY(cudaMemcpyAsync(h_chg + it, changed_dev + it, sizeof(int), cudaMemcpyDeviceToHost, s));
       if (screen && try_check)
@@ -1559,6 +1727,22 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   res->iters = best_it;
   res->r = best_r;
   res->C = best_C;
+  return SC_OK;
+}
+
+int kmeans_run_dist(const float* F, int64_t n_local, int64_t row_off, int64_t n_global, int d, int k, int restarts,
+                    int max_iter, uint64_t seed, const double* uniforms_host, int32_t* labels_dev,
+                    double* centroids_host, double* inertia_out, int* iters_out, int* best_out, Coll* coll,
+                    cudaStream_t s) {
+  // restarts one after another (every rank issues the same collectives in the same order)
+  KmResult res;
+  SC_TRY(kmeans_worker(F, n_local, d, k, 0, 1, restarts, max_iter, seed, uniforms_host, labels_dev, &res, s, coll,
+                       row_off, n_global));
+  if (res.r < 0) return fail(SC_ERR_ARG, "k-means produced no finite inertia");
+  if (centroids_host) std::memcpy(centroids_host, res.C.data(), sizeof(double) * k * d);
+  if (inertia_out) *inertia_out = res.inertia;
+  if (iters_out) *iters_out = res.iters;
+  if (best_out) *best_out = res.r;
   return SC_OK;
 }
 

@@ -424,6 +424,8 @@ int resident_filter(sc_graph* g, const double* d, int order, double lambda_max, 
   void* args[] = {(void*)&a_rp, (void*)&a_col, (void*)&a_val, (void*)&a_str, (void*)&ord, (void*)&rp};
   cudaEvent_t e0 = nullptr;
   prof_launch_begin(s, &e0);
+  // (the attribute is per kernel and plans of other graphs may have set a smaller one)
+  SC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SC_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k, grid, kRThreads, args, smem, s));
   SC_CUDA_TRY(cudaGetLastError());
   // algorithmic bytes as for the streaming path (§0(d)): per step the CSR share of this chunk

@@ -101,7 +101,7 @@ struct SellLayout {
     cap = cap_;
     meta_off = 0;
     ord_off = (size_t)kNC * 16;
-    idx_off = ord_off + (((size_t)tr * 2 + 15) & ~(size_t)15);
+    idx_off = ord_off + (((size_t)tr * 4 + 15) & ~(size_t)15);
     val_off = idx_off + (size_t)cap * 4;
     stage_bytes = val_off + (unit ? 0 : (size_t)cap * 4);
     stage_bytes = (stage_bytes + 127) & ~(size_t)127;
@@ -118,7 +118,8 @@ struct SellDev {
   const void* hubpart;            // [n_chunks][width] partial sums of the hub chunks (type T)
   const int32_t* idx;        // column indices (sentinel n_cols = the zero row)
   const float* val;          // weights (0 on padding), nullptr for unit weights
-  const uint16_t* order;     // [ntiles * tr] degree-sorted row order inside each tile
+  const int32_t* order;      // [ntiles * tr] row (relative to row_begin) at each tile position:
+                             // degree-sorted within windows of sigma rows (SELL-C-sigma)
 };
 
 // 16-byte gathers as two packed fp32 pairs (for add.rn.f32x2)
@@ -325,13 +326,13 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
         const int overflow = ncol > lay.cap;
         m.r0 = r0; m.r1 = r1; m.e0 = e0; m.overflow = overflow; m.tile = (int32_t)t;
         unsigned char* st = stages + (size_t)s * lay.stage_bytes;
-        uint32_t tx = (uint32_t)(kNC * 16) + (uint32_t)(TR * 2);
+        uint32_t tx = (uint32_t)(kNC * 16) + (uint32_t)(TR * 4);
         const bool cp_col = !overflow && ncol > 0;
         if (cp_col) tx += (uint32_t)(ncol * 4 * (UNIT ? 1 : 2));
         mbar_arrive_expect_tx(&full[s], tx);
         const uint64_t pol_stream = policy_evict_first();
         bulk_g2s(st + lay.meta_off, sd.meta + t * kNC, (uint32_t)(kNC * 16), &full[s], pol_stream);
-        bulk_g2s(st + lay.ord_off, sd.order + t * TR, (uint32_t)(TR * 2), &full[s], pol_stream);
+        bulk_g2s(st + lay.ord_off, sd.order + t * TR, (uint32_t)(TR * 4), &full[s], pol_stream);
         if (cp_col) {
           bulk_g2s(st + lay.idx_off, sd.idx + e0, (uint32_t)(ncol * 4), &full[s], pol_stream);
           if (!UNIT) bulk_g2s(st + lay.val_off, sd.val + e0, (uint32_t)(ncol * 4), &full[s], pol_stream);
@@ -370,10 +371,10 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
     // with the tile so every warp sees every degree class
     const int j = (warp + static_cast<int>(t % kNC)) % kNC;
     const int4 mj = reinterpret_cast<const int4*>(st + lay.meta_off)[j];
-    const uint16_t* ord = reinterpret_cast<const uint16_t*>(st + lay.ord_off);
+    const int32_t* ord = reinterpret_cast<const int32_t*>(st + lay.ord_off);
     const int rank = j * RPW + sub;
     const bool valid = sub < RPW && rank < static_cast<int>(m.r1 - m.r0);
-    const int32_t row = static_cast<int32_t>(m.r0) + (valid ? ord[rank] : 0);   // rows < 2^31
+    const int32_t row = static_cast<int32_t>(p.row_begin) + (valid ? ord[rank] : 0);   // rows < 2^31
     if (dense_stage && valid) {
       // own row, T_{s-1} and Y rows land in shared memory while the gathers run.  No L2
       // cache hint here: with one, ptxas 12.9 allocated the hint's 64-bit descriptor to an
@@ -394,6 +395,11 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
+    if (p.split_mode == 1) {
+      // first half of the columns: park the row sums, no epilogue (the second launch adds them)
+      if (valid) Vec<T>::st(static_cast<T*>(p.split_buf) + (int64_t)row * p.width + c, acc);
+      continue;
+    }
     if (valid && ((mj.z >> sub) & 1)) {
       // a hub row (degree above the plan's threshold): its slice entries are empty and its
       // neighbour sum was split over warps by hub_chunk_kernel (launched just before, so
@@ -409,6 +415,13 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
 #pragma unroll
         for (int w = 0; w < W; ++w) acc[w] += v[w];
       }
+    }
+    if (valid && p.split_mode == 2) {
+      // second half: + the first half's row sums (hub rows: 0 there, their sum came above)
+      T pv[W];
+      Vec<T>::ld(static_cast<const T*>(p.split_buf) + (int64_t)row * p.width + c, pv);
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc[w] += pv[w];
     }
     if (valid) {
       T own[W], prv[W], yv[W];
@@ -460,6 +473,7 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
 // has chunks.
 // ---------------------------------------------------------------------------
 constexpr int kHubChunk = 512;
+constexpr int kHubU = 8;   // gathers in flight per lane in hub_chunk_kernel
 
 struct HubChunk {
   int64_t e0;     // first edge (CSR position)
@@ -474,24 +488,57 @@ hub_chunk_kernel(const HubChunk* __restrict__ chunks, int n_chunks, const int32_
   constexpr int W = Vec<T>::W;
   constexpr int SW = VPR;
   constexpr int RPW = 32 / SW;
-  const int lane = threadIdx.x & 31;
+  // the chunk's column indices (and weights) are staged in shared memory by the whole warp with
+  // coalesced loads, so the gathers do not wait on a dependent index load
+  __shared__ __align__(16) int32_t s_idx[8][kHubChunk];
+  __shared__ __align__(16) float s_val[UNIT ? 1 : 8][UNIT ? 1 : kHubChunk];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int sub = lane / SW, sl = lane % SW, c = sl * W;
   const T* tcur = static_cast<const T*>(p.tcur);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < n_chunks; q += (gridDim.x * blockDim.x) >> 5) {
     const HubChunk ch = chunks[q];
+    __syncwarp();
+    for (int e = lane; e < ch.len; e += 32) {
+      s_idx[wib][e] = col[ch.e0 + e];
+      if (!UNIT) s_val[wib][e] = val[ch.e0 + e];
+    }
+    __syncwarp();
     T acc[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) acc[w] = T(0);
     if (sub < RPW) {
-      for (int e = sub; e < ch.len; e += RPW) {
-        const int64_t k = col[ch.e0 + e];
-        T v[W];
-        Vec<T>::ldg(tcur + k * p.ld_cur + c, v);
-        const T wt = UNIT ? T(1) : static_cast<T>(val[ch.e0 + e]);
+      // kHubU independent gathers in flight per lane (one accumulator each, added in order)
+      T part[kHubU][W];
 #pragma unroll
-        for (int w = 0; w < W; ++w) acc[w] = UNIT ? acc[w] + v[w] : fma(wt, v[w], acc[w]);
+      for (int u = 0; u < kHubU; ++u)
+#pragma unroll
+        for (int w = 0; w < W; ++w) part[u][w] = T(0);
+      for (int e0 = sub; e0 < ch.len; e0 += RPW * kHubU) {
+        T v[kHubU][W];
+        T wt[kHubU];
+#pragma unroll
+        for (int u = 0; u < kHubU; ++u) {
+          const int e = e0 + u * RPW;
+          if (e < ch.len) {
+            const int64_t k = s_idx[wib][e];
+            Vec<T>::ldg(tcur + k * p.ld_cur + c, v[u]);
+            wt[u] = UNIT ? T(1) : static_cast<T>(s_val[UNIT ? 0 : wib][UNIT ? 0 : e]);
+          } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) v[u][w] = T(0);
+            wt[u] = T(0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kHubU; ++u)
+#pragma unroll
+          for (int w = 0; w < W; ++w) part[u][w] = UNIT ? part[u][w] + v[u][w] : fma(wt[u], v[u][w], part[u][w]);
       }
+#pragma unroll
+      for (int u = 0; u < kHubU; ++u)
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[w] += part[u][w];
     }
     // groups added in group order by the lanes of group 0
 #pragma unroll
@@ -510,10 +557,66 @@ hub_chunk_kernel(const HubChunk* __restrict__ chunks, int n_chunks, const int32_
 // ---------------------------------------------------------------------------
 // SELL build
 // ---------------------------------------------------------------------------
+// Row order of the plan (SELL-C-sigma): rows sorted by degree (ascending, ties by index)
+// within windows of sigma consecutive rows, hub rows (degree > hub_deg) last; tile t takes
+// sorted positions [t tr, (t + 1) tr).  One block per window, bitonic sort in shared memory
+// of keys degree << 32 | local index (unique).  Positions past the last row hold -1.
+constexpr int kSigmaMax = 4096;
+
+// edges of `row` with column in [c0, c1) (full = the whole row)
+__device__ __forceinline__ int64_t deg_in(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                          int64_t row, int64_t c0, int64_t c1, bool full) {
+  const int64_t b = rp[row], e = rp[row + 1];
+  if (full) return e - b;
+  int64_t d = 0;
+  for (int64_t k = b; k < e; ++k) {
+    const int64_t c = col[k];
+    d += (c >= c0 && c < c1);
+  }
+  return d;
+}
+__global__ void __launch_bounds__(1024) sell_order_kernel(const int64_t* __restrict__ row_ptr,
+                                                          const int32_t* __restrict__ col, int64_t c0, int64_t c1,
+                                                          bool full, int64_t row_begin, int64_t row_end, int sigma,
+                                                          int64_t hub_deg, int32_t* __restrict__ order) {
+  __shared__ unsigned long long key[kSigmaMax];
+  const int64_t w0 = row_begin + (int64_t)blockIdx.x * sigma;
+  const int cnt = static_cast<int>(min((int64_t)sigma, row_end - w0));
+  int P = 1;
+  while (P < sigma) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    unsigned long long kk = ~0ull;
+    if (i < cnt) {
+      const int64_t d = row_ptr[w0 + i + 1] - row_ptr[w0 + i];   // hubs by their full degree
+      const unsigned long long dk = d > hub_deg ? (unsigned long long)hub_deg + 1
+                                                : (unsigned long long)deg_in(row_ptr, col, w0 + i, c0, c1, full);
+      kk = (dk << 32) | (unsigned)i;
+    }
+    key[i] = kk;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long a = key[i], b = key[l];
+          if ((a > b) == up) { key[i] = b; key[l] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < sigma; i += blockDim.x)
+    order[(int64_t)blockIdx.x * sigma + i] =
+        i < cnt ? static_cast<int32_t>(w0 - row_begin + (int64_t)(unsigned)(key[i] & 0xffffffffull)) : -1;
+}
+
 // padded length of every slice (max degree of its rows rounded up to 4) and entries per tile
 // (rows of degree > hub_deg are hubs: no slice entries, split-row path)
-__global__ void sell_len_kernel(const int64_t* __restrict__ row_ptr, int64_t row_begin, int64_t row_end, int tr,
-                                int rpw, const uint16_t* __restrict__ order, int64_t hub_deg,
+__global__ void sell_len_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, int64_t c0,
+                                int64_t c1, bool full, int64_t row_begin, int64_t row_end, int tr,
+                                int rpw, const int32_t* __restrict__ order, int64_t hub_deg,
                                 int32_t* __restrict__ slice_len, int64_t* __restrict__ tile_entries,
                                 int32_t* __restrict__ tile_hubs) {
   const int64_t t = blockIdx.x;
@@ -525,10 +628,10 @@ __global__ void sell_len_kernel(const int64_t* __restrict__ row_ptr, int64_t row
     for (int q = 0; q < rpw; ++q) {
       const int rank = j * rpw + q;
       if (rank < cnt) {
-        const int64_t row = r0 + order[t * tr + rank];
+        const int64_t row = row_begin + order[t * tr + rank];
         const int64_t d = row_ptr[row + 1] - row_ptr[row];
         if (d > hub_deg) ++nh;
-        else maxd = max(maxd, static_cast<int>(d));
+        else maxd = max(maxd, static_cast<int>(deg_in(row_ptr, col, row, c0, c1, full)));
       }
     }
     len[j] = (maxd + 3) & ~3;
@@ -549,17 +652,17 @@ __global__ void sell_len_kernel(const int64_t* __restrict__ row_ptr, int64_t row
 }
 
 __global__ void sell_fill_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                                 const float* __restrict__ val, int64_t row_begin, int64_t row_end, int tr, int rpw,
-                                 const uint16_t* __restrict__ order, const int32_t* __restrict__ slice_len,
-                                 const int64_t* __restrict__ tile_ptr, int32_t sentinel, int64_t hub_deg,
-                                 const int32_t* __restrict__ tile_hub_base, int4* __restrict__ meta,
-                                 int32_t* __restrict__ idx, float* __restrict__ sval, int32_t* __restrict__ hub_rows) {
+                                 const float* __restrict__ val, int64_t c0, int64_t c1, bool full, int64_t row_begin,
+                                 int64_t row_end, int tr, int rpw, const int32_t* __restrict__ order,
+                                 const int32_t* __restrict__ slice_len, const int64_t* __restrict__ tile_ptr,
+                                 int32_t sentinel, int64_t hub_deg, const int32_t* __restrict__ tile_hub_base,
+                                 int4* __restrict__ meta, int32_t* __restrict__ idx, float* __restrict__ sval,
+                                 int32_t* __restrict__ hub_rows) {
   const int64_t t = blockIdx.x;
   const int64_t r0 = row_begin + t * tr;
   const int cnt = static_cast<int>(min((int64_t)tr, row_end - r0));
   __shared__ int off[65];
-  __shared__ int64_t rb[1024];
-  __shared__ int deg[1024];
+  __shared__ int hub[1024];
   if (threadIdx.x == 0) {
     int o = 0;
     for (int j = 0; j < kNC; ++j) {
@@ -568,18 +671,11 @@ __global__ void sell_fill_kernel(const int64_t* __restrict__ row_ptr, const int3
     }
     off[kNC] = o;
   }
-  __shared__ int hub[1024];
   for (int r = threadIdx.x; r < tr; r += blockDim.x) {
+    hub[r] = 0;
     if (r < cnt) {
-      const int64_t row = r0 + order[t * tr + r];
-      rb[r] = row_ptr[row];
-      const int64_t d = row_ptr[row + 1] - rb[r];
-      hub[r] = d > hub_deg;
-      deg[r] = hub[r] ? 0 : static_cast<int>(d);
-    } else {
-      rb[r] = 0;
-      deg[r] = 0;
-      hub[r] = 0;
+      const int64_t row = row_begin + order[t * tr + r];
+      hub[r] = row_ptr[row + 1] - row_ptr[row] > hub_deg;
     }
   }
   __syncthreads();
@@ -593,25 +689,37 @@ __global__ void sell_fill_kernel(const int64_t* __restrict__ row_ptr, const int3
         const int rank = j * rpw + q;
         if (rank < cnt && hub[rank]) {
           mask |= 1 << q;
-          hub_rows[h++] = static_cast<int32_t>(r0 - row_begin + order[t * tr + rank]);
+          hub_rows[h++] = order[t * tr + rank];
         }
       }
       meta[t * kNC + j] = make_int4(off[j], slice_len[t * kNC + j], mask, base);
     }
   }
+  // one thread per tile row: its edges in [c0, c1), in CSR order, at the chunk-interleaved
+  // positions of its slice; the rest of the padded row gets the sentinel
   const int64_t base = tile_ptr[t];
-  const int total = off[kNC];
-  for (int q = threadIdx.x; q < total; q += blockDim.x) {
-    int j = 0;
-    while (off[j + 1] <= q) ++j;
-    const int rel = q - off[j];
-    const int chunk = rel / (4 * rpw), rem = rel % (4 * rpw);
-    const int r = rem / 4;
-    const int e = chunk * 4 + rem % 4;
-    const int rank = j * rpw + r;
-    const bool real = rank < cnt && e < deg[rank];
-    idx[base + q] = real ? col[rb[rank] + e] : sentinel;
-    if (sval) sval[base + q] = real ? val[rb[rank] + e] : 0.f;
+  for (int rank = threadIdx.x; rank < kNC * rpw; rank += blockDim.x) {
+    const int j = rank / rpw, q = rank % rpw;
+    const int L = slice_len[t * kNC + j];
+    int32_t* di = idx + base + off[j];
+    float* dv = sval ? sval + base + off[j] : nullptr;
+    int e = 0;
+    if (rank < cnt && !hub[rank]) {
+      const int64_t row = row_begin + order[t * tr + rank];
+      for (int64_t k = row_ptr[row]; k < row_ptr[row + 1]; ++k) {
+        const int64_t c = col[k];
+        if (!full && (c < c0 || c >= c1)) continue;
+        const int pos = (e / 4) * 4 * rpw + q * 4 + (e % 4);
+        di[pos] = col[k];
+        if (dv) dv[pos] = val[k];
+        ++e;
+      }
+    }
+    for (; e < L; ++e) {
+      const int pos = (e / 4) * 4 * rpw + q * 4 + (e % 4);
+      di[pos] = sentinel;
+      if (dv) dv[pos] = 0.f;
+    }
   }
 }
 
@@ -619,17 +727,39 @@ struct SellPlan {
   int tr = 0, rpw = 0;
   int64_t ntiles = 0, entries = 0, max_tile = 0;
   DevBuf tile_ptr, meta, idx, val;
-  const uint16_t* order = nullptr;
+  DevBuf order;   // int32 [ntiles * tr]
+  int sigma = 0;  // rows per degree-sorting window
   // split rows
   int64_t hub_deg = 0;
   int n_hubs = 0, n_chunks = 0;
   DevBuf hub_rows, hub_chunk_ptr, chunks, hubpart;
 };
 
+__global__ void max_degree_kernel(const int64_t* __restrict__ row_ptr, int64_t r0, int64_t r1,
+                                  unsigned long long* __restrict__ out) {
+  unsigned long long m = 0;
+  for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)(row_ptr[i + 1] - row_ptr[i]));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+int64_t max_row_degree(const sc_graph* g, int64_t r0, int64_t r1, cudaStream_t s) {
+  DevBuf b;
+  if (r1 <= r0 || b.ensure(sizeof(unsigned long long)) != SC_OK) return 0;
+  unsigned long long h = 0;
+  cudaMemsetAsync(b.ptr, 0, sizeof(h), s);
+  max_degree_kernel<<<g->num_sms * 4, 256, 0, s>>>(g->row_ptr.as<int64_t>(), r0, r1, b.as<unsigned long long>());
+  cudaMemcpyAsync(&h, b.ptr, sizeof(h), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  return (int64_t)h;
+}
+
 // split-row threshold: a row of degree > this is cut into chunks (env SC_SELL_HUB_DEG)
 int64_t hub_threshold() {
   const char* v = std::getenv("SC_SELL_HUB_DEG");
-  return v ? std::atoll(v) : 512;
+  return v ? std::atoll(v) : 128;   // Chung-Lu (N = 10^6, exponent 2.1): 281 / 229 / 207 / 209 ms per
+                                    // pass at 512 / 256 / 128 / 64 (profiles/r02_sell.md)
 }
 
 // hub rows' CSR ranges (device) -> host
@@ -643,17 +773,22 @@ __global__ void hub_range_kernel(const int64_t* __restrict__ row_ptr, int64_t ro
 }
 
 std::mutex g_sell_mu;
-std::map<std::tuple<const sc_graph*, int, int64_t, int64_t>, std::unique_ptr<SellPlan>> g_sell_plans;
+std::map<std::tuple<const sc_graph*, int, int64_t, int64_t, int64_t, int64_t>, std::unique_ptr<SellPlan>> g_sell_plans;
 
 int env_int_s(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
 }
 
-int sell_plan(const sc_graph* g, int vpr, int64_t row_begin, int64_t row_end, cudaStream_t s, SellPlan** out) {
+// Plan of the rows [row_begin, row_end) and the columns [c0, c1) (all columns: c0 = 0,
+// c1 = n_cols; a column range keeps only those edges -- the split gather's halves)
+int sell_plan(const sc_graph* g, int vpr, int64_t row_begin, int64_t row_end, cudaStream_t s, SellPlan** out,
+              int64_t c0 = 0, int64_t c1 = -1) {
   const int tr = sell_tile_rows(vpr), rpw = 32 / vpr;
+  if (c1 < 0) c1 = g->n_cols;
+  const bool full = c0 <= 0 && c1 >= g->n_cols;
   std::lock_guard<std::mutex> lock(g_sell_mu);
-  auto key = std::make_tuple(g, tr, row_begin, row_end);
+  auto key = std::make_tuple(g, tr, row_begin, row_end, full ? 0 : c0, full ? g->n_cols : c1);
   auto it = g_sell_plans.find(key);
   if (it != g_sell_plans.end()) {
     *out = it->second.get();
@@ -663,16 +798,37 @@ int sell_plan(const sc_graph* g, int vpr, int64_t row_begin, int64_t row_end, cu
   pl->tr = tr;
   pl->rpw = rpw;
   pl->ntiles = (row_end - row_begin + tr - 1) / tr;
-  pl->order = tile_order(g, tr, row_begin, row_end, s);
-  if (!pl->order) return fail(SC_ERR_NOMEM, "tile order allocation failed");
   const int64_t nt = pl->ntiles;
   pl->hub_deg = hub_threshold();
+  // sorting window: one tile when the degrees are narrow (the tile's own sort pads little:
+  // configs[3] 1.05), else up to kSigmaMax rows (power-law degrees: Chung-Lu padding
+  // 1.38 -> 1.15 at 4096; env SC_SELL_SIGMA overrides)
+  {
+    const double avg = (double)g->nnz / std::max<int64_t>(1, g->n_rows);
+    const int forced = env_int_s("SC_SELL_SIGMA", 0);
+    int sig = tr;
+    if (forced > 0) sig = std::max(tr, std::min(kSigmaMax, forced / tr * tr));
+    else if ((double)max_row_degree(g, row_begin, row_end, s) > 8.0 * std::max(1.0, avg)) sig = kSigmaMax / tr * tr;
+    pl->sigma = std::max(tr, sig);
+  }
+  SC_TRY(pl->order.ensure(sizeof(int32_t) * std::max<int64_t>(1, nt * tr)));
+  if (nt > 0) {
+    const int64_t nwin = (row_end - row_begin + pl->sigma - 1) / pl->sigma;
+    // the last window's positions past nt * tr do not exist: sigma divides into whole tiles,
+    // so allocate whole windows
+    SC_TRY(pl->order.ensure(sizeof(int32_t) * (size_t)nwin * pl->sigma));
+    sell_order_kernel<<<(unsigned)nwin, 1024, 0, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(), c0, c1,
+                                                      full, row_begin, row_end, pl->sigma, pl->hub_deg,
+                                                      pl->order.as<int32_t>());
+    SC_CUDA_TRY(cudaGetLastError());
+  }
   DevBuf slen, tent, thub;
   SC_TRY(slen.ensure(sizeof(int32_t) * std::max<int64_t>(1, nt * kNC)));
   SC_TRY(tent.ensure(sizeof(int64_t) * std::max<int64_t>(1, nt)));
   SC_TRY(thub.ensure(sizeof(int32_t) * std::max<int64_t>(1, nt)));
   if (nt > 0) {
-    sell_len_kernel<<<(unsigned)nt, 64, 0, s>>>(g->row_ptr.as<int64_t>(), row_begin, row_end, tr, rpw, pl->order,
+    sell_len_kernel<<<(unsigned)nt, 64, 0, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(), c0, c1, full,
+                                                row_begin, row_end, tr, rpw, pl->order.as<int32_t>(),
                                                 pl->hub_deg, slen.as<int32_t>(), tent.as<int64_t>(),
                                                 thub.as<int32_t>());
     SC_CUDA_TRY(cudaGetLastError());
@@ -702,8 +858,8 @@ int sell_plan(const sc_graph* g, int vpr, int64_t row_begin, int64_t row_end, cu
   if (!g->unit_weights) SC_TRY(pl->val.ensure(sizeof(float) * std::max<int64_t>(4, pl->entries)));
   if (nt > 0) {
     sell_fill_kernel<<<(unsigned)nt, 256, 0, s>>>(
-        g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(), g->unit_weights ? nullptr : g->values.as<float>(),
-        row_begin, row_end, tr, rpw, pl->order, slen.as<int32_t>(), pl->tile_ptr.as<int64_t>(),
+        g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(), g->unit_weights ? nullptr : g->values.as<float>(), c0,
+        c1, full, row_begin, row_end, tr, rpw, pl->order.as<int32_t>(), slen.as<int32_t>(), pl->tile_ptr.as<int64_t>(),
         static_cast<int32_t>(g->n_cols), pl->hub_deg, thbase.as<int32_t>(), pl->meta.as<int4>(),
         pl->idx.as<int32_t>(), g->unit_weights ? nullptr : pl->val.as<float>(), pl->hub_rows.as<int32_t>());
     SC_CUDA_TRY(cudaGetLastError());
@@ -840,19 +996,40 @@ void sell_release(const sc_graph* g) {
 // plan; false when a supported width has a tile whose padded entries exceed a stage (very
 // high-degree rows: the CSR kernel handles those graphs).
 template <typename T>
-int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end, cudaStream_t s, bool* ok) {
+int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end, cudaStream_t s, bool* ok,
+                int64_t split_col) {
   constexpr int W = Vec<T>::W;
   *ok = false;
   if (width % W || !pick_sell<T>(width / W, g->unit_weights) || row_end - row_begin >= INT_MAX) return SC_OK;
   const int vpr = width / W;
-  if ((sell_tile_rows(vpr) * 2) % 16) return SC_OK;   // the tile's order segment must be a 16-byte bulk copy
   SellPlan* pl = nullptr;
-  SC_TRY(sell_plan(g, vpr, row_begin, row_end, s, &pl));
+  if (split_col > 0) {
+    SC_TRY(sell_plan(g, vpr, row_begin, row_end, s, &pl, 0, split_col));
+    if (sell_config(sell_tile_rows(vpr), g->unit_weights, pl->max_tile).cap <= 0) return SC_OK;
+    SC_TRY(sell_plan(g, vpr, row_begin, row_end, s, &pl, split_col, g->n_cols));
+  } else {
+    SC_TRY(sell_plan(g, vpr, row_begin, row_end, s, &pl));
+  }
   *ok = sell_config(sell_tile_rows(vpr), g->unit_weights, pl->max_tile).cap > 0;
   return SC_OK;
 }
-template int sell_usable<float>(const sc_graph*, int, int64_t, int64_t, cudaStream_t, bool*);
-template int sell_usable<double>(const sc_graph*, int, int64_t, int64_t, cudaStream_t, bool*);
+template int sell_usable<float>(const sc_graph*, int, int64_t, int64_t, cudaStream_t, bool*, int64_t);
+template int sell_usable<double>(const sc_graph*, int, int64_t, int64_t, cudaStream_t, bool*, int64_t);
+
+// Split gather for this chunk?  When the gathered block of one chunk (n_cols x width) is too
+// big for L2 but each half of it fits (configs[3], 32-column chunks: a 128 MB table in a 126 MB
+// L2, ~68 % hit rate), the columns are gathered in two launches per step -- first [0, mid),
+// row sums parked, then [mid, n_cols) and the epilogue -- each from a 64 MB half-table.
+// Returns the split column (0: no split).  env SC_SELL_SPLIT: 0 off, 1 auto (default), 2 force.
+int64_t sell_split_col(const sc_graph* g, int width, size_t elem) {
+  const int mode = env_int_s("SC_SELL_SPLIT", 1);
+  if (mode == 0) return 0;
+  const double table = (double)g->n_cols * width * elem;
+  const double lo = env_int_s("SC_SELL_SPLIT_MIN_MB", 96) * 1048576.0;
+  const double hi = env_int_s("SC_SELL_SPLIT_MAX_MB", 160) * 1048576.0;
+  if (mode == 2 || (table > lo && table <= hi)) return g->n_cols / 2;
+  return 0;
+}
 
 // One fused step over the SELL layout.  Requirements: T_s (p.tcur) has a zero row at index
 // g->n_cols (the sentinel of the padding); rows [row_begin, row_end) of one graph.
@@ -865,19 +1042,30 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
   if (!k) return fail(SC_ERR_ARG, "unsupported chunk width " + std::to_string(p.width));
   const int tr = sell_tile_rows(vpr);
   SellPlan* pl = nullptr;
-  SC_TRY(sell_plan(g, vpr, p.row_begin, p.row_end, s, &pl));
-  const SellCfg cf = sell_config(tr, g->unit_weights, pl->max_tile);
+  if (p.split_mode == 1) SC_TRY(sell_plan(g, vpr, p.row_begin, p.row_end, s, &pl, 0, p.split_col));
+  else if (p.split_mode == 2) SC_TRY(sell_plan(g, vpr, p.row_begin, p.row_end, s, &pl, p.split_col, g->n_cols));
+  else SC_TRY(sell_plan(g, vpr, p.row_begin, p.row_end, s, &pl));
+  SellCfg cf = sell_config(tr, g->unit_weights, pl->max_tile);
+  if (p.split_mode == 1 && cf.cap > 0) {   // no epilogue: no dense-row staging
+    cf.dense = false;
+    cf.smem = SellLayout(tr, cf.cap, g->unit_weights, cf.stages, false).total;
+  }
   if (cf.cap <= 0) return fail(SC_ERR_STATE, "SELL tile exceeds the stage capacity");
   const int cap = cf.cap;
   const int smem = static_cast<int>(cf.smem);
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> occ_cache;
+  static std::map<const void*, int> smem_attr;   // largest dynamic smem set per kernel
   int occ = 0;
   {
     std::lock_guard<std::mutex> lock(mu);
+    int& attr = smem_attr[(const void*)k];
+    if (smem > attr) {   // the attribute only grows: plans of one kernel differ in their smem
+      SC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = smem;
+    }
     auto it = occ_cache.find({(const void*)k, smem});
     if (it == occ_cache.end()) {
-      SC_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
       occ_cache[{(const void*)k, smem}] = occ;
     } else {
@@ -892,10 +1080,11 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
   sd.meta = pl->meta.as<int4>();
   sd.idx = pl->idx.as<int32_t>();
   sd.val = g->unit_weights ? nullptr : pl->val.as<float>();
-  sd.order = pl->order;
+  sd.order = pl->order.as<int32_t>();
   sd.hub_chunk_ptr = pl->hub_chunk_ptr.as<int32_t>();
-  if (pl->n_chunks > 0) {
-    // split rows first: one warp per chunk of a hub row's edges -> hubpart
+  if (pl->n_chunks > 0 && p.split_mode != 1) {
+    // split rows first: one warp per chunk of a hub row's edges -> hubpart (all of the row's
+    // columns, also under the split gather: its first launch leaves hub rows at 0)
     SC_TRY(pl->hubpart.ensure(sizeof(T) * (size_t)pl->n_chunks * p.width));
     sd.hubpart = pl->hubpart.ptr;
     HubFn<T> hk = pick_hub<T>(vpr, g->unit_weights);

@@ -141,10 +141,14 @@ CASES = [
 ]
 
 # streaming paths: "streaming" = the SELL kernel (large graphs' default; rows above the split
-# threshold of 512 go through hub_chunk_kernel), "split" = SELL with every row of degree > 4
-# split, "csr" = the plain-CSR step kernel (SC_SELL=0; moments and partitioned paths)
+# threshold of 128 go through hub_chunk_kernel), "split" = SELL with every row of degree > 4
+# split, "csr" = the plain-CSR step kernel (SC_SELL=0; moments and partitioned paths),
+# "halves" = the split gather
 PATHS = {"resident": {"SC_RESIDENT": "1"}, "streaming": {"SC_RESIDENT": "0"},
-         "split": {"SC_RESIDENT": "0", "SC_SELL_HUB_DEG": "4"}, "csr": {"SC_RESIDENT": "0", "SC_SELL": "0"}}
+         "split": {"SC_RESIDENT": "0", "SC_SELL_HUB_DEG": "4"}, "csr": {"SC_RESIDENT": "0", "SC_SELL": "0"},
+         # split gather: the columns in two halves, two launches per step (SC_SELL_SPLIT=2 forces
+         # it on small graphs; configs[3] takes it by default), with a sigma window of 256 rows
+         "halves": {"SC_RESIDENT": "0", "SC_SELL_SPLIT": "2", "SC_SELL_SIGMA": "256", "SC_SELL_HUB_DEG": "64"}}
 
 
 def _path_env(monkeypatch, path):
@@ -759,6 +763,37 @@ def test_partitioned_lambda_estimates_emulated(sc, world):
     finally:
         for pl in plans:
             sc.sc_dist_free(pl)
+        for c in comms:
+            sc.sc_comm_free(c)
+
+
+@pytest.mark.parametrize("world,n,k,d,restarts,spread", [(1, 2000, 4, 6, 2, 0.5), (2, 3000, 5, 8, 3, 0.5),
+                                                         (3, 20000, 12, 16, 2, 1.0), (4, 40000, 32, 48, 2, 1.0)])
+def test_dist_kmeans_emulated_bit_exact(sc, world, n, k, d, restarts, spread):
+    """sc_dist_kmeans (§4.1 step 6 on a row partition): all ranks held by this
+    process (sc_comm_local; one host thread and stream per rank, reductions at a host
+    rendezvous), uneven row blocks, against the oracle on the rank-major concatenation:
+    labels, centroids, iteration count and best restart bit-exact (exact integer member sums
+    reduced over the ranks; the last case takes the fp32 screen + Hamerly paths)."""
+    rng = np.random.default_rng(n + k)
+    centers = rng.standard_normal((k, d)) * 2.0
+    X = (centers[rng.integers(0, k, n)] + spread * rng.standard_normal((n, d))).astype(np.float32)
+    cuts = np.sort(rng.choice(np.arange(1, n), world - 1, replace=False)) if world > 1 else np.array([], int)
+    bounds = np.concatenate([[0], cuts, [n]]).astype(int)
+    comms = [sc.sc_comm_local(world, r) for r in range(world)]
+    try:
+        Fs = [torch.from_numpy(np.ascontiguousarray(X[bounds[r]:bounds[r + 1]])).cuda() for r in range(world)]
+        labs = [torch.full((bounds[r + 1] - bounds[r],), -1, dtype=torch.int32, device="cuda") for r in range(world)]
+        u = np.stack([scinputs.uniforms(9, k, offset=k * r) for r in range(restarts)])
+        C = np.zeros((k, d))
+        inertia, it, best = sc.sc_dist_kmeans(comms, Fs, d, k, restarts, 100, 0, u, labs, C)
+        lab = np.concatenate([x.cpu().numpy() for x in labs])
+        lo, Co, io, ito, ro, _ = kmeans.kmeans(X, k, u, 100)
+        assert np.array_equal(lab, lo)
+        assert np.array_equal(C, Co)
+        assert best == ro and it == ito
+        assert inertia == pytest.approx(io, rel=1e-12)
+    finally:
         for c in comms:
             sc.sc_comm_free(c)
 
