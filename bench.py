@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--col-groups", type=int, default=0,
                     help="multi-GPU: column groups of the 2-D decomposition (0 = auto: the most groups "
                          "with >= 32 columns each; 1 = pure row partition)")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="row-partitioned runs: also time the whole pipeline (PAPER.md §4.1 steps 1-6: lambda "
+                         "estimates, filter, k-means over the ranks; configs[4]'s 'full pipeline including "
+                         "k-means'); implies --col-groups 1 (k-means needs whole feature rows)")
     ap.add_argument("--dist-path", action="store_true",
                     help="use the row-partitioned NCCL filter even on one rank (exercises the multi-GPU path)")
     return ap.parse_args()
@@ -281,7 +285,7 @@ def run_ours(args):
         from paper_1509_08863_b200 import dist as pdist
         # 2-D decomposition: column group cgrp filters columns [c0, c1) of every row; its
         # n_row ranks row-partition the graph and exchange halos among themselves only
-        n_cg, n_row = pdist.grid_shape(world, R, col_groups=args.col_groups or None)
+        n_cg, n_row = pdist.grid_shape(world, R, col_groups=1 if args.pipeline else (args.col_groups or None))
         cgrp, rrank, _ = pdist.grid_coords(rank, world, n_cg)
         c0, c1 = pdist.column_range(R, n_cg, cgrp)
         groups = pdist.make_row_groups(world, n_cg)
@@ -476,6 +480,33 @@ def run_ours(args):
         out["e2e"] = {"value": work / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 4),
                       "d2h_bytes_per_step": int(Yh.numel() * 4), "ms_per_step": ems / args.steps,
                       "api": "sc_filter_lowpass_f32(host X, host Y)"}
+
+    # ---- the pipeline on the row partition (configs[4]'s "full pipeline including k-means"):
+    # lambda_N, lambda~_k, the partitioned filter, k-means over the ranks; time = max over ranks
+    if partitioned and args.pipeline and not args.no_cluster:
+        est2 = nf if isinstance(nf, pdist.NcclFilter) else pdist.NcclFilter(part, handle, group=rgroup)
+        filt = None if est2 is nf else nf.filter
+        est2.cluster(w.k, R, order, w.jackson, 32, args.seed, w.kmeans_restarts, 100, False, filt=filt)   # warm-up
+        barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        labs, cinfo = est2.cluster(w.k, R, order, w.jackson, 32, args.seed, w.kmeans_restarts, 100, False, filt=filt)
+        e1.record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+        cms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([wall, cms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall, cms = float(t[0]), float(t[1])
+        if est2 is not nf:
+            est2.close()
+        if rank == 0:
+            out["cluster_e2e"] = {"seconds": wall, "device_ms": cms, "k": w.k, "restarts": w.kmeans_restarts,
+                                  "lambda_max": cinfo["lambda_max"], "lambda_k": cinfo["lambda_k"],
+                                  "count_k": cinfo["count_k"], "kmeans_iters": cinfo["kmeans_iters"],
+                                  "api": f"dist pipeline on {world} ranks (sc_dist_lambda_max, "
+                                         f"sc_dist_estimate_lambda_k, {exchange} filter, sc_dist_kmeans)"}
 
     # ---- end-to-end clustering time (BASELINE metric: "end-to-end cluster time"): sc_cluster =
     # lambda_max (Lanczos) + lambda_k (moments + dichotomy) + filter + k-means, graph resident

@@ -1016,13 +1016,16 @@ int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end
 template int sell_usable<float>(const sc_graph*, int, int64_t, int64_t, cudaStream_t, bool*, int64_t);
 template int sell_usable<double>(const sc_graph*, int, int64_t, int64_t, cudaStream_t, bool*, int64_t);
 
-// Split gather for this chunk?  When the gathered block of one chunk (n_cols x width) is too
-// big for L2 but each half of it fits (configs[3], 32-column chunks: a 128 MB table in a 126 MB
-// L2, ~68 % hit rate), the columns are gathered in two launches per step -- first [0, mid),
-// row sums parked, then [mid, n_cols) and the epilogue -- each from a 64 MB half-table.
-// Returns the split column (0: no split).  env SC_SELL_SPLIT: 0 off, 1 auto (default), 2 force.
+// Split gather for this chunk?  The columns are gathered in two launches per step -- first
+// [0, mid), row sums parked, then [mid, n_cols) and the epilogue -- each from half the table,
+// meant for tables a little too big for L2 (configs[3], 32-column chunks: 128 MB in a 126 MB
+// L2, ~68 % hit rate).  Measured slower everywhere (configs[3] 104.0 -> 136.8 ms per pass,
+// fp64 201 -> 282 ms, weighted 104 -> 145 ms: each half pays the per-row work of all rows and
+// the halves' degrees pad more), so it is off by default.  Returns the split column (0: none).
+// env SC_SELL_SPLIT: 0 off (default), 1 auto (tables in (SC_SELL_SPLIT_MIN_MB,
+// SC_SELL_SPLIT_MAX_MB]), 2 force.
 int64_t sell_split_col(const sc_graph* g, int width, size_t elem) {
-  const int mode = env_int_s("SC_SELL_SPLIT", 1);
+  const int mode = env_int_s("SC_SELL_SPLIT", 0);
   if (mode == 0) return 0;
   const double table = (double)g->n_cols * width * elem;
   const double lo = env_int_s("SC_SELL_SPLIT_MIN_MB", 96) * 1048576.0;

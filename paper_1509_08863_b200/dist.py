@@ -174,116 +174,35 @@ def make_row_groups(world: int, n_col_groups: int):
     return [dist.new_group(list(range(c * n_row, (c + 1) * n_row))) for c in range(n_col_groups)]
 
 
-# ---------------------------------------------------------------------------
-# step schedule (coefficients per launch)
-# ---------------------------------------------------------------------------
-
-def step_schedule(order: int, d, lambda_max: float):
-    """Per-step arguments of the fused recurrence: T_{s+1} = a L T_s + b_cur T_s +
-    b_prev T_{s-1}; Y is updated when three terms are pending or at the last step."""
-    added = -1
-    for s in range(order):
-        last = s == order - 1
-        st = dict(s=s, a=(2.0 if s == 0 else 4.0) / lambda_max, b_cur=-1.0 if s == 0 else -2.0,
-                  b_prev=0.0 if s == 0 else -1.0, cy_prev=0.0, cy_cur=0.0, cy_next=0.0, y_mode=0,
-                  store_next=not last)
-        if last or (s + 1) - added == 3:
-            st["cy_prev"] = float(d[s - 1]) if (s >= 1 and added < s - 1) else 0.0
-            st["cy_cur"] = float(d[s]) if added < s else 0.0
-            st["cy_next"] = float(d[s + 1])
-            st["y_mode"] = 1 if added == -1 else 2
-            added = s + 1
-        yield st
-
-
-# ---------------------------------------------------------------------------
-# driver
-# ---------------------------------------------------------------------------
-
-class HaloExchange:
-    """all_to_all_single of the halo rows of a (n_local + n_halo) x R block."""
-
-    def __init__(self, part: LocalPart, R: int, device, dtype, group=None):
-        import torch
-        self.part, self.group, self.R = part, group, R
-        self.send_idx = torch.as_tensor(part.send_idx, dtype=torch.int64, device=device)
-        self.send_buf = torch.empty((int(part.send_idx.size), R), dtype=dtype, device=device)
-        self.recv_buf = torch.empty((part.n_halo, R), dtype=dtype, device=device)
-
-    def start(self, T):
-        import torch
-        import torch.distributed as dist
-        if self.part.world == 1:
-            return None
-        torch.index_select(T[: self.part.n_local], 0, self.send_idx, out=self.send_buf)
-        return dist.all_to_all_single(self.recv_buf, self.send_buf, self.part.recv_counts, self.part.send_counts,
-                                      group=self.group, async_op=True)
-
-    def finish(self, work, T):
-        if work is None:
-            return
-        work.wait()
-        T[self.part.n_local:].copy_(self.recv_buf)
-
-
-def run_filter(part: LocalPart, step_fn, d, order: int, lambda_max: float, X_local, group=None):
-    """Y_local = sum_j d_j T_j X restricted to this rank's rows (original local order).
-
-    step_fn(row_begin, row_end, T_prev, T_cur, T_next, Y, st) runs one fused step on
-    local rows [row_begin, row_end) of the permuted order (GPU: sc_cheb_step_f32)."""
+def _cluster_partition(sc, parts, plans, comms, filt, k, R, order, jackson, n_probe, seed, restarts, max_iter,
+                       normalize):
+    """The accelerated spectral clustering (§4.1 steps 1-6) on a row partition, one
+    library call per step: lambda_N (sc_dist_lambda_max), lambda~_k (sc_dist_estimate_lambda_k),
+    the coefficients, the seeded signals of the ranks' rows (the same block as sc_cluster:
+    stream 0, rows r0..r1 of the global block, permuted to local order), the filter (the
+    caller's partitioned filter), the optional row normalisation, k-means over the ranks
+    (sc_dist_kmeans, points in rank-major local order).  Random draws as sc_cluster.
+    Returns (labels per rank in local order, info dict)."""
     import torch
-    nl, nh = part.n_local, part.n_halo
-    R = X_local.shape[1]
-    dev, dt = X_local.device, X_local.dtype
-    perm = torch.as_tensor(part.perm, dtype=torch.int64, device=dev)
-    T0 = torch.zeros((nl + nh, R), dtype=dt, device=dev)
-    T0[:nl] = X_local.index_select(0, perm)
-    bufs = [torch.zeros((nl + nh, R), dtype=dt, device=dev) for _ in range(2)]   # T_j in bufs[j & 1]
-    Y = torch.empty((nl, R), dtype=dt, device=dev)
-    ex = HaloExchange(part, R, dev, dt, group)
-    for st in step_schedule(order, d, lambda_max):
-        s = st["s"]
-        T_cur = T0 if s == 0 else bufs[s & 1]
-        T_prev = None if s == 0 else (T0 if s == 1 else bufs[(s - 1) & 1])
-        T_next = bufs[(s + 1) & 1] if st["store_next"] else None
-        work = ex.start(T_cur)
-        step_fn(0, part.n_interior, T_prev, T_cur, T_next, Y, st)
-        ex.finish(work, T_cur)
-        step_fn(part.n_interior, nl, T_prev, T_cur, T_next, Y, st)
-    out = torch.empty_like(Y)
-    out[perm] = Y
-    return out
-
-
-def cuda_step_fn(handle):
-    """step_fn backed by the C ABI (fp32, device buffers)."""
-    from . import _lib
-
-    def fn(rb, re, T_prev, T_cur, T_next, Y, st):
-        if re <= rb:
-            return
-        R = T_cur.shape[1]
-        _lib.sc_cheb_step_f32(handle, rb, re, R, T_prev, R, T_cur, R, T_next, R, Y, R, st["a"], st["b_cur"],
-                              st["b_prev"], st["cy_prev"], st["cy_cur"], st["cy_next"], st["y_mode"])
-    return fn
-
-
-def filter_local_steps(handle, d, order, lambda_max, X, row_split=None):
-    """Single-GPU use of the per-step entry point over several row ranges (tests)."""
-    import torch
-    n, R = X.shape
-    split = list(row_split) if row_split else [0, n]
-    fn = cuda_step_fn(handle)
-    bufs = [torch.zeros_like(X) for _ in range(2)]
-    Y = torch.empty_like(X)
-    for st in step_schedule(order, d, lambda_max):
-        s = st["s"]
-        T_cur = X if s == 0 else bufs[s & 1]
-        T_prev = None if s == 0 else (X if s == 1 else bufs[(s - 1) & 1])
-        T_next = bufs[(s + 1) & 1] if st["store_next"] else None
-        for a, b in zip(split[:-1], split[1:]):
-            fn(a, b, T_prev, T_cur, T_next, Y, st)
-    return Y
+    row0 = [p.r0 for p in parts]
+    lmax = sc.sc_dist_lambda_max(plans, 60, 0.01, seed ^ 0x1A2B3C4D, row0)
+    lam_k, count_k = sc.sc_dist_estimate_lambda_k(plans, k, lmax, order, True, n_probe, seed ^ 0x5E5E5E5E, row0,
+                                                  40, 1e-4)
+    d = sc.sc_cheby_coeffs(lam_k, lmax, order, jackson)
+    Xs, Ys = [], []
+    for p in parts:
+        xb = torch.empty((p.n_local, R), dtype=torch.float32, device="cuda")
+        sc.sc_random_signals_f32(p.n_local, R, p.r0, seed, 0, 0.0, xb)
+        Xs.append(xb[torch.as_tensor(p.perm, device="cuda")].contiguous())
+        Ys.append(torch.empty_like(Xs[-1]))
+    filt(d, order, lmax, Xs, Ys)
+    if normalize:
+        for y in Ys:
+            sc.sc_normalize_rows_f32(y, y.shape[0], R)
+    labels = [torch.empty(p.n_local, dtype=torch.int32, device="cuda") for p in parts]
+    inertia, iters, best = sc.sc_dist_kmeans(comms, Ys, R, k, restarts, max_iter, seed, None, labels)
+    return labels, dict(lambda_max=lmax, lambda_k=lam_k, count_k=count_k, inertia=inertia, kmeans_iters=iters,
+                        best_restart=best)
 
 
 class NcclFilter:
@@ -305,6 +224,7 @@ class NcclFilter:
                                         np.asarray(part.send_counts, dtype=np.int64),
                                         np.asarray(part.recv_counts, dtype=np.int64))
         self.r0 = int(part.r0)   # counter offset of the rank's rows (start vector, probes)
+        self.part = part
 
     def filter(self, d, order: int, lambda_max: float, X, Y):
         self._lib.sc_dist_filter_f32(self.plan, d, order, lambda_max, X.shape[1], X, Y)
@@ -317,6 +237,18 @@ class NcclFilter:
     def estimate_lambda_k(self, k, lambda_max, order, jackson=True, n_probe=32, seed=0, max_iter=40, rtol=1e-4):
         return self._lib.sc_dist_estimate_lambda_k(self.plan, k, lambda_max, order, jackson, n_probe, seed,
                                                    [self.r0], max_iter, rtol)
+
+    def cluster(self, k, R, order, jackson=True, n_probe=32, seed=0, restarts=10, max_iter=100, normalize=False,
+                filt=None):
+        """PAPER.md §4.1 steps 1-6 for this rank (collective over the ranks; configs[4]'s
+        "full pipeline including k-means"): see _cluster_partition.  filt: the rank's
+        partitioned filter (default: this NCCL schedule)."""
+        part = self.part
+
+        def own_filter(d, order_, lmax, Xs, Ys):
+            (filt or self.filter)(d, order_, lmax, Xs[0], Ys[0])
+        return _cluster_partition(self._lib, [part], [self.plan], [self.comm], own_filter, k, R, order, jackson,
+                                  n_probe, seed, restarts, max_iter, normalize)
 
     def close(self):
         if getattr(self, "plan", None):
@@ -364,18 +296,6 @@ def p2p_descriptors(part: LocalPart, recv_counts_all):
     ptr = np.zeros(nl + 1, dtype=np.int64)
     np.cumsum(np.bincount(row, minlength=nl), out=ptr[1:])
     return ptr, row, peer, slot
-
-
-def p2p_scatter_reference(parts, T_locals):
-    """Host model of the fused exchange (tests): every rank's descriptors applied to its
-    local rows; returns each rank's halo block."""
-    rc_all = [p.recv_counts for p in parts]
-    halos = [np.zeros((p.n_halo,) + T_locals[p.rank].shape[1:], dtype=T_locals[p.rank].dtype) for p in parts]
-    for p in parts:
-        ptr, row, peer, slot = p2p_descriptors(p, rc_all)
-        for e in range(row.size):
-            halos[int(peer[e])][int(slot[e])] = T_locals[p.rank][int(row[e])]
-    return halos
 
 
 class P2PFilter:
@@ -433,13 +353,32 @@ class P2PGroup:
             for b in range(world):
                 if a != b:
                     sc.sc_p2p_link_local(self.handles[a], self.handles[b])
+        # the same partition as sc_dist plans on local (emulation) communicators: the lambda
+        # estimates and the distributed k-means of the pipeline
+        self.comms = [sc.sc_comm_local(world, r) for r in range(world)]
+        self.plans = [sc.sc_dist_create(self.graphs[r].handle, self.comms[r], p.n_interior, p.send_idx,
+                                        np.asarray(p.send_counts, dtype=np.int64),
+                                        np.asarray(p.recv_counts, dtype=np.int64))
+                      for r, p in enumerate(self.parts)]
+        self.world = world
 
     def filter(self, d, order, lambda_max, Xs, Ys, stream=None):
         self.sc.sc_p2p_filter_group_f32(self.handles, d, order, lambda_max, Xs[0].shape[1], Xs, Ys, stream)
+
+    def cluster(self, k, R, order, jackson=True, n_probe=32, seed=0, restarts=10, max_iter=100, normalize=False):
+        """PAPER.md §4.1 steps 1-6 on the partition (every rank held here): see _cluster_partition."""
+        return _cluster_partition(self.sc, self.parts, self.plans, self.comms, self.filter, k, R, order, jackson,
+                                  n_probe, seed, restarts, max_iter, normalize)
 
     def close(self):
         for h in self.handles:
             self.sc.sc_p2p_free(h)
         self.handles = []
+        for pl in getattr(self, "plans", []):
+            self.sc.sc_dist_free(pl)
+        self.plans = []
+        for c in getattr(self, "comms", []):
+            self.sc.sc_comm_free(c)
+        self.comms = []
         for g in self.graphs:
             g.close()

@@ -19,6 +19,8 @@ import torch.multiprocessing as mp
 import scinputs
 from oracle import chebyshev, laplacian
 
+import dist_reference as dref
+
 
 def _free_port():
     s = socket.socket()
@@ -65,7 +67,7 @@ def _worker(rank, world, port, gspec, R, order, q):
         d = chebyshev.filter_coeffs(0.15 * lmax, lmax, order, True)
         X = torch.from_numpy(scinputs.gaussian_block(5, g.n, R).astype(np.float64))
         Xl = X[part.r0:part.r1].contiguous()
-        Y = pdist.run_filter(part, _cpu_step_fn(part), d, order, lmax, Xl)
+        Y = dref.run_filter(part, _cpu_step_fn(part), d, order, lmax, Xl)
         parts = [None] * world
         dist.all_gather_object(parts, (part.r0, part.r1, Y.numpy(), part.n_interior, part.n_halo))
         if rank == 0:
@@ -106,7 +108,7 @@ def test_partition_and_schedule_pure():
     for order in [1, 2, 3, 4, 5, 9, 10]:
         d = np.arange(1, order + 2, dtype=float)
         seen = np.zeros(order + 1)
-        for st in pdist.step_schedule(order, d, 2.0):
+        for st in dref.step_schedule(order, d, 2.0):
             s = st["s"]
             if st["y_mode"]:
                 if s >= 1:
@@ -177,7 +179,7 @@ def test_p2p_scatter_reference_reproduces_halos(world):
     parts = [pdist.send_lists_from_halos(p, halos) for p in parts]
     X = scinputs.gaussian_block(2, g.n, 3)
     T_locals = [X[p.r0:p.r1][p.perm] for p in parts]
-    got = pdist.p2p_scatter_reference(parts, T_locals)
+    got = dref.p2p_scatter_reference(parts, T_locals)
     for p, h in zip(parts, got):
         assert np.array_equal(h, X[p.halo_gid])
 
@@ -205,7 +207,7 @@ def _grid_worker(rank, world, port, gspec, R, order, n_cg, q):
         d = chebyshev.filter_coeffs(0.15 * lmax, lmax, order, True)
         X = torch.from_numpy(scinputs.gaussian_block(5, g.n, R).astype(np.float64))
         Xl = X[part.r0:part.r1, c0:c1].contiguous()
-        Y = pdist.run_filter(part, _cpu_step_fn(part), d, order, lmax, Xl, group=groups[cgrp])
+        Y = dref.run_filter(part, _cpu_step_fn(part), d, order, lmax, Xl, group=groups[cgrp])
         outs = [None] * world
         dist.all_gather_object(outs, (part.r0, part.r1, c0, c1, Y.numpy(), rank in members))
         if rank == 0:

@@ -10,6 +10,7 @@ import os
 import numpy as np
 import pytest
 
+import dist_reference as dref
 import scinputs
 from oracle import ari as oari
 from oracle import chebyshev, eigencount, kmeans, lambda_max, laplacian, pipeline
@@ -245,7 +246,7 @@ def test_cheb_step_building_block_matches_filter(sc):
     d = chebyshev.filter_coeffs(0.1 * lmax, lmax, order, True)
     X = torch.from_numpy(scinputs.gaussian_block(8, g.n, R)).cuda()
     from paper_1509_08863_b200 import dist
-    Y = dist.filter_local_steps(G.handle, d, order, lmax, X, row_split=(0, 1000, g.n))
+    Y = dref.filter_local_steps(G.handle, d, order, lmax, X, row_split=(0, 1000, g.n))
     Yo = chebyshev.cheb_filter(laplacian.laplacian(g), X.cpu().numpy().astype(np.float64), d, lmax)
     assert rel(Y.cpu().numpy(), Yo) <= F32_TOL
 
@@ -675,7 +676,7 @@ def test_row_partitioned_steps_emulated_two_ranks(sc):
     for p in parts:
         pdist.send_lists_from_halos(p, halos)
     Gs = [sc.Graph(p.n_local, p.row_ptr, p.col_idx, p.values, n_cols=p.n_local + p.n_halo) for p in parts]
-    fns = [pdist.cuda_step_fn(G.handle) for G in Gs]
+    fns = [dref.cuda_step_fn(G.handle) for G in Gs]
     lmax = 2.0 * float(g.degrees().max())
     d = chebyshev.filter_coeffs(0.12 * lmax, lmax, order, True)
     X = scinputs.gaussian_block(41, g.n, R)
@@ -688,7 +689,7 @@ def test_row_partitioned_steps_emulated_two_ranks(sc):
         Ys.append(torch.empty((p.n_local, R), dtype=torch.float32, device="cuda"))
         off = np.concatenate([[0], np.cumsum(p.send_counts)])
         sends.append({q: torch.from_numpy(p.send_idx[off[q]:off[q + 1]]).cuda() for q in range(world)})
-    for st in pdist.step_schedule(order, d, lmax):
+    for st in dref.step_schedule(order, d, lmax):
         s = st["s"]
         cur = [T0[r] if s == 0 else bufs[r][s & 1] for r in range(world)]
         prev = [None if s == 0 else (T0[r] if s == 1 else bufs[r][(s - 1) & 1]) for r in range(world)]
@@ -796,6 +797,36 @@ def test_dist_kmeans_emulated_bit_exact(sc, world, n, k, d, restarts, spread):
     finally:
         for c in comms:
             sc.sc_comm_free(c)
+
+
+@pytest.mark.parametrize("world,normalize", [(2, False), (3, True)])
+def test_partitioned_pipeline_emulated(sc, world, normalize):
+    """PAPER.md §4.1 steps 1-6 on a row partition held by this process (dist.P2PGroup.cluster:
+    sc_dist_lambda_max, sc_dist_estimate_lambda_k, the fused-exchange filter, row
+    normalisation, sc_dist_kmeans) against the single-GPU sc_cluster on the same graph and
+    seed: lambda estimates agree to estimator accuracy, the partitions agree (ARI >= 0.99) and
+    recover the planted communities."""
+    from paper_1509_08863_b200 import dist as pdist
+    g = scinputs.sbm(3000, 5, 20, 0.05, seed=17)
+    k, R, order, npr, seed, restarts = 5, 32, 60, 32, 77, 5
+    G = sc.Graph.from_csr(g)
+    lab1 = np.zeros(g.n, dtype=np.int32)
+    info1 = sc.sc_cluster(G.handle, k, R, order, True, npr, seed, restarts, 100, normalize, lab1)
+    grp = pdist.P2PGroup(g.row_ptr, g.col_idx, g.values, g.n, world, R)
+    try:
+        labs, info = grp.cluster(k, R, order, True, npr, seed, restarts, 100, normalize)
+        torch.cuda.synchronize()
+        lab = np.zeros(g.n, dtype=np.int32)
+        for p, l in zip(grp.parts, labs):
+            lab[p.r0 + p.perm] = l.cpu().numpy()
+    finally:
+        grp.close()
+    ev = np.linalg.eigvalsh(laplacian.laplacian_dense(g))
+    assert ev[-1] <= info["lambda_max"] <= 1.02 * ev[-1]
+    assert info["lambda_max"] == pytest.approx(info1[0], rel=1e-3)
+    assert 4.5 <= info["count_k"] <= 5.5
+    assert oari.ari(lab, lab1) >= 0.99
+    assert oari.ari(lab, g.labels) > 0.95
 
 
 @pytest.mark.parametrize("world,R,chunk,waits", [(2, 16, None, False), (3, 6, None, False), (4, 16, "8", False),
