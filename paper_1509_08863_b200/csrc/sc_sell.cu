@@ -473,7 +473,7 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
 // has chunks.
 // ---------------------------------------------------------------------------
 constexpr int kHubChunk = 512;
-constexpr int kHubU = 8;   // gathers in flight per lane in hub_chunk_kernel
+constexpr int kHubU = 16;  // gathers in flight per lane in hub_chunk_kernel
 
 struct HubChunk {
   int64_t e0;     // first edge (CSR position)
@@ -508,12 +508,7 @@ hub_chunk_kernel(const HubChunk* __restrict__ chunks, int n_chunks, const int32_
 #pragma unroll
     for (int w = 0; w < W; ++w) acc[w] = T(0);
     if (sub < RPW) {
-      // kHubU independent gathers in flight per lane (one accumulator each, added in order)
-      T part[kHubU][W];
-#pragma unroll
-      for (int u = 0; u < kHubU; ++u)
-#pragma unroll
-        for (int w = 0; w < W; ++w) part[u][w] = T(0);
+      // kHubU gathers in flight per lane, added in edge order once the batch has landed
       for (int e0 = sub; e0 < ch.len; e0 += RPW * kHubU) {
         T v[kHubU][W];
         T wt[kHubU];
@@ -533,12 +528,8 @@ hub_chunk_kernel(const HubChunk* __restrict__ chunks, int n_chunks, const int32_
 #pragma unroll
         for (int u = 0; u < kHubU; ++u)
 #pragma unroll
-          for (int w = 0; w < W; ++w) part[u][w] = UNIT ? part[u][w] + v[u][w] : fma(wt[u], v[u][w], part[u][w]);
+          for (int w = 0; w < W; ++w) acc[w] = UNIT ? acc[w] + v[u][w] : fma(wt[u], v[u][w], acc[w]);
       }
-#pragma unroll
-      for (int u = 0; u < kHubU; ++u)
-#pragma unroll
-        for (int w = 0; w < W; ++w) acc[w] += part[u][w];
     }
     // groups added in group order by the lanes of group 0
 #pragma unroll
