@@ -230,10 +230,20 @@ def working_set(g, w):
     return 8 * (g.n + 1) + (8 if g.values is not None else 4) * g.nnz + 4 * 4 * g.n * w.R
 
 
+def components(g):
+    """Connected components of W (PAPER.md l.79 assumes a connected graph; the SBM generator
+    repairs connectivity only up to N = 2e5)."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import connected_components
+    A = sp.csr_matrix((np.ones(g.nnz, dtype=np.int8), g.col_idx, g.row_ptr), shape=(g.n, g.n))
+    return int(connected_components(A, directed=False, return_labels=False))
+
+
 def base_config(args, g, w, world):
     """The workload description both arms print (same keys)."""
     ws = working_set(g, w)
     return {"workload": args.workload, "N": g.n, "nnz_W": int(g.nnz), "nnz_L": int(g.nnz + g.n), "R": w.R,
+            "components": components(g),
             "order": w.order, "jackson": w.jackson, "graph_seed": args.seed,
             "l2": (f"inputs larger than L2 ({ws / 2**20:.0f} MB working set > 126 MB L2); no flush" if ws > 2 * L2_BYTES
                    else f"working set {ws / 2**20:.0f} MB fits L2: L2 flushed (256 MB write) before every timed step, "

@@ -93,7 +93,7 @@ def check_sass(lib: str) -> None:
     for ln in r.stdout.splitlines():
         if "Function :" in ln:
             fn = ln.split("Function :")[1].strip()
-        elif re.search(r"desc\[UR\d*[13579]\]", ln):
+        elif re.search(r"(?<![a-z])desc\[UR\d*[13579]\]", ln):   # memory descriptors only (not idesc/gdesc)
             bad.append(fn)
     if bad:
         os.remove(lib)

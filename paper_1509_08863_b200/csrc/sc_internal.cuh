@@ -332,6 +332,17 @@ struct Coll {
   virtual int max_u32(unsigned* p, size_t n, cudaStream_t s) = 0;
 };
 
+// tcgen05 assignment screen (sc_kmeans_tc.cu): the points (all, or the pruning list) grouped
+// by their current label, screened in centred coordinates on the tensor cores with a rigorous
+// bound; decided points get label / exact dmin / lo, the rest go to amb for the exact scan
+struct TcWork {
+  PoolBuf cnt, off, items, gperm;
+};
+bool tc_screen_supported(int k, int d);
+int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf, const double* cm, int k,
+              const int32_t* old_lab, const int32_t* list, const int* list_len, int32_t* lab, double* dmin,
+              double* lo, int32_t* amb, int* amb_len, TcWork& w, cudaStream_t s);
+
 // k-means over the rows of every rank (distributed Lloyd): the points are the
 // ranks' local rows in rank-major order (rank 0's n_0 rows, then rank 1's ...); row_off = this
 // rank's first global index, n_global = all ranks' rows.  Every rank returns the same

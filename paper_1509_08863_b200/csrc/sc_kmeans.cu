@@ -1465,6 +1465,10 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_CUDA_TRY(cudaFuncSetAttribute(d2_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_d2));
   SC_CUDA_TRY(cudaFuncSetAttribute(d2_update_skip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_d2));
 
+  // tensor-core screen (sc_kmeans_tc.cu) for the assignments after a restart's first (env
+  // SC_KMEANS_TC=0: the fp32 screen throughout)
+  const bool use_tc = screen && tc_screen_supported(k, d);
+  TcWork tcw;
   // Lloyd assignment of every point; host receives inertia (fixed-order sum of block
   // partials), the number of changed labels and the label histogram
   // Hamerly pruning pays off when a full assignment is expensive; small problems (many of
@@ -1498,10 +1502,17 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
         centroid_prep_kernel<<<1, 256, 0, s>>>(C, k, d, d_Cf, d_cm);
         SC_CUDA_TRY(cudaGetLastError());
       }
-      (screen_nbuf == 2 ? assign_screen_kernel<2> : assign_screen_kernel<1>)<<<(unsigned)((n + kSPT - 1) / kSPT),
-                                                                               256, smem_screen, s>>>(
-          F, n, d, C, d_Cf, d_cm, k, pruned ? b_list.as<int32_t>() : nullptr, pruned ? b_len.as<int>() : nullptr,
-          out_lab, b_dmin.as<double>(), b_lo.as<double>(), b_amb.as<int32_t>(), amb_len);
+      if (old && use_tc) {
+        // tensor-core screen in coordinates centred on each point's current centroid
+        SC_TRY(tc_screen(F, n, d, C, d_Cf, d_cm, k, old, pruned ? b_list.as<int32_t>() : nullptr,
+                         pruned ? b_len.as<int>() : nullptr, out_lab, b_dmin.as<double>(), b_lo.as<double>(),
+                         b_amb.as<int32_t>(), amb_len, tcw, s));
+      } else {
+        (screen_nbuf == 2 ? assign_screen_kernel<2> : assign_screen_kernel<1>)<<<(unsigned)((n + kSPT - 1) / kSPT),
+                                                                                 256, smem_screen, s>>>(
+            F, n, d, C, d_Cf, d_cm, k, pruned ? b_list.as<int32_t>() : nullptr, pruned ? b_len.as<int>() : nullptr,
+            out_lab, b_dmin.as<double>(), b_lo.as<double>(), b_amb.as<int32_t>(), amb_len);
+      }
       SC_CUDA_TRY(cudaGetLastError());
       assign3<<<(unsigned)list_grid, 256, smem_assign, s>>>(F, n, d, C, k, b_amb.as<int32_t>(), amb_len, out_lab,
                                                              b_dmin.as<double>(), b_lo.as<double>());
