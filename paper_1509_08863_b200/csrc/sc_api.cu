@@ -1,7 +1,10 @@
 // The C ABI (include/sc_b200.h): argument checking, host/device staging and
 // dispatch to the kernels.  Every entry point cites its PAPER.md passage in the
 // header.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -519,17 +522,38 @@ int sc_cluster(sc_graph* g, int k, int R, int order, int jackson, int n_probe, u
   SC_CHECK_ARG(k >= 1 && k < g->n_rows && R >= 1 && order >= 1 && n_probe >= 1 && restarts >= 1 && max_iter >= 1,
                "bad arguments");
   cudaStream_t s = as_stream(stream);
+  // env SC_CLUSTER_TRACE: per-phase device-synchronised times on stderr (tooling)
+  const bool trace = std::getenv("SC_CLUSTER_TRACE") != nullptr;
+  double t_ph[4] = {0, 0, 0, 0};
+  auto t_now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double t_mark = 0.0;
+  auto phase = [&](int i) -> int {
+    if (!trace) return SC_OK;
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+    const double t = t_now();
+    if (i >= 0) t_ph[i] = t - t_mark;
+    t_mark = t;
+    return SC_OK;
+  };
+  SC_TRY(phase(-1));
   double lmax = 0.0, lk = 0.0, ck = 0.0;
   SC_TRY(sc_lambda_max(g, 60, 0.01, seed ^ 0x1a2b3c4dULL, &lmax, stream));
+  SC_TRY(phase(0));
   SC_TRY(sc_estimate_lambda_k(g, k, lmax, order, 1, n_probe, seed ^ 0x5e5e5e5eULL, 40, 1e-4, &lk, &ck, stream));
+  SC_TRY(phase(1));
   DevBuf feats;
   SC_TRY(feats.ensure(sizeof(float) * g->n_rows * R));
   SC_TRY(sc_filter_lowpass_f32(g, lk, lmax, order, jackson, R, seed, nullptr, feats.as<float>(), stream));
   if (normalize) SC_TRY(normalize_rows_f32(feats.as<float>(), g->n_rows, R, s));
+  SC_TRY(phase(2));
   double inertia = 0.0;
   int it = 0, best = 0;
   SC_TRY(sc_kmeans(feats.as<float>(), g->n_rows, R, k, restarts, max_iter, seed, nullptr, labels, nullptr, &inertia,
                    &it, &best, stream));
+  SC_TRY(phase(3));
+  if (trace)
+    std::fprintf(stderr, "[sc_cluster] lambda_max %.4f s, lambda_k %.4f s, filter %.4f s, k-means %.4f s\n", t_ph[0],
+                 t_ph[1], t_ph[2], t_ph[3]);
   if (info) {
     info[0] = lmax;
     info[1] = lk;

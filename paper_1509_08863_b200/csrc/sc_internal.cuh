@@ -336,7 +336,7 @@ struct Coll {
 // by their current label, screened in centred coordinates on the tensor cores with a rigorous
 // bound; decided points get label / exact dmin / lo, the rest go to amb for the exact scan
 struct TcWork {
-  PoolBuf cnt, off, items, gperm;
+  PoolBuf cnt, off, items, gperm, panels, pscal, fix;
 };
 bool tc_screen_supported(int k, int d);
 int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf, const double* cm, int k,

@@ -19,22 +19,31 @@
 // ||x|| ||c_j||: the uncentred expanded form left 44 % of the configs[3] points undecided in
 // fp32.
 //
-// Bound (all in fp64, u = 2^-24, eps_s = 2^-10 + 2^-22 + (K + 2) 2^-23 (1 + 2^-10): tf32
-// rounding of both operands (cvt.rna: 2^-11 each) and a K-term fp32 accumulation in any order
-// with at worst truncating adds):
+// Bound (u = 2^-24, eps_s = 2^-10 + 2^-22 + (K + 2) 2^-23 (1 + 2^-10): tf32 rounding of both
+// operands (cvt.rna: 2^-11 each) and a K-term fp32 accumulation in any order with at worst
+// truncating adds):
 //   |S_j - y.z_j|            <= eps_s ||y|| ||z_j||
 //   delta_j (centring error) <= u (||y|| + ||c_a|| + ||z_j||) + 2^-51 C_m + tiny <= delta
 //                               (delta: the same with max_j ||z_j||)
-//   |D_j - rho_j^2|          <= 2 eps_s ||y|| ||z_j|| + 2 (||y|| + ||z_j|| + delta) delta
-//                               + delta^2 + 2^-49 (Y2 + Z2_j + 2 |S_j|)  =: E_j
-//   (the 2^-49 term covers the fp64 evaluation of D_j and E_j; every term is inflated by 1e-6)
-// with D_j = Y2 + Z2_j - 2 S_j (Y2, Z2_j the fp64 squared norms of the fp32 vectors) and rho_j
-// the exact distance of the fp32 point to the fp64 centroid.  The point is decided when
-// min_{j != b} (D_j - E_j) > (D_b + E_b)(1 + 1e-12), b = argmin D_j (the 1e-12 covers the fp64
-// evaluation of the winner's distance, as in the fp32 screen).  lo = sqrt of that minimum
-// (times 1 - 1e-12) is a lower bound of the distance to every other centroid (Hamerly).
+//   |D*_j - rho_j^2|         <= 2 eps_s ||y|| ||z_j|| + 2 (||y|| + ||z_j|| + delta) delta + delta^2
+//                             = Ea ||z_j|| + Eb0 =: E_j
+// with D*_j = Y2 + Z2_j - 2 S_j exactly (Y2, Z2_j the fp64 squared norms of the fp32 vectors;
+// their own fp64 rounding is ~2^-47 relative) and rho_j the exact distance of the fp32 point to
+// the fp64 centroid.  Ea, Eb0 are per point (fp64, inflated by 1e-6; Ea rounded up to fp32).
+// Per column the epilogue evaluates in fp32, with kappa = 2^-20,
+//   L_j = fma(-2 kappa, |S_j|, fma(-2, S_j, fma(-Ea, zn_j, W_j) + V)),
+//   W_j = fl32(fl32(Z2_j)(1 - kappa)),  zn_j >= ||z_j||,  V = fl32_down(Y2 (1 - kappa) - Eb0),
+// i.e. D*_j - E_j - kappa M_j (M_j = Y2 + Z2_j + 2 |S_j|) up to seven roundings of at most
+// 2^-24 M_j each (< 2^-21 M_j < kappa M_j), so L_j <= rho_j^2 rigorously.  With b = argmin_j L_j
+// and U = D*_b + E_b evaluated in fp64 from S_b (an upper bound of rho_b^2), the point is
+// decided when min_{j != b} L_j (1 - 1e-12) > U (1 + 1e-12): rho_b^2 is then below every other
+// rho_j^2 by a relative gap far larger than the fp64 evaluation of the distances in R8, so the
+// fp64 scan picks b too.  lo = sqrt of the left-hand side is a lower bound of the distance to
+// every other centroid (Hamerly).  Points with ||y||^2 or a ||z_j||^2 >= 1e30 (fp32 overflow)
+// are left undecided.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -76,12 +85,18 @@ struct TcArgs {
   const float* Cf;       // k x d (fp32 copies)
   const double* cm;      // max_c ||c|| (rounded up)
   int n_items_max;
-  const int* items;      // [item][2]: cluster, first position in gperm
+  const int* ioff;       // [k + 1] exclusive prefix of the clusters' tile counts (<= 128 points)
   const int* n_items;    // device
   const int64_t* goff;   // [k + 1] cluster offsets in gperm
   const int32_t* gperm;  // points grouped by current label
   int k, d, Dp, NT, tmem_cols;
   int v4;                // rows and centroids 16-byte aligned (d % 4 == 0): vector staging
+  const float* panels;   // [k][panel_floats]: per current cluster a, see tc_panel_kernel
+  const double* pscal;   // [k][16]: see tc_panel_kernel
+  int panel_floats;      // NT * Dp + 3 * NT
+  int* ctr;              // item-chunk counter (zeroed by group_plan_kernel)
+  int32_t* fix;          // decided points whose exact distance tc_fix_kernel computes
+  int* fix_len;
   int32_t* lab;
   double* dmin;
   double* lo;
@@ -89,17 +104,85 @@ struct TcArgs {
   int* amb_len;
 };
 
-__global__ void __launch_bounds__(kTM) assign_tc_kernel(TcArgs a) {
+constexpr int kPV = 16;   // prefetched 16-byte chunks per point (d <= 64)
+constexpr double kKappa = 0x1p-20;   // fp32 evaluation budget of the per-column bound (above)
+constexpr float kKappaF = 0x1p-20f;
+constexpr int kChunk = 2; // items a CTA takes per counter increment
+
+// shared-memory bytes of assign_tc_kernel
+__host__ __device__ inline size_t tc_smem_bytes(int NT, int Dp) {
+  return (size_t)(kTM + NT) * Dp * 4 + (size_t)(3 * NT + Dp) * 4 + (size_t)(kTM + Dp) * 8;
+}
+
+// Per-cluster panels, once per assignment (grid k x NT/32, a warp per 4 centroids): for the
+// current cluster a, the centred centroids z_j = fl32(c_j - c_a) rounded to tf32 in the MMA's
+// canonical K-major layout, then per column {W_j = fl32(fl32(||z_j||^2) (1 - kappa)), ||z_j||
+// rounded up to fp32}, then fl32(||z_j||^2); padding columns j >= k get W_j = +inf (never a
+// candidate).  The squared norms are fp64 sums of the fp32 (not yet tf32-rounded) z_j.
+// pscal[16 a]: ||c_a|| (1 + 1e-9); pscal[16 a + 1 + jb]: max ||z_j|| (fp64, times 1 + 1e-15)
+// over the block's 32 columns, +inf when a ||z_j||^2 overflows fp32.
+__global__ void __launch_bounds__(256) tc_panel_kernel(const double* __restrict__ C, int k, int d, int Dp, int NT,
+                                                       float* __restrict__ panels, double* __restrict__ pscal,
+                                                       int panel_floats) {
+  __shared__ double s_zn[32];
+  const int a = blockIdx.x, jb = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int KC = Dp / 4;
+  const double* cA = C + (size_t)a * d;
+  float* P = panels + (size_t)a * panel_floats;
+#pragma unroll 1
+  for (int r = 0; r < 4; ++r) {
+    const int jl = warp * 4 + r, j = jb * 32 + jl;
+    double s2 = 0.0;
+    for (int q = lane; q < Dp; q += 32) {
+      float z = 0.f;
+      if (j < k && q < d) z = (float)(C[(size_t)j * d + q] - cA[q]);
+      s2 += (double)z * (double)z;
+      P[canon(j, q, KC)] = to_tf32(z);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (lane == 0) {
+      const double zn = sqrt(s2) * (1.0 + 1e-15);
+      const float z2f = (float)s2;
+      const bool pad = j >= k;
+      P[NT * Dp + 2 * j] = pad ? INFINITY : __fmul_rn(z2f, 1.f - kKappaF);   // W_j
+      P[NT * Dp + 2 * j + 1] = pad ? 0.f : __double2float_ru(zn);
+      P[NT * Dp + 2 * NT + j] = z2f;
+      s_zn[jl] = (!pad && !(z2f < 1e30f)) ? (double)INFINITY : zn;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double zm = s_zn[lane], s2 = 0.0;
+    if (jb == 0)
+      for (int q = lane; q < d; q += 32) s2 += cA[q] * cA[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      zm = fmax(zm, __shfl_xor_sync(0xffffffffu, zm, o));
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      pscal[16 * (size_t)a + 1 + jb] = zm;
+      if (jb == 0) pscal[16 * (size_t)a] = sqrt(s2) * (1.0 + 1e-9);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   const int KC = a.Dp / 4;
   extern __shared__ __align__(1024) unsigned char tsm[];
   float* sA = reinterpret_cast<float*>(tsm);                    // [128][Dp] canonical
-  float* sB = sA + (size_t)kTM * a.Dp;                          // [NT][Dp] canonical
-  double* sZ2 = reinterpret_cast<double*>(sB + (size_t)a.NT * a.Dp);   // [NT]
-  double* sZn = sZ2 + a.NT;                                     // [NT]
-  double* sY2 = sZn + a.NT;                                     // [128]
+  float* sB = sA + (size_t)kTM * a.Dp;                          // [NT][Dp] canonical, then:
+  const float2* sWZ = reinterpret_cast<const float2*>(sB + (size_t)a.NT * a.Dp);   // [NT] {W_j, zn_j}
+  const float* sZ2f = sB + (size_t)a.NT * a.Dp + 2 * a.NT;      // [NT] fl32(||z_j||^2)
+  float* s_caf = sB + (size_t)a.NT * a.Dp + 3 * a.NT;           // [Dp] fl32(c_a)
+  double* sY2 = reinterpret_cast<double*>(s_caf + a.Dp);        // [128]
+  double* s_ca = sY2 + kTM;                                     // [Dp]: c_a (fp64)
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tmem_base;
   __shared__ double s_ca_norm, s_zmax;
+  __shared__ int s_zbad, s_chunk;
+  __shared__ int s_ioff[257];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
@@ -115,75 +198,116 @@ __global__ void __launch_bounds__(kTM) assign_tc_kernel(TcArgs a) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   const int items = *a.n_items;
+  for (int c = tid; c <= a.k; c += kTM) s_ioff[c] = a.ioff[c];
+  __syncthreads();
+  // tile i -> (cluster, first position): the last cluster whose prefix is <= i
+  auto tile_of = [&](int i, int& ca, int& start) {
+    int lo = 0, hi = a.k - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_ioff[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    ca = lo;
+    start = (i - s_ioff[lo]) * kTM;
+  };
   const double u = 0x1p-24;
   const double eps_s = 0x1p-10 + 0x1p-22 + (a.Dp + 2) * 0x1p-23 * (1.0 + 0x1p-10);
   const double Cm = *a.cm;
-  int cur = -1;   // cluster whose centred centroids sit in sB
+  const int nval = a.d / 4;
+  // d <= 64 with 16-byte rows: the next tile's rows are loaded into registers while the
+  // tensor cores and the epilogue work on the current one
+  const bool pref = a.v4 && nval <= kPV;
+  int cur = -1;   // cluster whose panel sits in sB
   uint32_t phase = 0;
-  // contiguous item ranges per CTA: consecutive items mostly share a cluster (centred
-  // centroids staged once per cluster)
-  const int per = (items + gridDim.x - 1) / gridDim.x;
-  const int it0 = blockIdx.x * per, it1 = min(items, it0 + per);
-  for (int it = it0; it < it1; ++it) {
-    const int ca = a.items[2 * it], start = a.items[2 * it + 1];
-    const int64_t cend = a.goff[ca + 1];
-    const int cnt = (int)min((int64_t)kTM, cend - (a.goff[ca] + start));
-    const int32_t* pts = a.gperm + a.goff[ca] + start;
-    // ---- centred centroids z_j = fl32(c_j - c_a), their squared norms (once per cluster)
+  // dynamic schedule: chunks of kChunk consecutive items (consecutive items mostly share a
+  // cluster, so the panel is staged about once per chunk or less)
+  if (tid == 0) s_chunk = atomicAdd(a.ctr, kChunk);
+  __syncthreads();
+  int it = s_chunk, chunk_end = min(items, it + kChunk);
+  float4 xv[kPV];
+  int64_t gi_next = -1;
+  auto prefetch = [&](int jt) {
+    int ca, start;
+    tile_of(jt, ca, start);
+    const int64_t g0 = a.goff[ca] + start;
+    const int cnt = (int)min((int64_t)kTM, a.goff[ca + 1] - g0);
+    gi_next = tid < cnt ? a.gperm[g0 + tid] : -1;
+    const float4* xr = reinterpret_cast<const float4*>(a.F + (gi_next >= 0 ? gi_next : 0) * a.d);
+#pragma unroll
+    for (int t = 0; t < kPV; ++t)
+      xv[t] = (gi_next >= 0 && t < nval) ? __ldg(xr + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  if (pref && it < items) prefetch(it);
+  while (it < items) {
+    int ca, start;
+    tile_of(it, ca, start);
+    const int64_t g0 = a.goff[ca] + start;
+    const int cnt = (int)min((int64_t)kTM, a.goff[ca + 1] - g0);
+    const int32_t* pts = a.gperm + g0;
+    // ---- the cluster's panel (tc_panel_kernel), c_a in fp64 and fp32
     if (ca != cur) {
-      const double* cA = a.C + (size_t)ca * a.d;
-      for (int e = tid; e < a.NT * a.Dp; e += kTM) {
-        const int j = e / a.Dp, q = e % a.Dp;
-        float z = 0.f;
-        if (j < a.k && q < a.d) z = (float)(a.C[(size_t)j * a.d + q] - cA[q]);
-        sB[canon(j, q, KC)] = z;   // rounded to tf32 below, after the norms
-      }
-      __syncthreads();
-      for (int j = tid; j < a.NT; j += kTM) {
-        double s2 = 0.0;
-        for (int q = 0; q < a.Dp; ++q) {
-          const double z = sB[canon(j, q, KC)];
-          s2 += z * z;
-        }
-        sZ2[j] = s2;
-        sZn[j] = sqrt(s2) * (1.0 + 1e-15);
+      const float* P = a.panels + (size_t)ca * a.panel_floats;
+      for (int e = tid; e < a.panel_floats / 4; e += kTM)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sB + 4 * e)), "l"(P + 4 * e)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      for (int q = tid; q < a.Dp; q += kTM) {
+        s_ca[q] = q < a.d ? a.C[(size_t)ca * a.d + q] : 0.0;
+        s_caf[q] = q < a.d ? a.Cf[(size_t)ca * a.d + q] : 0.f;
       }
       if (tid == 0) {
-        double s2 = 0.0;
-        for (int q = 0; q < a.d; ++q) s2 += cA[q] * cA[q];
-        s_ca_norm = sqrt(s2) * (1.0 + 1e-15);
-      }
-      __syncthreads();
-      if (tid == 0) {
+        const double* ps = a.pscal + 16 * (size_t)ca;
         double zm = 0.0;
-        for (int j = 0; j < a.NT; ++j) zm = fmax(zm, sZn[j]);
+        for (int jb = 0; jb < a.NT / 32; ++jb) zm = fmax(zm, ps[1 + jb]);
+        s_ca_norm = ps[0];
         s_zmax = zm;
+        s_zbad = isinf(zm);
       }
-      for (int e = tid; e < a.NT * a.Dp; e += kTM) {
-        const int j = e / a.Dp, q = e % a.Dp;
-        float* p = sB + canon(j, q, KC);
-        *p = to_tf32(*p);
-      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
       cur = ca;
     }
-    // ---- centred points y = fl32(x - fl32(c_a)), tf32 copies for the MMA, fp64 ||y||^2
-    // (a warp takes a row, lanes along it)
-    const float* cAf = a.Cf + (size_t)ca * a.d;
-    if (a.v4) {
-      // thread tid stages its own point (row tid = TMEM lane tid of the epilogue): its row's
-      // 16-byte chunks, up to 16 loads in flight, written to the canonical layout (the lanes
-      // of a warp fill four contiguous 128-byte runs: no bank conflicts)
+    // the item after this one: the next of the chunk, else the first of a new chunk (taken
+    // before the barrier below, read after it)
+    const bool last_of_chunk = it + 1 >= chunk_end;
+    if (last_of_chunk && tid == 0) s_chunk = atomicAdd(a.ctr, kChunk);
+    // ---- centred points y = fl32(x - fl32(c_a)), tf32 copies for the MMA, fp64 ||y||^2; with
+    // the prefetched rows also the exact (R8) distance to c_a, the usual winner
+    double acc_a = 0.0;
+    if (pref) {
+      const int r = tid;
+      double s2 = 0.0;
+#pragma unroll
+      for (int t = 0; t < kPV; ++t) {
+        if (t >= KC) break;
+        float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (t < nval) {
+          const float4 c = *reinterpret_cast<const float4*>(s_caf + 4 * t);
+          y = make_float4(__fsub_rn(xv[t].x, c.x), __fsub_rn(xv[t].y, c.y), __fsub_rn(xv[t].z, c.z),
+                          __fsub_rn(xv[t].w, c.w));
+          const float xs[4] = {xv[t].x, xv[t].y, xv[t].z, xv[t].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const double diff = __dsub_rn((double)xs[e], s_ca[4 * t + e]);
+            acc_a = __dadd_rn(acc_a, __dmul_rn(diff, diff));
+          }
+        }
+        s2 += (double)y.x * y.x + (double)y.y * y.y + (double)y.z * y.z + (double)y.w * y.w;
+        *reinterpret_cast<float4*>(sA + ((r & 7) + (r >> 3) * (8 * KC) + t * 8) * 4) =
+            make_float4(to_tf32(y.x), to_tf32(y.y), to_tf32(y.z), to_tf32(y.w));
+      }
+      sY2[r] = s2;
+    } else if (a.v4) {
       const int r = tid;
       const int64_t gi = r < cnt ? pts[r] : -1;
       const float4* xr = reinterpret_cast<const float4*>(a.F + (gi >= 0 ? gi : 0) * a.d);
-      const int nval = a.d / 4;
       double s2 = 0.0;
       for (int j0 = 0; j0 < KC; j0 += 16) {
-        float4 xv[16];
+        float4 xw[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
           const int j = j0 + t;
-          xv[t] = (gi >= 0 && j < nval) ? __ldg(xr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+          xw[t] = (gi >= 0 && j < nval) ? __ldg(xr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
@@ -191,9 +315,9 @@ __global__ void __launch_bounds__(kTM) assign_tc_kernel(TcArgs a) {
           if (j >= KC) break;
           float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
           if (gi >= 0 && j < nval) {
-            const float4 c = *reinterpret_cast<const float4*>(cAf + 4 * j);
-            y = make_float4(__fsub_rn(xv[t].x, c.x), __fsub_rn(xv[t].y, c.y), __fsub_rn(xv[t].z, c.z),
-                            __fsub_rn(xv[t].w, c.w));
+            const float4 c = *reinterpret_cast<const float4*>(s_caf + 4 * j);
+            y = make_float4(__fsub_rn(xw[t].x, c.x), __fsub_rn(xw[t].y, c.y), __fsub_rn(xw[t].z, c.z),
+                            __fsub_rn(xw[t].w, c.w));
           }
           s2 += (double)y.x * y.x + (double)y.y * y.y + (double)y.z * y.z + (double)y.w * y.w;
           *reinterpret_cast<float4*>(sA + ((r & 7) + (r >> 3) * (8 * KC) + j * 8) * 4) =
@@ -207,7 +331,7 @@ __global__ void __launch_bounds__(kTM) assign_tc_kernel(TcArgs a) {
         const int64_t gi = r < cnt ? pts[r] : -1;
         for (int q = lane; q < a.Dp; q += 32) {
           float y = 0.f;
-          if (gi >= 0 && q < a.d) y = __fsub_rn(a.F[gi * a.d + q], cAf[q]);
+          if (gi >= 0 && q < a.d) y = __fsub_rn(a.F[gi * a.d + q], s_caf[q]);
           s2 += (double)y * (double)y;
           sA[canon(r, q, KC)] = to_tf32(y);
         }
@@ -220,6 +344,11 @@ __global__ void __launch_bounds__(kTM) assign_tc_kernel(TcArgs a) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    int it_next = it + 1;
+    if (last_of_chunk) {
+      it_next = s_chunk;
+      chunk_end = min(items, it_next + kChunk);
+    }
     if (tid == 0) {
       const uint32_t id = idesc_tf32(kTM, a.NT);
       for (int ks = 0; ks < a.Dp / 8; ++ks) {   // one MMA per 8 tf32 of K (two 16-byte chunks)
@@ -235,6 +364,8 @@ __global__ void __launch_bounds__(kTM) assign_tc_kernel(TcArgs a) {
                        smem_u32(&bar))
                    : "memory");
     }
+    // the next tile's rows in flight during the MMA and the epilogue
+    if (pref && it_next < items) prefetch(it_next);
     asm volatile(
         "{\n.reg .pred P1;\nTCW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra TCW_%=;\n}\n" ::"r"(
             smem_u32(&bar)),
@@ -242,69 +373,118 @@ __global__ void __launch_bounds__(kTM) assign_tc_kernel(TcArgs a) {
         : "memory");
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // ---- epilogue: thread tid owns point tid (TMEM lane tid)
+    // ---- epilogue: thread tid owns point tid (TMEM lane tid); per column the fp32 lower
+    // bound L_j of rho_j^2 (bound above), tracking the smallest (index b, its S) and the
+    // second smallest
     const double Y2 = sY2[tid];
-    const double yn = sqrt(Y2) * (1.0 + 1e-15);
-    // E_j <= Ea zn_j + Eb0 + 2^-49 Z2_j + 2^-48 |S_j| with the centring error bounded by its
-    // largest value over j (zmax = max_j ||z_j||): fewer fp64 operations per column
+    const double yn = (double)__fsqrt_ru(__double2float_ru(Y2));   // >= ||y||
     const double dmx = u * (yn + s_ca_norm + s_zmax) + 0x1p-51 * Cm + 0x1p-120;
     const double Ea = (2.0 * eps_s * yn + 2.0 * dmx) * (1.0 + 1e-6);
-    const double Eb0 = (2.0 * (yn + dmx) * dmx + dmx * dmx + 0x1p-49 * Y2 + 0x1p-100) * (1.0 + 1e-6);
-    double Db = INFINITY, Eb = 0.0, m2 = INFINITY;
-    int b = -1;
-    for (int c0 = 0; c0 < a.NT; c0 += 8) {
-      uint32_t v[8];
+    const double Eb0 = (2.0 * (yn + dmx) * dmx + dmx * dmx + 0x1p-100) * (1.0 + 1e-6);
+    const float Eaf = __double2float_ru(Ea);
+    const float V = __double2float_rd(Y2 * (1.0 - kKappa) - Eb0);
+    // two independent chains (even / odd columns) for instruction-level parallelism
+    float L1e = INFINITY, L2e = INFINITY, Sbe = 0.f, L1o = INFINITY, L2o = INFINITY, Sbo = 0.f;
+    int be = -1, bo = -1;
+    const float4* sWZ2 = reinterpret_cast<const float4*>(sWZ);   // column pairs
+    for (int c0 = 0; c0 < a.NT; c0 += 32) {   // NT: a multiple of 32, padding columns L = +inf
+      uint32_t v[32];
       const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                   : "r"(taddr));
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int j = c0 + q;
-        if (j >= a.k) break;
-        const double S = (double)__uint_as_float(v[q]);
-        const double Z2 = sZ2[j];
-        const double D = Y2 + Z2 - 2.0 * S;
-        const double E = fma(Ea, sZn[j], Eb0) + 0x1p-49 * (1.0 + 1e-6) * Z2 + 0x1p-48 * (1.0 + 1e-6) * fabs(S);
-        if (D < Db) {
-          if (b >= 0) m2 = fmin(m2, Db - Eb);
-          b = j;
-          Db = D;
-          Eb = E;
-        } else {
-          m2 = fmin(m2, D - E);
-        }
+      for (int q = 0; q < 32; q += 2) {
+        const float4 wz = sWZ2[(c0 + q) >> 1];   // {W_j, zn_j, W_j+1, zn_j+1}
+        const float S0 = __uint_as_float(v[q]), S1 = __uint_as_float(v[q + 1]);
+        const float L0 = fmaf(-2.f * kKappaF, fabsf(S0), fmaf(-2.f, S0, fmaf(-Eaf, wz.y, wz.x) + V));
+        const float Lx = fmaf(-2.f * kKappaF, fabsf(S1), fmaf(-2.f, S1, fmaf(-Eaf, wz.w, wz.z) + V));
+        L2e = fminf(L2e, fmaxf(L1e, L0));
+        const bool lte = L0 < L1e;
+        L1e = fminf(L1e, L0);
+        Sbe = lte ? S0 : Sbe;
+        be = lte ? c0 + q : be;
+        L2o = fminf(L2o, fmaxf(L1o, Lx));
+        const bool lto = Lx < L1o;
+        L1o = fminf(L1o, Lx);
+        Sbo = lto ? S1 : Sbo;
+        bo = lto ? c0 + q + 1 : bo;
       }
     }
+    const float L2 = fminf(fminf(L2e, L2o), fmaxf(L1e, L1o));
+    const bool odd = L1o < L1e;
+    const float Sb = odd ? Sbo : Sbe;
+    const int b = odd ? bo : be;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     if (tid < cnt) {
       const int64_t gi = pts[tid];
-      const double up = (Db + Eb) * (1.0 + 1e-12);
-      const double low = (a.k == 1) ? (double)INFINITY : m2 * (1.0 - 1e-12);
-      if (b >= 0 && low > up) {
-        // proven unique argmin: its exact distance with the scan's arithmetic (R8)
-        const double* c = a.C + (size_t)b * a.d;
-        const float* x = a.F + gi * a.d;
-        double acc = 0.0;
-        for (int q = 0; q < a.d; ++q) {
-          const double diff = __dsub_rn((double)__ldg(x + q), c[q]);
-          acc = __dadd_rn(acc, __dmul_rn(diff, diff));
-        }
+      bool ok = b >= 0 && Y2 < 1e30 && !s_zbad;
+      double low = (double)INFINITY;
+      if (ok) {
+        // upper bound of rho_b^2 in fp64: D*_b + E_b with ||z_b||^2 <= fl32(.)(1 + 2^-23)
+        const double Z2b = (double)sZ2f[b] * (1.0 + 0x1p-23);
+        const double Sd = (double)Sb;
+        const double up = (Y2 + Z2b - 2.0 * Sd + Ea * (double)sWZ[b].y + Eb0 +
+                           0x1p-40 * (Y2 + Z2b + 2.0 * fabs(Sd))) * (1.0 + 1e-12) + 0x1p-100;
+        if (a.k > 1) low = (double)L2 * (1.0 - 1e-12);
+        ok = low > up;
+      }
+      if (ok) {
+        // proven unique argmin; its exact distance with the scan's arithmetic (R8): computed
+        // during staging when b == a (prefetch path), else by tc_fix_kernel
         a.lab[gi] = b;
-        a.dmin[gi] = acc;
-        a.lo[gi] = isinf(low) ? (double)INFINITY : sqrt(fmax(low, 0.0));
+        a.lo[gi] = isinf(low) ? (double)INFINITY : sqrt(low);
+        if (pref && b == ca) a.dmin[gi] = acc_a;
+        else a.fix[atomicAdd(a.fix_len, 1)] = static_cast<int32_t>(gi);
       } else {
         a.amb[atomicAdd(a.amb_len, 1)] = static_cast<int32_t>(gi);
       }
     }
-    __syncthreads();   // sA / TMEM reused by the next tile
+    __syncthreads();   // sA / TMEM / s_chunk reused by the next tile
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    it = it_next;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
+}
+
+// exact (R8) distance of the decided points whose winner is not their current cluster
+__global__ void __launch_bounds__(256) tc_fix_kernel(const float* __restrict__ F, const double* __restrict__ C, int d,
+                                                     int v4, const int32_t* __restrict__ lab,
+                                                     const int32_t* __restrict__ fix, const int* __restrict__ fix_len,
+                                                     double* __restrict__ dmin) {
+  const int m = *fix_len;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int64_t gi = fix[i];
+    const double* c = C + (size_t)lab[gi] * d;
+    const float* x = F + gi * d;
+    double acc = 0.0;
+    if (v4) {
+      for (int q0 = 0; q0 < d; q0 += 4) {
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(x + q0));
+        const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double diff = __dsub_rn((double)xs[e], c[q0 + e]);
+          acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+        }
+      }
+    } else {
+      for (int q = 0; q < d; ++q) {
+        const double diff = __dsub_rn((double)__ldg(x + q), c[q]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+      }
+    }
+    dmin[gi] = acc;
+  }
 }
 
 // ---- grouping of the points to screen by their current label (counting sort).  Shared-
@@ -328,49 +508,39 @@ __global__ void __launch_bounds__(256) group_hist_kernel(const int32_t* __restri
     if (sh_cnt[c]) atomicAdd(&cnt[c], sh_cnt[c]);
 }
 
-// offsets (exclusive scan of the counts), work items (cluster, first position) of <= 128
-// points, cursors zeroed; one block
+// offsets (exclusive scan of the counts) and the tiles' prefix ioff (tiles of <= 128 points
+// of one cluster), cursors and counters zeroed; one block, k <= 256
 __global__ void __launch_bounds__(256) group_plan_kernel(const unsigned* __restrict__ cnt, int k,
                                                          int64_t* __restrict__ off, unsigned* __restrict__ cursor,
-                                                         int* __restrict__ items, int* __restrict__ n_items) {
+                                                         int* __restrict__ ioff, int* __restrict__ n_items,
+                                                         int* __restrict__ ctr, int* __restrict__ fix_len) {
   __shared__ long long s_c[256];
   __shared__ int s_i[256];
-  __shared__ long long carry;
-  __shared__ int carry_i;
   const int tid = threadIdx.x;
-  if (tid == 0) { carry = 0; carry_i = 0; }
+  const long long cc = tid < k ? (long long)cnt[tid] : 0;
+  const int ni = (int)((cc + kTM - 1) / kTM);
+  s_c[tid] = cc;
+  s_i[tid] = ni;
   __syncthreads();
-  for (int base = 0; base < k; base += 256) {
-    const int c = base + tid;
-    const long long cc = c < k ? (long long)cnt[c] : 0;
-    const int ni = (int)((cc + kTM - 1) / kTM);
-    s_c[tid] = cc;
-    s_i[tid] = ni;
+  for (int o = 1; o < 256; o <<= 1) {
+    const long long x = tid >= o ? s_c[tid - o] : 0;
+    const int y = tid >= o ? s_i[tid - o] : 0;
     __syncthreads();
-    for (int o = 1; o < 256; o <<= 1) {
-      const long long x = tid >= o ? s_c[tid - o] : 0;
-      const int y = tid >= o ? s_i[tid - o] : 0;
-      __syncthreads();
-      s_c[tid] += x;
-      s_i[tid] += y;
-      __syncthreads();
-    }
-    if (c < k) {
-      off[c] = carry + s_c[tid] - cc;
-      cursor[c] = 0u;
-      const int i0 = carry_i + s_i[tid] - ni;
-      for (int t = 0; t < ni; ++t) {
-        items[2 * (i0 + t)] = c;
-        items[2 * (i0 + t) + 1] = t * kTM;
-      }
-    }
-    __syncthreads();
-    if (tid == 255) { carry += s_c[255]; carry_i += s_i[255]; }
+    s_c[tid] += x;
+    s_i[tid] += y;
     __syncthreads();
   }
+  if (tid < k) {
+    off[tid] = s_c[tid] - cc;
+    ioff[tid] = s_i[tid] - ni;
+    cursor[tid] = 0u;
+  }
   if (tid == 0) {
-    off[k] = carry;
-    *n_items = carry_i;
+    off[k] = s_c[255];
+    ioff[k] = s_i[255];
+    *n_items = s_i[255];
+    *ctr = 0;
+    *fix_len = 0;
   }
 }
 
@@ -406,30 +576,38 @@ __global__ void __launch_bounds__(256) group_scatter_kernel(const int32_t* __res
 bool tc_screen_supported(int k, int d) {
   const char* e = std::getenv("SC_KMEANS_TC");
   if (e && std::atoi(e) == 0) return false;
-  const int NT = (k + 7) / 8 * 8, Dp = (d + 7) / 8 * 8;
-  const size_t smem = (size_t)(kTM + NT) * Dp * 4 + (size_t)(2 * NT + kTM) * 8;
+  const int NT = (k + 31) / 32 * 32, Dp = (d + 7) / 8 * 8;
+  const size_t smem = tc_smem_bytes(NT, Dp);
   return k >= 2 && NT <= 256 && smem <= 200 * 1024;
 }
 
 int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf, const double* cm, int k,
               const int32_t* old_lab, const int32_t* list, const int* list_len, int32_t* lab, double* dmin,
               double* lo, int32_t* amb, int* amb_len, TcWork& w, cudaStream_t s) {
-  const int NT = (k + 7) / 8 * 8, Dp = (d + 7) / 8 * 8;
+  const int NT = (k + 31) / 32 * 32, Dp = (d + 7) / 8 * 8;
   const int max_items = (int)((n + kTM - 1) / kTM) + k;
   SC_TRY(w.cnt.ensure(sizeof(unsigned) * 2 * (size_t)k, s));
   SC_TRY(w.off.ensure(sizeof(int64_t) * (size_t)(k + 1), s));
-  SC_TRY(w.items.ensure(sizeof(int) * (2 * (size_t)max_items + 1), s));
+  SC_TRY(w.items.ensure(sizeof(int) * ((size_t)k + 4), s));   // ioff[k + 1], n_items, ctr, fix_len
+  SC_TRY(w.fix.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(1, n), s));
+  const int panel_floats = NT * Dp + 3 * NT;
+  SC_TRY(w.panels.ensure(sizeof(float) * (size_t)k * panel_floats, s));
+  SC_TRY(w.pscal.ensure(sizeof(double) * 16 * (size_t)k, s));
   SC_TRY(w.gperm.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(1, n), s));
   unsigned* cnt = w.cnt.as<unsigned>();
   unsigned* cursor = cnt + k;
-  int* n_items = w.items.as<int>() + 2 * (size_t)max_items;
+  int* n_items = w.items.as<int>() + (size_t)k + 1;
+  int* ctr = n_items + 1;
+  int* fix_len = n_items + 2;
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   SC_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * k, s));
   const int pgrid = (int)std::max<int64_t>(1, (n + kGChunk - 1) / kGChunk);   // (list: <= n entries)
   group_hist_kernel<<<pgrid, 256, sizeof(unsigned) * k, s>>>(old_lab, list, list_len, n, k, cnt);
-  group_plan_kernel<<<1, 256, 0, s>>>(cnt, k, w.off.as<int64_t>(), cursor, w.items.as<int>(), n_items);
+  group_plan_kernel<<<1, 256, 0, s>>>(cnt, k, w.off.as<int64_t>(), cursor, w.items.as<int>(), n_items, ctr, fix_len);
+  tc_panel_kernel<<<dim3(k, NT / 32), 256, 0, s>>>(C, k, d, Dp, NT, w.panels.as<float>(), w.pscal.as<double>(),
+                                                    panel_floats);
   group_scatter_kernel<<<pgrid, 256, sizeof(unsigned) * 3 * k, s>>>(old_lab, list, list_len, n, k,
                                                                     w.off.as<int64_t>(), cursor,
                                                                     w.gperm.as<int32_t>());
@@ -440,7 +618,7 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   a.Cf = Cf;
   a.cm = cm;
   a.n_items_max = max_items;
-  a.items = w.items.as<int>();
+  a.ioff = w.items.as<int>();
   a.n_items = n_items;
   a.goff = w.off.as<int64_t>();
   a.gperm = w.gperm.as<int32_t>();
@@ -450,22 +628,42 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   a.NT = NT;
   a.tmem_cols = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
   a.v4 = (d % 4 == 0) && ((uintptr_t)F % 16 == 0) && ((uintptr_t)Cf % 16 == 0);
+  a.panels = w.panels.as<float>();
+  a.pscal = w.pscal.as<double>();
+  a.panel_floats = panel_floats;
+  a.ctr = ctr;
+  a.fix = w.fix.as<int32_t>();
+  a.fix_len = fix_len;
   a.lab = lab;
   a.dmin = dmin;
   a.lo = lo;
   a.amb = amb;
   a.amb_len = amb_len;
-  const int smem = (int)((size_t)(kTM + NT) * Dp * 4 + (size_t)(2 * NT + kTM) * 8);
+  const int smem = (int)tc_smem_bytes(NT, Dp);
   static int attr = 0;
   if (smem > attr) {
     SC_CUDA_TRY(cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = 200 * 1024;
   }
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, assign_tc_kernel, kTM, smem);
-  occ = std::max(1, std::min(occ, 512 / a.tmem_cols));   // TMEM: 512 columns per SM
+  // resident CTAs per SM: shared memory (228 KB per SM, 1 KB reserved per CTA) and TMEM
+  // (512 columns per SM)
+  // (computed here: the occupancy API answered 1 for this kernel where the hardware fits 3,
+  // ncu "Block Limit Shared Mem" / "Block Limit Registers" = 3 / 4 at k = 100, d = 64)
+  static int carve = 0;
+  if (!carve) {
+    SC_CUDA_TRY(cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    carve = 1;
+  }
+  cudaFuncAttributes fa{};
+  SC_CUDA_TRY(cudaFuncGetAttributes(&fa, assign_tc_kernel));
+  const int regs_cta = std::max(1, fa.numRegs) * kTM;
+  int occ = std::min((227 * 1024) / (smem + (int)fa.sharedSizeBytes + 1024), 65536 / regs_cta);
+  occ = std::max(1, std::min(occ, 512 / a.tmem_cols));
+  if (std::getenv("SC_KMEANS_TRACE")) std::fprintf(stderr, "[sc_kmeans] tensor screen: %d CTAs per SM, smem %d B\n", occ, smem);
   const int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * occ);
   assign_tc_kernel<<<grid, kTM, smem, s>>>(a);
+  SC_CUDA_TRY(cudaGetLastError());
+  tc_fix_kernel<<<sms * 2, 256, 0, s>>>(F, C, d, a.v4, lab, a.fix, fix_len, dmin);
   SC_CUDA_TRY(cudaGetLastError());
   return SC_OK;
 }
