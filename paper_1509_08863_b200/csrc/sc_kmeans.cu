@@ -641,6 +641,84 @@ __global__ void __launch_bounds__(256) assign3_kernel(const float* __restrict__ 
   }
 }
 
+// Exact scan of a short list of points (the screens' ambiguous points): one warp per point,
+// lane l owns centroids l, l + 32, l + 64, l + 96 (four independent fp64 chains), the
+// centroids transposed in shared memory ([d][k], loaded once per block), the point's row
+// broadcast from a per-warp shared-memory copy.  Same arithmetic and decisions as
+// assign3_kernel: sum_q (x_q - c_q)^2 in ascending q with __dsub_rn/__dmul_rn/__dadd_rn, first
+// minimum (lowest index on ties), second-smallest distance -> lo (R8).  Used when
+// k <= 128 and k d doubles fit in shared memory; the tile kernel above serves the rest.
+constexpr int kAmbK = 128;   // centroids per point pass: 4 per lane
+__global__ void __launch_bounds__(256) amb_scan_kernel(const float* __restrict__ F, int d,
+                                                       const double* __restrict__ C, int k,
+                                                       const int32_t* __restrict__ list,
+                                                       const int* __restrict__ list_len,
+                                                       int32_t* __restrict__ lab, double* __restrict__ dmin,
+                                                       double* __restrict__ lo) {
+  extern __shared__ double smA[];
+  double* sCt = smA;                          // [d][k]
+  double* sXw = smA + (size_t)d * k;          // [8 warps][d]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = *list_len;
+  if ((int64_t)blockIdx.x * 8 >= m) return;
+  for (int e = tid; e < k * d; e += 256) {
+    const int j = e / d, q = e - j * d;
+    sCt[(size_t)q * k + j] = C[e];
+  }
+  __syncthreads();
+  double* xw = sXw + (size_t)warp * d;
+  for (int pi = blockIdx.x * 8 + warp; pi < m; pi += gridDim.x * 8) {
+    const int64_t gi = list[pi];
+    for (int q = lane; q < d; q += 32) xw[q] = (double)__ldg(F + gi * d + q);
+    __syncwarp();
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const bool v0 = lane < k, v1 = lane + 32 < k, v2 = lane + 64 < k, v3 = lane + 96 < k;
+    const double* c0 = sCt + (v0 ? lane : 0);
+    const double* c1 = sCt + (v1 ? lane + 32 : 0);
+    const double* c2 = sCt + (v2 ? lane + 64 : 0);
+    const double* c3 = sCt + (v3 ? lane + 96 : 0);
+#pragma unroll 4
+    for (int q = 0; q < d; ++q) {
+      const double x = xw[q];
+      const size_t o = (size_t)q * k;
+      const double d0 = __dsub_rn(x, c0[o]), d1 = __dsub_rn(x, c1[o]);
+      const double d2 = __dsub_rn(x, c2[o]), d3 = __dsub_rn(x, c3[o]);
+      acc[0] = __dadd_rn(acc[0], __dmul_rn(d0, d0));
+      acc[1] = __dadd_rn(acc[1], __dmul_rn(d1, d1));
+      acc[2] = __dadd_rn(acc[2], __dmul_rn(d2, d2));
+      acc[3] = __dadd_rn(acc[3], __dmul_rn(d3, d3));
+    }
+    __syncwarp();   // xw reused by the warp's next point
+    // this lane's centroids in ascending index, then the (dist, index) lexicographic min over
+    // the warp with the second-smallest distance merged (as assign3_kernel)
+    double best = INFINITY, second = INFINITY;
+    int bidx = -1;
+    const bool valid[4] = {v0, v1, v2, v3};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (!valid[t]) continue;
+      const double v = acc[t];
+      if (v < best) { second = best; best = v; bidx = lane + 32 * t; }
+      else if (v < second) second = v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const double os = __shfl_xor_sync(0xffffffffu, second, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      const bool take = (oi >= 0) && (bidx < 0 || ob < best || (ob == best && oi < bidx));
+      const double loser = take ? best : ob;
+      second = fmin(fmin(second, os), loser);
+      if (take) { best = ob; bidx = oi; }
+    }
+    if (lane == 0) {
+      lab[gi] = bidx < 0 ? 0 : bidx;   // all distances NaN/inf: deterministic fallback
+      dmin[gi] = best;
+      lo[gi] = sqrt(second);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Screened assignment: an fp32 pass finds, for every point, the nearest and second-nearest
 // centroid under approximate distances R~ = fl32(sum_q fma((x_q - c~_q)^2)) (c~ = fp32(c)),
@@ -1443,6 +1521,18 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   }
   auto assign3 = nc_best == 4 ? assign3_kernel<4> : nc_best == 2 ? assign3_kernel<2> : assign3_kernel<1>;
   SC_CUDA_TRY(cudaFuncSetAttribute(assign3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
+  // the screens' ambiguous points: warp-per-point scan when the centroids fit in shared memory
+  // (env SC_KMEANS_AMB_WARP=0: the tile kernel)
+  const int smem_amb = (int)(sizeof(double) * ((size_t)k * d + 8 * (size_t)d));
+  const bool amb_direct = k <= kAmbK && smem_amb <= 100 * 1024 &&
+                          !(std::getenv("SC_KMEANS_AMB_WARP") && std::atoi(std::getenv("SC_KMEANS_AMB_WARP")) == 0);
+  int64_t amb_grid = 1;
+  if (amb_direct) {
+    SC_CUDA_TRY(cudaFuncSetAttribute(amb_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_amb));
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, amb_scan_kernel, 256, smem_amb);
+    amb_grid = (int64_t)sms * std::max(1, occ);
+  }
   // double-buffered centroid tiles unless that drops the screen below 3 blocks per SM (d > ~70)
   int smem_sm = 0, cur_dev = 0;
   cudaGetDevice(&cur_dev);
@@ -1514,8 +1604,13 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
             out_lab, b_dmin.as<double>(), b_lo.as<double>(), b_amb.as<int32_t>(), amb_len);
       }
       SC_CUDA_TRY(cudaGetLastError());
-      assign3<<<(unsigned)list_grid, 256, smem_assign, s>>>(F, n, d, C, k, b_amb.as<int32_t>(), amb_len, out_lab,
-                                                             b_dmin.as<double>(), b_lo.as<double>());
+      if (amb_direct) {
+        amb_scan_kernel<<<(unsigned)amb_grid, 256, smem_amb, s>>>(F, d, C, k, b_amb.as<int32_t>(), amb_len, out_lab,
+                                                                   b_dmin.as<double>(), b_lo.as<double>());
+      } else {
+        assign3<<<(unsigned)list_grid, 256, smem_assign, s>>>(F, n, d, C, k, b_amb.as<int32_t>(), amb_len, out_lab,
+                                                               b_dmin.as<double>(), b_lo.as<double>());
+      }
       if (trace_len) {
         int h_len[3] = {0, 0, 0};
         SC_CUDA_TRY(cudaMemcpyAsync(h_len, b_len.ptr, sizeof(h_len), cudaMemcpyDeviceToHost, s));

@@ -107,7 +107,7 @@ struct TcArgs {
 constexpr int kPV = 16;   // prefetched 16-byte chunks per point (d <= 64)
 constexpr double kKappa = 0x1p-20;   // fp32 evaluation budget of the per-column bound (above)
 constexpr float kKappaF = 0x1p-20f;
-constexpr int kChunk = 2; // items a CTA takes per counter increment
+constexpr int kChunk = 4; // items a CTA takes per counter increment
 
 // shared-memory bytes of assign_tc_kernel
 __host__ __device__ inline size_t tc_smem_bytes(int NT, int Dp) {
@@ -226,9 +226,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   int it = s_chunk, chunk_end = min(items, it + kChunk);
   float4 xv[kPV];
   int64_t gi_next = -1;
-  auto prefetch = [&](int jt) {
-    int ca, start;
-    tile_of(jt, ca, start);
+  auto prefetch = [&](int ca, int start) {
     const int64_t g0 = a.goff[ca] + start;
     const int cnt = (int)min((int64_t)kTM, a.goff[ca + 1] - g0);
     gi_next = tid < cnt ? a.gperm[g0 + tid] : -1;
@@ -237,10 +235,10 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
     for (int t = 0; t < kPV; ++t)
       xv[t] = (gi_next >= 0 && t < nval) ? __ldg(xr + t) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
-  if (pref && it < items) prefetch(it);
+  int ca = 0, start = 0;   // the current tile
+  if (it < items) tile_of(it, ca, start);
+  if (pref && it < items) prefetch(ca, start);
   while (it < items) {
-    int ca, start;
-    tile_of(it, ca, start);
     const int64_t g0 = a.goff[ca] + start;
     const int cnt = (int)min((int64_t)kTM, a.goff[ca + 1] - g0);
     const int32_t* pts = a.gperm + g0;
@@ -349,6 +347,18 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
       it_next = s_chunk;
       chunk_end = min(items, it_next + kChunk);
     }
+    // the next tile: the following one of the same cluster or of the next non-empty cluster,
+    // a binary search only for a new chunk elsewhere
+    int ca_n = ca, start_n = start + kTM;
+    if (it_next < items) {
+      if (it_next != it + 1) {
+        tile_of(it_next, ca_n, start_n);
+      } else if (start_n >= (s_ioff[ca + 1] - s_ioff[ca]) * kTM) {
+        ca_n = ca + 1;
+        while (s_ioff[ca_n + 1] == s_ioff[ca_n]) ++ca_n;
+        start_n = 0;
+      }
+    }
     if (tid == 0) {
       const uint32_t id = idesc_tf32(kTM, a.NT);
       for (int ks = 0; ks < a.Dp / 8; ++ks) {   // one MMA per 8 tf32 of K (two 16-byte chunks)
@@ -365,7 +375,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
                    : "memory");
     }
     // the next tile's rows in flight during the MMA and the epilogue
-    if (pref && it_next < items) prefetch(it_next);
+    if (pref && it_next < items) prefetch(ca_n, start_n);
     asm volatile(
         "{\n.reg .pred P1;\nTCW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra TCW_%=;\n}\n" ::"r"(
             smem_u32(&bar)),
@@ -449,6 +459,8 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
     __syncthreads();   // sA / TMEM / s_chunk reused by the next tile
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     it = it_next;
+    ca = ca_n;
+    start = start_n;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
