@@ -28,6 +28,27 @@
 #include "sc_internal.cuh"
 
 namespace sc {
+
+// Max dynamic shared memory of a kernel, grow-only and never below the 48 KB default:
+// concurrent k-means calls (the stability scan's workers) with different sizes must not lower
+// it under another call's launch.
+static int smem_attr_at_least(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> cur;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : cur)
+    if (e.first == kern) {
+      if (bytes > e.second) {
+        SC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        e.second = bytes;
+      }
+      return SC_OK;
+    }
+  const int v = std::max(bytes, 48 * 1024);
+  SC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+  cur.emplace_back(kern, v);
+  return SC_OK;
+}
 namespace {
 
 constexpr int kB = 256;
@@ -1520,7 +1541,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
     }
   }
   auto assign3 = nc_best == 4 ? assign3_kernel<4> : nc_best == 2 ? assign3_kernel<2> : assign3_kernel<1>;
-  SC_CUDA_TRY(cudaFuncSetAttribute(assign3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_assign));
+  SC_TRY(smem_attr_at_least(reinterpret_cast<const void*>(assign3), smem_assign));
   // the screens' ambiguous points: warp-per-point scan when the centroids fit in shared memory
   // (env SC_KMEANS_AMB_WARP=0: the tile kernel)
   const int smem_amb = (int)(sizeof(double) * ((size_t)k * d + 8 * (size_t)d));
@@ -1528,7 +1549,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
                           !(std::getenv("SC_KMEANS_AMB_WARP") && std::atoi(std::getenv("SC_KMEANS_AMB_WARP")) == 0);
   int64_t amb_grid = 1;
   if (amb_direct) {
-    SC_CUDA_TRY(cudaFuncSetAttribute(amb_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_amb));
+    SC_TRY(smem_attr_at_least(reinterpret_cast<const void*>(amb_scan_kernel), smem_amb));
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, amb_scan_kernel, 256, smem_amb);
     amb_grid = (int64_t)sms * std::max(1, occ);
@@ -1540,8 +1561,7 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   const auto screen_bytes = [&](int nb) { return (int)(sizeof(float) * (size_t)d * (kSLX + nb * kSLC)); };
   const int screen_nbuf = 3 * (screen_bytes(2) + 512 + 1024) <= smem_sm ? 2 : 1;
   const int smem_screen = screen_bytes(screen_nbuf);
-  SC_CUDA_TRY(cudaFuncSetAttribute(screen_nbuf == 2 ? assign_screen_kernel<2> : assign_screen_kernel<1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_screen));
+  SC_TRY(smem_attr_at_least(reinterpret_cast<const void*>(screen_nbuf == 2 ? assign_screen_kernel<2> : assign_screen_kernel<1>), smem_screen));
   // the screen pays off when the exact scan is expensive (env SC_KMEANS_SCREEN=0 disables it);
   // threshold measured on the configs[2] stability scan (k-means 0.57 s at 2^27, 0.47 s at 3e7
   // and 1e7: 10^5 x 48 features, k = 10..30); the Hamerly check follows the same size rule
@@ -1551,9 +1571,9 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   const bool screen = (double)n * k * d >= screen_min && !(std::getenv("SC_KMEANS_SCREEN") && std::atoi(std::getenv("SC_KMEANS_SCREEN")) == 0);
   const int smem_rows = (int)(sizeof(float) * kSP * (d + 4));   // (row stride d + 4 or d + 1)
   const int smem_d2 = smem_rows + (int)(sizeof(double) * d);
-  SC_CUDA_TRY(cudaFuncSetAttribute(check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_rows));
-  SC_CUDA_TRY(cudaFuncSetAttribute(d2_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_d2));
-  SC_CUDA_TRY(cudaFuncSetAttribute(d2_update_skip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_d2));
+  SC_TRY(smem_attr_at_least(reinterpret_cast<const void*>(check_kernel), smem_rows));
+  SC_TRY(smem_attr_at_least(reinterpret_cast<const void*>(d2_update_kernel), smem_d2));
+  SC_TRY(smem_attr_at_least(reinterpret_cast<const void*>(d2_update_skip_kernel), smem_d2));
 
   // tensor-core screen (sc_kmeans_tc.cu) for the assignments after a restart's first (env
   // SC_KMEANS_TC=0: the fp32 screen throughout)

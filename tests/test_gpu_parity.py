@@ -664,6 +664,26 @@ def test_stability_estimated_cuts_and_j2(sc):
     assert int(np.argmax(gam)) + 2 == 3
 
 
+def test_stability_screened_workers_match_exact_scan(sc, monkeypatch):
+    """At a size where the k-means screens run (n k d >= 3e7: tensor screen, fp32 screen, exact
+    scan of their ambiguous points) with concurrent workers of different k: labels and gamma
+    identical to the plain exact scan with one worker (R8 bit-exactness; regression for a
+    shared-memory attribute lowered by one worker under another's launch)."""
+    g = scinputs.sbm(80_000, 10, 16, 0.05, seed=31)
+    G = sc.Graph.from_csr(g)
+    args = (G.handle, 9, 12, 2, 48, 60, True, 24, 5, 2, 30)
+    lab = np.zeros((4, 2, g.n), dtype=np.int32)
+    gam, lk = sc.sc_stability(*args, labels=lab)
+    monkeypatch.setenv("SC_KMEANS_SCREEN", "0")
+    monkeypatch.setenv("SC_KMEANS_PRUNE_MIN", "1e30")
+    monkeypatch.setenv("SC_STABILITY_WORKERS", "1")
+    lab2 = np.zeros((4, 2, g.n), dtype=np.int32)
+    gam2, lk2 = sc.sc_stability(*args, labels=lab2)
+    assert np.array_equal(lk, lk2)
+    assert np.array_equal(lab, lab2)
+    assert np.array_equal(gam, gam2)
+
+
 def test_row_partitioned_steps_emulated_two_ranks(sc):
     """The multi-GPU data path on one GPU without inter-rank waiting: both ranks' local CSR
     (renumbered columns, interior-first rows, halo block), per-step halo fill from the
