@@ -27,12 +27,14 @@
 //                               (delta: the same with max_j ||z_j||)
 //   |D*_j - rho_j^2|         <= 2 eps_s ||y|| ||z_j|| + 2 (||y|| + ||z_j|| + delta) delta + delta^2
 //                             = Ea ||z_j|| + Eb0 =: E_j
-// with D*_j = Y2 + Z2_j - 2 S_j exactly (Y2, Z2_j the fp64 squared norms of the fp32 vectors;
-// their own fp64 rounding is ~2^-47 relative) and rho_j the exact distance of the fp32 point to
-// the fp64 centroid.  Ea, Eb0 are per point (fp64, inflated by 1e-6; Ea rounded up to fp32).
+// with D*_j = Y2 + Z2_j - 2 S_j exactly (Y2, Z2_j the exact squared norms of the fp32
+// vectors) and rho_j the exact distance of the fp32 point to the fp64 centroid.  Z2_j is an
+// fp64 sum (rounding ~2^-47 relative, inside kappa below); Y2 is summed in fp32 and enclosed
+// in [Y2c (1 - gamma), Y2c (1 + gamma)], gamma = (K + 2) 2^-24: the lower end enters the lower
+// bounds L_j (V below), the upper end the winner's upper bound U and ||y||.  Ea, Eb0 are per point (fp64, inflated by 1e-6; Ea rounded up to fp32).
 // Per column the epilogue evaluates in fp32, with kappa = 2^-20,
 //   L_j = fma(-2 kappa, |S_j|, fma(-2, S_j, fma(-Ea, zn_j, W_j) + V)),
-//   W_j = fl32(fl32(Z2_j)(1 - kappa)),  zn_j >= ||z_j||,  V = fl32_down(Y2 (1 - kappa) - Eb0),
+//   W_j = fl32(fl32(Z2_j)(1 - kappa)),  zn_j >= ||z_j||,  V = fl32_down(Y2l (1 - kappa) - Eb0),
 // i.e. D*_j - E_j - kappa M_j (M_j = Y2 + Z2_j + 2 |S_j|) up to seven roundings of at most
 // 2^-24 M_j each (< 2^-21 M_j < kappa M_j), so L_j <= rho_j^2 rigorously.  With b = argmin_j L_j
 // and U = D*_b + E_b evaluated in fp64 from S_b (an upper bound of rho_b^2), the point is
@@ -95,6 +97,7 @@ struct TcArgs {
   const double* pscal;   // [k][16]: see tc_panel_kernel
   int panel_floats;      // NT * Dp + 3 * NT
   int* ctr;              // item-chunk counter (zeroed by group_plan_kernel)
+  unsigned long long* prof;   // env SC_TC_PROFILE (tooling): per-phase clock64 sums of thread 0
   int32_t* fix;          // decided points whose exact distance tc_fix_kernel computes
   int* fix_len;
   int32_t* lab;
@@ -132,6 +135,10 @@ __global__ void __launch_bounds__(256) tc_panel_kernel(const double* __restrict_
 #pragma unroll 1
   for (int r = 0; r < 4; ++r) {
     const int jl = warp * 4 + r, j = jb * 32 + jl;
+    if (j >= NT) {   // (NT: k rounded up to 16; the last block may be half empty)
+      if (lane == 0) s_zn[jl] = 0.0;
+      continue;
+    }
     double s2 = 0.0;
     for (int q = lane; q < Dp; q += 32) {
       float z = 0.f;
@@ -168,6 +175,56 @@ __global__ void __launch_bounds__(256) tc_panel_kernel(const double* __restrict_
   }
 }
 
+// per-thread state of the epilogue's column scan: smallest / second smallest L and the
+// smallest's S and index, for even and odd columns separately
+struct ColTrack {
+  float L1e = INFINITY, L2e = INFINITY, Sbe = 0.f, L1o = INFINITY, L2o = INFINITY, Sbo = 0.f;
+  int be = -1, bo = -1;
+};
+
+// NW accumulator columns c0 .. c0 + NW - 1 of this thread's TMEM lane: L_j (bound in the file
+// header) and the tracking update
+template <int NW>
+__device__ __forceinline__ void tc_columns(uint32_t taddr, int c0, const float4* __restrict__ sWZ2, float Eaf,
+                                           float V, ColTrack& t) {
+  uint32_t v[NW];
+  if constexpr (NW == 32) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+  } else {
+    static_assert(NW == 16, "32- or 16-column loads");
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < NW; q += 2) {
+    const float4 wz = sWZ2[(c0 + q) >> 1];   // {W_j, zn_j, W_j+1, zn_j+1}
+    const float S0 = __uint_as_float(v[q]), S1 = __uint_as_float(v[q + 1]);
+    const float L0 = fmaf(-2.f * kKappaF, fabsf(S0), fmaf(-2.f, S0, fmaf(-Eaf, wz.y, wz.x) + V));
+    const float Lx = fmaf(-2.f * kKappaF, fabsf(S1), fmaf(-2.f, S1, fmaf(-Eaf, wz.w, wz.z) + V));
+    t.L2e = fminf(t.L2e, fmaxf(t.L1e, L0));
+    const bool lte = L0 < t.L1e;
+    t.L1e = fminf(t.L1e, L0);
+    t.Sbe = lte ? S0 : t.Sbe;
+    t.be = lte ? c0 + q : t.be;
+    t.L2o = fminf(t.L2o, fmaxf(t.L1o, Lx));
+    const bool lto = Lx < t.L1o;
+    t.L1o = fminf(t.L1o, Lx);
+    t.Sbo = lto ? S1 : t.Sbo;
+    t.bo = lto ? c0 + q + 1 : t.bo;
+  }
+}
+
 __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   const int KC = a.Dp / 4;
   extern __shared__ __align__(1024) unsigned char tsm[];
@@ -183,6 +240,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   __shared__ double s_ca_norm, s_zmax;
   __shared__ int s_zbad, s_chunk;
   __shared__ int s_ioff[257];
+  __shared__ long long s_goff[257];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
@@ -198,7 +256,10 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   const int items = *a.n_items;
-  for (int c = tid; c <= a.k; c += kTM) s_ioff[c] = a.ioff[c];
+  for (int c = tid; c <= a.k; c += kTM) {
+    s_ioff[c] = a.ioff[c];
+    s_goff[c] = a.goff[c];
+  }
   __syncthreads();
   // tile i -> (cluster, first position): the last cluster whose prefix is <= i
   auto tile_of = [&](int i, int& ca, int& start) {
@@ -219,28 +280,69 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   const bool pref = a.v4 && nval <= kPV;
   int cur = -1;   // cluster whose panel sits in sB
   uint32_t phase = 0;
-  // dynamic schedule: chunks of kChunk consecutive items (consecutive items mostly share a
-  // cluster, so the panel is staged about once per chunk or less)
+  // dynamic schedule: chunks of kChunk consecutive tiles (consecutive tiles mostly share a
+  // cluster, so the panel is staged about once per chunk or less).  Two tiles ahead are
+  // known: the next tile's rows are loaded during this tile's MMA and epilogue from an index
+  // loaded one tile earlier (no dependent global load on the critical path).
   if (tid == 0) s_chunk = atomicAdd(a.ctr, kChunk);
   __syncthreads();
-  int it = s_chunk, chunk_end = min(items, it + kChunk);
+  int it = s_chunk, ca = 0, start = 0;   // the current tile
+  const int chunk_end0 = min(items, it + kChunk);
+  if (it < items) tile_of(it, ca, start);
+  // the successor of a tile inside its chunk: the next tile of the same cluster or the first of
+  // the next non-empty cluster
+  auto walk = [&](int c, int st, int& c_n, int& st_n) {
+    c_n = c;
+    st_n = st + kTM;
+    if (st_n >= (s_ioff[c + 1] - s_ioff[c]) * kTM) {
+      c_n = c + 1;
+      while (s_ioff[c_n + 1] == s_ioff[c_n]) ++c_n;
+      st_n = 0;
+    }
+  };
+  int it1 = items, ca1 = 0, st1 = 0, chunk_end1 = chunk_end0;   // the next tile
+  if (it < items) {
+    if (it + 1 < chunk_end0) {
+      it1 = it + 1;
+      walk(ca, start, ca1, st1);
+    } else {
+      __syncthreads();   // (all threads: the condition is uniform)
+      if (tid == 0) s_chunk = atomicAdd(a.ctr, kChunk);
+      __syncthreads();
+      it1 = s_chunk;
+      chunk_end1 = min(items, it1 + kChunk);
+      if (it1 < items) tile_of(it1, ca1, st1);
+    }
+  }
+  auto load_idx = [&](int c, int st) -> int64_t {
+    const int64_t g0 = s_goff[c] + st;
+    const int cnt = (int)min((int64_t)kTM, (int64_t)(s_goff[c + 1] - g0));
+    return tid < cnt ? (int64_t)a.gperm[g0 + tid] : (int64_t)-1;
+  };
   float4 xv[kPV];
-  int64_t gi_next = -1;
-  auto prefetch = [&](int ca, int start) {
-    const int64_t g0 = a.goff[ca] + start;
-    const int cnt = (int)min((int64_t)kTM, a.goff[ca + 1] - g0);
-    gi_next = tid < cnt ? a.gperm[g0 + tid] : -1;
-    const float4* xr = reinterpret_cast<const float4*>(a.F + (gi_next >= 0 ? gi_next : 0) * a.d);
+  auto load_rows = [&](int64_t gi) {
+    const float4* xr = reinterpret_cast<const float4*>(a.F + (gi >= 0 ? gi : 0) * a.d);
 #pragma unroll
     for (int t = 0; t < kPV; ++t)
-      xv[t] = (gi_next >= 0 && t < nval) ? __ldg(xr + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+      xv[t] = (gi >= 0 && t < nval) ? __ldg(xr + t) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
-  int ca = 0, start = 0;   // the current tile
-  if (it < items) tile_of(it, ca, start);
-  if (pref && it < items) prefetch(ca, start);
+  int64_t gi_cur = -1, gi1 = -1;
+  if (it < items) gi_cur = load_idx(ca, start);
+  if (it1 < items) gi1 = load_idx(ca1, st1);
+  if (pref && it < items) load_rows(gi_cur);
+  unsigned long long pt[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+  auto mark = [&](int i) {
+    if (a.prof && tid == 0) {
+      const long long t = clock64();
+      pt[i] += (unsigned long long)(t - tprev);
+      tprev = t;
+    }
+  };
   while (it < items) {
-    const int64_t g0 = a.goff[ca] + start;
-    const int cnt = (int)min((int64_t)kTM, a.goff[ca + 1] - g0);
+    mark(6);
+    const int64_t g0 = s_goff[ca] + start;
+    const int cnt = (int)min((int64_t)kTM, (int64_t)(s_goff[ca + 1] - g0));
     const int32_t* pts = a.gperm + g0;
     // ---- the cluster's panel (tc_panel_kernel), c_a in fp64 and fp32
     if (ca != cur) {
@@ -256,7 +358,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
       if (tid == 0) {
         const double* ps = a.pscal + 16 * (size_t)ca;
         double zm = 0.0;
-        for (int jb = 0; jb < a.NT / 32; ++jb) zm = fmax(zm, ps[1 + jb]);
+        for (int jb = 0; jb < (a.NT + 31) / 32; ++jb) zm = fmax(zm, ps[1 + jb]);
         s_ca_norm = ps[0];
         s_zmax = zm;
         s_zbad = isinf(zm);
@@ -265,16 +367,17 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
       __syncthreads();
       cur = ca;
     }
-    // the item after this one: the next of the chunk, else the first of a new chunk (taken
-    // before the barrier below, read after it)
-    const bool last_of_chunk = it + 1 >= chunk_end;
-    if (last_of_chunk && tid == 0) s_chunk = atomicAdd(a.ctr, kChunk);
+    // the tile after next: the next of its chunk, else the first of a new chunk (taken before
+    // the barrier below, read after it)
+    const bool need_grab = it1 < items && it1 + 1 >= chunk_end1;
+    if (need_grab && tid == 0) s_chunk = atomicAdd(a.ctr, kChunk);
+    mark(0);
     // ---- centred points y = fl32(x - fl32(c_a)), tf32 copies for the MMA, fp64 ||y||^2; with
     // the prefetched rows also the exact (R8) distance to c_a, the usual winner
     double acc_a = 0.0;
     if (pref) {
       const int r = tid;
-      double s2 = 0.0;
+      float s2 = 0.f;   // ||y||^2 in fp32, sequential: within (K + 2) 2^-24 relative (epilogue)
 #pragma unroll
       for (int t = 0; t < kPV; ++t) {
         if (t >= KC) break;
@@ -290,11 +393,11 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
             acc_a = __dadd_rn(acc_a, __dmul_rn(diff, diff));
           }
         }
-        s2 += (double)y.x * y.x + (double)y.y * y.y + (double)y.z * y.z + (double)y.w * y.w;
+        s2 = fmaf(y.w, y.w, fmaf(y.z, y.z, fmaf(y.y, y.y, fmaf(y.x, y.x, s2))));
         *reinterpret_cast<float4*>(sA + ((r & 7) + (r >> 3) * (8 * KC) + t * 8) * 4) =
             make_float4(to_tf32(y.x), to_tf32(y.y), to_tf32(y.z), to_tf32(y.w));
       }
-      sY2[r] = s2;
+      sY2[r] = (double)s2;
     } else if (a.v4) {
       const int r = tid;
       const int64_t gi = r < cnt ? pts[r] : -1;
@@ -338,25 +441,20 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
         if (lane == 0) sY2[r] = s2;
       }
     }
+    mark(1);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // smem writes -> tensor core
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    int it_next = it + 1;
-    if (last_of_chunk) {
-      it_next = s_chunk;
-      chunk_end = min(items, it_next + kChunk);
-    }
-    // the next tile: the following one of the same cluster or of the next non-empty cluster,
-    // a binary search only for a new chunk elsewhere
-    int ca_n = ca, start_n = start + kTM;
-    if (it_next < items) {
-      if (it_next != it + 1) {
-        tile_of(it_next, ca_n, start_n);
-      } else if (start_n >= (s_ioff[ca + 1] - s_ioff[ca]) * kTM) {
-        ca_n = ca + 1;
-        while (s_ioff[ca_n + 1] == s_ioff[ca_n]) ++ca_n;
-        start_n = 0;
+    int it2 = items, ca2 = 0, st2 = 0, chunk_end2 = chunk_end1;
+    if (it1 < items) {
+      if (need_grab) {
+        it2 = s_chunk;
+        chunk_end2 = min(items, it2 + kChunk);
+        if (it2 < items) tile_of(it2, ca2, st2);
+      } else {
+        it2 = it1 + 1;
+        walk(ca1, st1, ca2, st2);
       }
     }
     if (tid == 0) {
@@ -374,8 +472,11 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
                        smem_u32(&bar))
                    : "memory");
     }
-    // the next tile's rows in flight during the MMA and the epilogue
-    if (pref && it_next < items) prefetch(ca_n, start_n);
+    // the next tile's rows in flight during the MMA and the epilogue; the index of the tile
+    // after next
+    if (pref && it1 < items) load_rows(gi1);
+    const int64_t gi2 = it2 < items ? load_idx(ca2, st2) : -1;
+    mark(2);
     asm volatile(
         "{\n.reg .pred P1;\nTCW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra TCW_%=;\n}\n" ::"r"(
             smem_u32(&bar)),
@@ -383,65 +484,45 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
         : "memory");
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    mark(3);
     // ---- epilogue: thread tid owns point tid (TMEM lane tid); per column the fp32 lower
     // bound L_j of rho_j^2 (bound above), tracking the smallest (index b, its S) and the
     // second smallest
-    const double Y2 = sY2[tid];
-    const double yn = (double)__fsqrt_ru(__double2float_ru(Y2));   // >= ||y||
+    // ||y||^2 as computed (fp32 sequential on the prefetch path, fp64 otherwise) and its
+    // enclosure [Y2l, Y2u] with gamma = (K + 2) 2^-24
+    const double Y2c = sY2[tid];
+    const double gamY = (a.Dp + 2) * 0x1p-24;
+    const double Y2u = Y2c * (1.0 + gamY), Y2l = Y2c * (1.0 - gamY);
+    const double yn = (double)__fsqrt_ru(__double2float_ru(Y2u));   // >= ||y||
     const double dmx = u * (yn + s_ca_norm + s_zmax) + 0x1p-51 * Cm + 0x1p-120;
     const double Ea = (2.0 * eps_s * yn + 2.0 * dmx) * (1.0 + 1e-6);
     const double Eb0 = (2.0 * (yn + dmx) * dmx + dmx * dmx + 0x1p-100) * (1.0 + 1e-6);
     const float Eaf = __double2float_ru(Ea);
-    const float V = __double2float_rd(Y2 * (1.0 - kKappa) - Eb0);
-    // two independent chains (even / odd columns) for instruction-level parallelism
-    float L1e = INFINITY, L2e = INFINITY, Sbe = 0.f, L1o = INFINITY, L2o = INFINITY, Sbo = 0.f;
-    int be = -1, bo = -1;
+    const float V = __double2float_rd(Y2l * (1.0 - kKappa) - Eb0);
+    // two independent chains (even / odd columns) for instruction-level parallelism; NT is k
+    // rounded up to 16 (padding columns: L = +inf): 32-column loads, a 16-column tail
+    ColTrack tr;
     const float4* sWZ2 = reinterpret_cast<const float4*>(sWZ);   // column pairs
-    for (int c0 = 0; c0 < a.NT; c0 += 32) {   // NT: a multiple of 32, padding columns L = +inf
-      uint32_t v[32];
-      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int q = 0; q < 32; q += 2) {
-        const float4 wz = sWZ2[(c0 + q) >> 1];   // {W_j, zn_j, W_j+1, zn_j+1}
-        const float S0 = __uint_as_float(v[q]), S1 = __uint_as_float(v[q + 1]);
-        const float L0 = fmaf(-2.f * kKappaF, fabsf(S0), fmaf(-2.f, S0, fmaf(-Eaf, wz.y, wz.x) + V));
-        const float Lx = fmaf(-2.f * kKappaF, fabsf(S1), fmaf(-2.f, S1, fmaf(-Eaf, wz.w, wz.z) + V));
-        L2e = fminf(L2e, fmaxf(L1e, L0));
-        const bool lte = L0 < L1e;
-        L1e = fminf(L1e, L0);
-        Sbe = lte ? S0 : Sbe;
-        be = lte ? c0 + q : be;
-        L2o = fminf(L2o, fmaxf(L1o, Lx));
-        const bool lto = Lx < L1o;
-        L1o = fminf(L1o, Lx);
-        Sbo = lto ? S1 : Sbo;
-        bo = lto ? c0 + q + 1 : bo;
-      }
-    }
-    const float L2 = fminf(fminf(L2e, L2o), fmaxf(L1e, L1o));
-    const bool odd = L1o < L1e;
-    const float Sb = odd ? Sbo : Sbe;
-    const int b = odd ? bo : be;
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    int c0 = 0;
+    for (; c0 + 32 <= a.NT; c0 += 32) tc_columns<32>(trow + (uint32_t)c0, c0, sWZ2, Eaf, V, tr);
+    if (c0 < a.NT) tc_columns<16>(trow + (uint32_t)c0, c0, sWZ2, Eaf, V, tr);
+    const float L2 = fminf(fminf(tr.L2e, tr.L2o), fmaxf(tr.L1e, tr.L1o));
+    const bool odd = tr.L1o < tr.L1e;
+    const float Sb = odd ? tr.Sbo : tr.Sbe;
+    const int b = odd ? tr.bo : tr.be;
+    mark(4);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     if (tid < cnt) {
-      const int64_t gi = pts[tid];
-      bool ok = b >= 0 && Y2 < 1e30 && !s_zbad;
+      const int64_t gi = gi_cur;
+      bool ok = b >= 0 && Y2u < 1e30 && !s_zbad;
       double low = (double)INFINITY;
       if (ok) {
         // upper bound of rho_b^2 in fp64: D*_b + E_b with ||z_b||^2 <= fl32(.)(1 + 2^-23)
         const double Z2b = (double)sZ2f[b] * (1.0 + 0x1p-23);
         const double Sd = (double)Sb;
-        const double up = (Y2 + Z2b - 2.0 * Sd + Ea * (double)sWZ[b].y + Eb0 +
-                           0x1p-40 * (Y2 + Z2b + 2.0 * fabs(Sd))) * (1.0 + 1e-12) + 0x1p-100;
+        const double up = (Y2u + Z2b - 2.0 * Sd + Ea * (double)sWZ[b].y + Eb0 +
+                           0x1p-40 * (Y2u + Z2b + 2.0 * fabs(Sd))) * (1.0 + 1e-12) + 0x1p-100;
         if (a.k > 1) low = (double)L2 * (1.0 - 1e-12);
         ok = low > up;
       }
@@ -456,11 +537,22 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
         a.amb[atomicAdd(a.amb_len, 1)] = static_cast<int32_t>(gi);
       }
     }
+    mark(5);
     __syncthreads();   // sA / TMEM / s_chunk reused by the next tile
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    it = it_next;
-    ca = ca_n;
-    start = start_n;
+    it = it1;
+    ca = ca1;
+    start = st1;
+    gi_cur = gi1;
+    it1 = it2;
+    ca1 = ca2;
+    st1 = st2;
+    chunk_end1 = chunk_end2;
+    gi1 = gi2;
+  }
+  if (a.prof && tid == 0) {
+    for (int i = 0; i < 7; ++i) atomicAdd(a.prof + i, pt[i]);
+    atomicAdd(a.prof + 7, 1ull);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -588,7 +680,7 @@ __global__ void __launch_bounds__(256) group_scatter_kernel(const int32_t* __res
 bool tc_screen_supported(int k, int d) {
   const char* e = std::getenv("SC_KMEANS_TC");
   if (e && std::atoi(e) == 0) return false;
-  const int NT = (k + 31) / 32 * 32, Dp = (d + 7) / 8 * 8;
+  const int NT = (k + 15) / 16 * 16, Dp = (d + 7) / 8 * 8;
   const size_t smem = tc_smem_bytes(NT, Dp);
   return k >= 2 && NT <= 256 && smem <= 200 * 1024;
 }
@@ -596,7 +688,7 @@ bool tc_screen_supported(int k, int d) {
 int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf, const double* cm, int k,
               const int32_t* old_lab, const int32_t* list, const int* list_len, int32_t* lab, double* dmin,
               double* lo, int32_t* amb, int* amb_len, TcWork& w, cudaStream_t s) {
-  const int NT = (k + 31) / 32 * 32, Dp = (d + 7) / 8 * 8;
+  const int NT = (k + 15) / 16 * 16, Dp = (d + 7) / 8 * 8;
   const int max_items = (int)((n + kTM - 1) / kTM) + k;
   SC_TRY(w.cnt.ensure(sizeof(unsigned) * 2 * (size_t)k, s));
   SC_TRY(w.off.ensure(sizeof(int64_t) * (size_t)(k + 1), s));
@@ -618,7 +710,7 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   const int pgrid = (int)std::max<int64_t>(1, (n + kGChunk - 1) / kGChunk);   // (list: <= n entries)
   group_hist_kernel<<<pgrid, 256, sizeof(unsigned) * k, s>>>(old_lab, list, list_len, n, k, cnt);
   group_plan_kernel<<<1, 256, 0, s>>>(cnt, k, w.off.as<int64_t>(), cursor, w.items.as<int>(), n_items, ctr, fix_len);
-  tc_panel_kernel<<<dim3(k, NT / 32), 256, 0, s>>>(C, k, d, Dp, NT, w.panels.as<float>(), w.pscal.as<double>(),
+  tc_panel_kernel<<<dim3(k, (NT + 31) / 32), 256, 0, s>>>(C, k, d, Dp, NT, w.panels.as<float>(), w.pscal.as<double>(),
                                                     panel_floats);
   group_scatter_kernel<<<pgrid, 256, sizeof(unsigned) * 3 * k, s>>>(old_lab, list, list_len, n, k,
                                                                     w.off.as<int64_t>(), cursor,
@@ -644,6 +736,10 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   a.pscal = w.pscal.as<double>();
   a.panel_floats = panel_floats;
   a.ctr = ctr;
+  static unsigned long long* prof = nullptr;
+  static const bool want_prof = std::getenv("SC_TC_PROFILE") != nullptr;
+  if (want_prof && !prof) SC_CUDA_TRY(cudaMallocManaged(&prof, 8 * sizeof(unsigned long long)));
+  a.prof = want_prof ? prof : nullptr;
   a.fix = w.fix.as<int32_t>();
   a.fix_len = fix_len;
   a.lab = lab;
@@ -677,6 +773,16 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   SC_CUDA_TRY(cudaGetLastError());
   tc_fix_kernel<<<sms * 2, 256, 0, s>>>(F, C, d, a.v4, lab, a.fix, fix_len, dmin);
   SC_CUDA_TRY(cudaGetLastError());
+  if (want_prof) {   // tooling: per-phase cycles of thread 0, summed over CTAs and launches
+    static int calls = 0;
+    if (++calls % 200 == 0) {
+      SC_CUDA_TRY(cudaStreamSynchronize(s));
+      const double c = (double)std::max(1ull, prof[7]);
+      std::fprintf(stderr, "[sc_kmeans] tensor screen cycles per CTA: next/panel %.0f stage %.0f mma+prefetch %.0f "
+                   "wait %.0f columns %.0f decide %.0f end %.0f\n", prof[0] / c, prof[1] / c, prof[2] / c, prof[3] / c,
+                   prof[4] / c, prof[5] / c, prof[6] / c);
+    }
+  }
   return SC_OK;
 }
 
