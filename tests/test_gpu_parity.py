@@ -378,6 +378,19 @@ def test_moments_counts_match_oracle(sc):
         assert abs(c - o) <= 1e-9 * mu[0]
 
 
+def test_moments_and_lambda_k_deterministic(sc):
+    """Moments are reduced in a fixed order (static tile schedule, per-CTA partials summed in
+    CTA order): repeated calls with the same seed give the same bits, at a size where many
+    CTAs share the tiles; so does the lambda_k estimate built on them."""
+    g = scinputs.sbm(150_000, 20, 16, 0.05, seed=8)
+    G = sc.Graph.from_csr(g)
+    lmax = 2.0 * G.info()[3]
+    mus = [sc.sc_cheb_moments(G.handle, lmax, 60, 16, 42) for _ in range(3)]
+    assert np.array_equal(mus[0], mus[1]) and np.array_equal(mus[0], mus[2])
+    lks = [sc.sc_estimate_lambda_k(G.handle, 20, lmax, 60, True, 16, 42, 40, 1e-4) for _ in range(2)]
+    assert lks[0] == lks[1]
+
+
 def test_lambda_k_dichotomy_matches_oracle(sc):
     g = scinputs.sbm(2000, 5, 10, 0.1, seed=1234)
     G = sc.Graph.from_csr(g)
