@@ -444,7 +444,11 @@ def _features(seed, n, k, d, spread):
     # exact fp64 rescan of the ambiguous points decides them
     pytest.param(40000, 64, 56, -1.0, 1, 6, marks=pytest.mark.slow),
     # screened path with d and k off every tile multiple (29 dims, 70 centroids)
-    pytest.param(70000, 70, 29, 0.7, 1, 6, marks=pytest.mark.slow)])
+    pytest.param(70000, 70, 29, 0.7, 1, 6, marks=pytest.mark.slow),
+    # tensor screen with rows wider than its register prefetch (d = 96: configs[4]'s width) and
+    # with k = 200 (N = 208 columns of TMEM, 1 CTA per SM)
+    pytest.param(30000, 40, 96, 0.8, 1, 6, marks=pytest.mark.slow),
+    pytest.param(20000, 200, 96, 0.8, 1, 5, marks=pytest.mark.slow)])
 def test_kmeans_bit_exact(sc, n, k, d, spread, restarts, max_iter):
     X = _features(n + k, n, k, d, spread)
     u = np.stack([scinputs.uniforms(7, k, offset=k * r) for r in range(restarts)])
