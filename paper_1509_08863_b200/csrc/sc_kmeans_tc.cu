@@ -44,9 +44,12 @@
 // every other centroid (Hamerly).  Points with ||y||^2 or a ||z_j||^2 >= 1e30 (fp32 overflow)
 // are left undecided.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <utility>
 #include <vector>
 
 #include "sc_internal.cuh"
@@ -736,10 +739,15 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   a.pscal = w.pscal.as<double>();
   a.panel_floats = panel_floats;
   a.ctr = ctr;
-  static unsigned long long* prof = nullptr;
+  // tooling (env SC_TC_PROFILE): per-phase cycle sums in managed memory, allocated once
   static const bool want_prof = std::getenv("SC_TC_PROFILE") != nullptr;
-  if (want_prof && !prof) SC_CUDA_TRY(cudaMallocManaged(&prof, 8 * sizeof(unsigned long long)));
-  a.prof = want_prof ? prof : nullptr;
+  static unsigned long long* const prof = [] {
+    unsigned long long* q = nullptr;
+    if (want_prof && cudaMallocManaged(&q, 8 * sizeof(unsigned long long)) != cudaSuccess) q = nullptr;
+    if (q) std::memset(q, 0, 8 * sizeof(unsigned long long));
+    return q;
+  }();
+  a.prof = prof;
   a.fix = w.fix.as<int32_t>();
   a.fix_len = fix_len;
   a.lab = lab;
@@ -748,22 +756,23 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   a.amb = amb;
   a.amb_len = amb_len;
   const int smem = (int)tc_smem_bytes(NT, Dp);
-  static int attr = 0;
-  if (smem > attr) {
-    SC_CUDA_TRY(cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = 200 * 1024;
-  }
-  // resident CTAs per SM: shared memory (228 KB per SM, 1 KB reserved per CTA) and TMEM
-  // (512 columns per SM)
-  // (computed here: the occupancy API answered 1 for this kernel where the hardware fits 3,
-  // ncu "Block Limit Shared Mem" / "Block Limit Registers" = 3 / 4 at k = 100, d = 64)
-  static int carve = 0;
-  if (!carve) {
-    SC_CUDA_TRY(cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    carve = 1;
-  }
-  cudaFuncAttributes fa{};
-  SC_CUDA_TRY(cudaFuncGetAttributes(&fa, assign_tc_kernel));
+  // kernel attributes once per process (thread-safe static initialisation: restarts call this
+  // from several worker threads): the largest dynamic shared memory any supported (k, d) needs
+  // (tc_screen_supported caps it at 200 KB), the full shared-memory carve-out, and the
+  // registers per thread for the occupancy below
+  static const std::pair<cudaError_t, cudaFuncAttributes> kattr = [] {
+    cudaFuncAttributes f{};
+    cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&f, assign_tc_kernel);
+    return std::make_pair(e, f);
+  }();
+  SC_CUDA_TRY(kattr.first);
+  const cudaFuncAttributes& fa = kattr.second;
+  // resident CTAs per SM: shared memory (228 KB per SM, 1 KB reserved per CTA), registers and
+  // TMEM (512 columns per SM), computed here: the occupancy API answered 1 for this kernel
+  // where the hardware fits 3 (ncu "Block Limit Shared Mem" / "Block Limit Registers" = 3 / 4
+  // at k = 100, d = 64)
   const int regs_cta = std::max(1, fa.numRegs) * kTM;
   int occ = std::min((227 * 1024) / (smem + (int)fa.sharedSizeBytes + 1024), 65536 / regs_cta);
   occ = std::max(1, std::min(occ, 512 / a.tmem_cols));
@@ -773,8 +782,8 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   SC_CUDA_TRY(cudaGetLastError());
   tc_fix_kernel<<<sms * 2, 256, 0, s>>>(F, C, d, a.v4, lab, a.fix, fix_len, dmin);
   SC_CUDA_TRY(cudaGetLastError());
-  if (want_prof) {   // tooling: per-phase cycles of thread 0, summed over CTAs and launches
-    static int calls = 0;
+  if (prof) {   // tooling: per-phase cycles of thread 0, summed over CTAs and launches
+    static std::atomic<int> calls{0};
     if (++calls % 200 == 0) {
       SC_CUDA_TRY(cudaStreamSynchronize(s));
       const double c = (double)std::max(1ull, prof[7]);
