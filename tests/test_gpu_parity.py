@@ -462,6 +462,33 @@ def test_kmeans_bit_exact(sc, n, k, d, spread, restarts, max_iter):
     assert inertia == pytest.approx(io, rel=1e-12)
 
 
+@pytest.mark.parametrize("n,k,d,spread", [
+    (100, 2, 4, 0.5),        # one partial tile, N = 16 (k padded), K = 8 (d padded)
+    (257, 17, 12, 0.4),      # tiles of 1-128 points, clusters of a few points
+    (1000, 3, 8, -1.0),      # integer grid: ties everywhere -> the exact rescan decides
+    (3000, 40, 64, 0.6),     # the register-prefetch staging at its widest (d = 64)
+    (2000, 30, 68, 0.6),     # d = 68: 16-byte rows wider than the prefetch
+    (1500, 9, 20, 0.05)])    # tight clusters: most points decided, few change
+def test_kmeans_screens_forced_small(sc, n, k, d, spread, monkeypatch):
+    """The screens (tensor-core and fp32) and the Hamerly check forced on small problems
+    (thresholds 0): edge shapes of the tiles / panels / queues, labels, centroids, iteration
+    count and best restart identical to the fp64 oracle (R8)."""
+    monkeypatch.setenv("SC_KMEANS_SCREEN_MIN", "0")
+    monkeypatch.setenv("SC_KMEANS_PRUNE_MIN", "0")
+    X = _features(n + 7 * k + d, n, k, d, spread)
+    restarts, max_iter = 3, 30
+    u = np.stack([scinputs.uniforms(3, k, offset=k * r) for r in range(restarts)])
+    lo, Co, io, ito, ro, _ = kmeans.kmeans(X, k, u, max_iter)
+    for tc in ("1", "0"):
+        monkeypatch.setenv("SC_KMEANS_TC", tc)
+        lab = torch.empty(n, dtype=torch.int32, device="cuda")
+        C = np.zeros((k, d), dtype=np.float64)
+        inertia, it, best = sc.sc_kmeans(torch.from_numpy(X).cuda(), n, d, k, restarts, max_iter, 0, u, lab, C)
+        assert np.array_equal(lab.cpu().numpy(), lo), tc
+        assert np.array_equal(C, Co) and best == ro and it == ito, tc
+        assert inertia == pytest.approx(io, rel=1e-12)
+
+
 def test_kmeans_unaligned_features_same_labels(sc):
     """Features whose base pointer is not 16-byte aligned (a view one float into its storage)
     take the 4-byte staging path of the per-point kernels; d % 4 == 0 aligned features the
