@@ -832,14 +832,21 @@ def test_partitioned_lambda_estimates_emulated(sc, world):
             sc.sc_comm_free(c)
 
 
-@pytest.mark.parametrize("world,n,k,d,restarts,spread", [(1, 2000, 4, 6, 2, 0.5), (2, 3000, 5, 8, 3, 0.5),
-                                                         (3, 20000, 12, 16, 2, 1.0), (4, 40000, 32, 48, 2, 1.0)])
-def test_dist_kmeans_emulated_bit_exact(sc, world, n, k, d, restarts, spread):
+@pytest.mark.parametrize("world,n,k,d,restarts,spread,force", [
+    (1, 2000, 4, 6, 2, 0.5, False), (2, 3000, 5, 8, 3, 0.5, False), (3, 20000, 12, 16, 2, 1.0, False),
+    (4, 40000, 32, 48, 2, 1.0, False),
+    # screens (tensor-core, fp32 for the first assignment) and the Hamerly check forced on
+    # every rank's rows
+    (3, 20000, 12, 16, 2, 1.0, True), (4, 40000, 32, 48, 2, 1.0, True)])
+def test_dist_kmeans_emulated_bit_exact(sc, world, n, k, d, restarts, spread, force, monkeypatch):
     """sc_dist_kmeans (§4.1 step 6 on a row partition): all ranks held by this
     process (sc_comm_local; one host thread and stream per rank, reductions at a host
     rendezvous), uneven row blocks, against the oracle on the rank-major concatenation:
     labels, centroids, iteration count and best restart bit-exact (exact integer member sums
-    reduced over the ranks; the last case takes the fp32 screen + Hamerly paths)."""
+    reduced over the ranks; `force`: the screened and pruned assignment paths)."""
+    if force:
+        monkeypatch.setenv("SC_KMEANS_SCREEN_MIN", "0")
+        monkeypatch.setenv("SC_KMEANS_PRUNE_MIN", "0")
     rng = np.random.default_rng(n + k)
     centers = rng.standard_normal((k, d)) * 2.0
     X = (centers[rng.integers(0, k, n)] + spread * rng.standard_normal((n, d))).astype(np.float32)
