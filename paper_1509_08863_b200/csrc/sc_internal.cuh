@@ -351,10 +351,12 @@ int kmeans_run_dist(const float* F, int64_t n_local, int64_t row_off, int64_t n_
                     int max_iter, uint64_t seed, const double* uniforms_host, int32_t* labels_dev,
                     double* centroids_host, double* inertia, int* iters, int* best_restart, Coll* coll,
                     cudaStream_t s);
+// max_workers: concurrent restarts (0: env SC_KMEANS_WORKERS, default 10 -- all of a
+// 10-restart call; callers that already run several k-means problems at once pass fewer)
 int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_iter,
                uint64_t seed, const double* uniforms_host, int32_t* labels_dev,
                double* centroids_host, double* inertia, int* iters, int* best_restart,
-               cudaStream_t s);
+               cudaStream_t s, int max_workers = 0);
 int ari_dev(const int32_t* a, const int32_t* b, int64_t n, double* out, cudaStream_t s);
 
 // stability measure gamma(k) over [k_min, k_max] (sc_stability.cu)

@@ -277,7 +277,7 @@ int stability_scan(sc_graph* g, int k_min, int k_max, int J, int R, int order, b
         int it = 0, best = 0;
         const int rc = kmeans_run(yall.as<float>() + ((size_t)jj * K + c) * n * R, n, R, k_min + c, restarts,
                                   max_iter, seed + (uint64_t)j, nullptr, labels_dev + ((size_t)c * J + j) * n,
-                                  nullptr, &inertia, &it, &best, ws);
+                                  nullptr, &inertia, &it, &best, ws, 4);
         if (rc != SC_OK) {
           std::lock_guard<std::mutex> lk(err_mu);
           if (err_code == SC_OK) { err_code = rc; err_msg = sc_last_error(); }
