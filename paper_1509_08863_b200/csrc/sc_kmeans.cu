@@ -1030,6 +1030,98 @@ __global__ void __launch_bounds__(kSP) check_kernel(const float* __restrict__ F,
   }
 }
 
+// Bound-only pruning test of the screened path (Hamerly's upper bound, no feature read):
+// u_i bounds the distance from x_i to its centroid -- sqrt(dmin_i) (1 + 1e-12) when dmin_i is
+// exact for the current label (u_i < 0 or NaN: the last assignment computed it), else the
+// carried bound -- and the centroid moved by at most shift[a] since, so
+//   ||x_i - c_a_new|| <= (u_i + shift[a]) (1 + 1e-12) =: ub.
+// lo_i (a lower bound of the distance to every other centroid) drops by dmax as in
+// check_kernel.  If ub (1 + 1e-9) < (lo_i - dmax)(1 - 1e-9) the assigned centroid is the
+// unique nearest (the margins cover the fp64 evaluation of R8, as in check_kernel): the point
+// keeps its label and carries ub, its dmin is left stale (final_dmin_kernel recomputes the
+// stale ones once the restart ends).  Otherwise it is queued for the screen, which computes
+// its exact dmin (u_i = -1 marks that).
+__global__ void __launch_bounds__(256) check_bound_kernel(int64_t n, const int32_t* __restrict__ old_lab,
+                                                          const double* __restrict__ dmin, double* __restrict__ u,
+                                                          double* __restrict__ lo, const double* __restrict__ shift,
+                                                          const double* __restrict__ dmax, int32_t* __restrict__ lab,
+                                                          int32_t* __restrict__ list, int* __restrict__ list_len) {
+  const double dm = *dmax;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool keep = true;
+    if (i < n) {
+      const int a = old_lab[i];
+      const double ui = u[i];
+      const double b0 = ui >= 0.0 ? ui : sqrt(dmin[i]) * (1.0 + 1e-12);
+      const double ub = (b0 + shift[a]) * (1.0 + 1e-12);
+      const double l = lo[i] - dm;
+      lo[i] = l;
+      keep = ub * (1.0 + 1e-9) < l * (1.0 - 1e-9);
+      if (keep) {
+        lab[i] = a;
+        u[i] = ub;
+      } else {
+        u[i] = -1.0;
+      }
+    }
+    const unsigned need = __ballot_sync(0xffffffffu, !keep);
+    if (!keep) {
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(need) - 1;
+      int b = 0;
+      if (lane == leader) b = atomicAdd(list_len, __popc(need));
+      b = __shfl_sync(need, b, leader);
+      list[b + __popc(need & ((1u << lane) - 1))] = static_cast<int32_t>(i);
+    }
+  }
+}
+
+// The exact R8 distances of the points whose dmin is stale (u_i >= 0: kept by
+// check_bound_kernel since their last exact distance) to their final centroid, staged rows as
+// in check_kernel; then the restart's inertia is summed again (inertia_parts_kernel).
+__global__ void __launch_bounds__(kSP) final_dmin_kernel(const float* __restrict__ F, int64_t n, int d,
+                                                         const double* __restrict__ C,
+                                                         const int32_t* __restrict__ lab, const double* __restrict__ u,
+                                                         double* __restrict__ dmin) {
+  extern __shared__ unsigned char smk[];
+  float* sx = reinterpret_cast<float*>(smk);
+  __shared__ int s_any;
+  const int64_t p0 = (int64_t)blockIdx.x * kSP;
+  const int64_t i = p0 + threadIdx.x;
+  const bool stale = i < n && u[i] >= 0.0;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  if (stale) s_any = 1;
+  __syncthreads();
+  if (!s_any) return;
+  const bool v4 = rows_v4(F, d);
+  stage_rows(F, n, d, p0, sx, v4);
+  __syncthreads();
+  if (stale) dmin[i] = row_dist(sx + threadIdx.x * rows_ld(v4, d), C + (size_t)lab[i] * d, d, v4);
+}
+
+// inertia partials with assign_stats_kernel's summation order (grid nstat x 256: each thread
+// sums its grid-stride points in order, then the same block tree), so the total is the one a
+// pass with exact distances throughout would give
+__global__ void __launch_bounds__(256) inertia_parts_kernel(const double* __restrict__ dmin, int64_t n,
+                                                            double* __restrict__ part_inertia) {
+  double inertia = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    if (i < n) inertia += dmin[i];
+  }
+  __shared__ double sh[256];
+  sh[threadIdx.x] = inertia;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part_inertia[blockIdx.x] = sh[0];
+}
+
 // Per-assignment statistics: cluster sizes, the list of changed points with the histogram of
 // their old and new labels, and per-block inertia partials.  Grid-stride blocks keep both
 // histograms in shared memory (k <= kHistMax) and flush k atomics per block at the end: a
@@ -1344,7 +1436,7 @@ __global__ void __launch_bounds__(256) member_finalize_kernel(unsigned long long
                                                               const unsigned* __restrict__ counts, int k, int d,
                                                               int shift, double* __restrict__ C,
                                                               float* __restrict__ Cf, double* __restrict__ cm,
-                                                              double* __restrict__ dmax) {
+                                                              double* __restrict__ dmax, double* __restrict__ shifts) {
   __shared__ double s_n[256], s_d[256];
   const int c = blockIdx.x;
   const unsigned cnt = counts[c];
@@ -1375,8 +1467,11 @@ __global__ void __launch_bounds__(256) member_finalize_kernel(unsigned long long
   if (threadIdx.x == 0) {
     if (cm) atomicMax(reinterpret_cast<unsigned long long*>(cm),
                       (unsigned long long)__double_as_longlong(sqrt(s_n[0]) * (1.0 + 1e-9)));
-    if (dmax) atomicMax(reinterpret_cast<unsigned long long*>(dmax),
-                        (unsigned long long)__double_as_longlong(sqrt(s_d[0]) * (1.0 + 1e-9) + 1e-300));
+    if (dmax) {
+      const double sh = sqrt(s_d[0]) * (1.0 + 1e-9) + 1e-300;
+      atomicMax(reinterpret_cast<unsigned long long*>(dmax), (unsigned long long)__double_as_longlong(sh));
+      if (shifts) shifts[c] = sh;   // this centroid's move (bound-only pruning test)
+    }
   }
 }
 
@@ -1481,6 +1576,11 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   SC_TRY(b_list.ensure(sizeof(int32_t) * n, s));
   SC_TRY(b_len.ensure(16, s));   // [0] pruning queue length, [1] member work items, [2] ambiguous
   SC_TRY(b_dmax.ensure(16, s));
+  // bound-only pruning of the screened path: distance upper bounds (u < 0: dmin exact) and
+  // the centroids' moves of the last update
+  PoolBuf b_u, b_shift;
+  SC_TRY(b_u.ensure(sizeof(double) * n, s));
+  SC_TRY(b_shift.ensure(sizeof(double) * (k + 1), s));
   PoolBuf b_chg, b_near, b_gap;
   SC_TRY(b_chg.ensure(sizeof(int) * (max_iter + 2), s));
   SC_TRY(b_near.ensure(sizeof(int32_t) * n, s));     // k-means++: nearest seed per point
@@ -1586,6 +1686,10 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
   const double prune_min = std::getenv("SC_KMEANS_PRUNE_MIN") ? std::atof(std::getenv("SC_KMEANS_PRUNE_MIN"))
                                                               : 3.0e7;
   const bool prune = (double)n * k * d >= prune_min;
+  // the screened path prunes with bounds only (check_bound_kernel: no feature reads; the
+  // stale distances are recomputed once per restart); env SC_KMEANS_BOUND=0: exact check
+  const bool bound_check = screen && prune && !(std::getenv("SC_KMEANS_BOUND") && std::atoi(std::getenv("SC_KMEANS_BOUND")) == 0);
+  if (bound_check) SC_TRY(smem_attr_at_least(reinterpret_cast<const void*>(final_dmin_kernel), smem_rows));
   // Lloyd assignment of every point, no host synchronisation: labels, exact dmin, the
   // number of changed labels into changed_dev[slot] and the label histogram (device);
   // block partials of the inertia in b_part
@@ -1603,10 +1707,19 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
       const bool pruned = old && prune && try_check;
       int* amb_len = b_len.as<int>() + 2;
       if (pruned) {
-        check_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_rows, s>>>(
-            F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(), b_lo.as<double>(),
-            b_list.as<int32_t>(), b_len.as<int>());
+        if (bound_check) {
+          check_bound_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16), 256, 0, s>>>(
+              n, old, b_dmin.as<double>(), b_u.as<double>(), b_lo.as<double>(), b_shift.as<double>(),
+              b_dmax.as<double>(), out_lab, b_list.as<int32_t>(), b_len.as<int>());
+        } else {
+          check_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_rows, s>>>(
+              F, n, d, C, old, b_dmax.as<double>(), out_lab, b_dmin.as<double>(), b_lo.as<double>(),
+              b_list.as<int32_t>(), b_len.as<int>());
+        }
         SC_CUDA_TRY(cudaGetLastError());
+      } else if (bound_check) {
+        // every point's dmin is recomputed by this assignment: no carried bounds
+        SC_CUDA_TRY(cudaMemsetAsync(b_u.ptr, 0xff, sizeof(double) * n, s));
       }
       if (!old) {   // first assignment of a restart; later ones get Cf, cm from the finalize kernel
         centroid_prep_kernel<<<1, 256, 0, s>>>(C, k, d, d_Cf, d_cm);
@@ -1741,7 +1854,8 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
       const int fin_threads = bounds ? 256 : std::min(256, (d + 31) / 32 * 32);
       member_finalize_kernel<<<(unsigned)k, fin_threads, 0, s>>>(
           b_psum.as<unsigned long long>(), counts, k, d, shift, C, screen ? d_Cf : nullptr,
-          screen ? d_cm : nullptr, prune ? b_dmax.as<double>() : nullptr);
+          screen ? d_cm : nullptr, prune ? b_dmax.as<double>() : nullptr,
+          (screen && prune) ? b_shift.as<double>() : nullptr);
     }
     SC_CUDA_TRY(cudaGetLastError());
     return SC_OK;
@@ -1834,6 +1948,13 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
       // (a run that never converges ends at max_iter, like the oracle)
     }
     it = conv;
+    if (bound_check) {
+      // the stale distances of the points the bound-only test kept, then the inertia again
+      final_dmin_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_rows, s>>>(F, n, d, C, lab, b_u.as<double>(),
+                                                                               b_dmin.as<double>());
+      inertia_parts_kernel<<<(unsigned)nstat, 256, 0, s>>>(b_dmin.as<double>(), n, b_part.as<double>());
+      SC_CUDA_TRY(cudaGetLastError());
+    }
     double inertia = 0.0;
     SC_TRY(read_inertia(&inertia));
     if (trace) {
