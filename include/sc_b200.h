@@ -112,6 +112,25 @@ int sc_lambda_max(sc_graph* g, int iters, double margin, uint64_t seed, double* 
  */
 int sc_cheby_coeffs(double lambda_c, double lambda_max, int order, int jackson, double* coeffs);
 
+/*
+ * sc_filter_order -- m*(lambda_c/lambda_N; delta), the filter order of PAPER.md §2.4
+ * "Note on the choice of m" (Eq. (4)) used by §4.1 step 3 (line 312): the
+ * smallest m in [1, m_max] whose polynomial (the coefficients sc_cheby_coeffs gives for
+ * lambda_c = ratio, lambda_max = 1, `jackson`) satisfies |h_ratio(l) - p_m(l)| <= delta at
+ * every point l of the grid {i/(n_grid-1)} U {i min(1, 2 ratio)/(n_grid-1)}, i < n_grid,
+ * outside the transition band [ratio(1-theta), ratio(1+theta)] (reading R18: the
+ * sup over the whole interval is >= 1/2 for any polynomial at the jump).  The paper fixes
+ * delta = 0.1 (line 162); R18 takes theta = 0.1, n_grid = 10000.
+ * Evaluated on the device (fp64 Clenshaw, orders tried in batches of increasing size on
+ * `stream`; the call synchronises the stream).
+ *  m_star  host int: m*, or 0 if no order <= m_max meets delta.
+ *  err     host double or NULL: the grid error of m* (of the last order tried when m* = 0).
+ * Errors: SC_ERR_ARG for ratio outside (0, 1], delta <= 0, theta outside [0, 1),
+ *         n_grid outside [2, 2^24], m_max outside [1, 4096]; SC_ERR_CUDA.
+ */
+int sc_filter_order(double ratio, double delta, int jackson, double theta, int n_grid, int m_max,
+                    int* m_star, double* err, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Random signals (§3.1, §4.1 step 4 line 316)       */
 /* ------------------------------------------------------------------------ */
@@ -247,8 +266,11 @@ int sc_ari(const int32_t* a, const int32_t* b, int64_t n, double* out, void* str
  * sc_cluster -- lambda_max (Lanczos), lambda_k (moments + dichotomy, n_probe
  * probes, Jackson), filter R random signals at lambda_k (order, jackson),
  * optional row normalisation, k-means (restarts).  labels: n int32.
- * info (host, may be NULL): [lambda_max, lambda_k, count_k, inertia,
- * kmeans_iters, best_restart].
+ * order > 0: steps 2 and 5 use this order.  order < 0: step 2 uses -order and step 5
+ * the order m*(lambda~_k/lambda_N; 0.1) of sc_filter_order (theta 0.1, 10000-point grid,
+ * 2000 if no order <= 2000 meets delta) -- PAPER.md §4.1 step 3, line 312.
+ * info (host, may be NULL): 7 doubles [lambda_max, lambda_k, count_k, inertia,
+ * kmeans_iters, best_restart, filter order used].
  * The eigencount of step 2 always uses the Jackson-damped polynomial, whatever
  * `jackson` says: the count ||F X||^2 estimates #{lambda_l <= lambda_c} only if
  * the polynomial stays in [0, 1] (R5); the undamped truncated series

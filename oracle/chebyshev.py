@@ -75,6 +75,38 @@ def poly_eval(lam, coeffs: np.ndarray, lambda_max: float):
     return np.cos(np.multiply.outer(t, j)) @ coeffs
 
 
+def order_grid(ratio: float, theta: float = 0.1, n_grid: int = 10000) -> np.ndarray:
+    """Points of [0, 1] where the §2.4 criterion (Eq. (4), l.151-156) is checked for
+    h_{ratio} = h_{lambda_c/lambda_N} on [0, 1] (l.157-159: the normalised filter depends on
+    the ratio only): the uniform n_grid-point grids i/(n_grid-1) of [0, 1] and of
+    [0, min(1, 2 ratio)] (the second resolves the neighbourhood of the cut whatever the
+    ratio), minus the transition band [ratio(1-theta), ratio(1+theta)] (reading R18:
+    the sup over all of [0, lambda_N] is >= 1/2 for any polynomial at the jump)."""
+    i = np.arange(n_grid, dtype=np.float64) / (n_grid - 1)
+    lam = np.union1d(i, i * min(1.0, 2.0 * ratio))
+    keep = (lam < ratio * (1.0 - theta)) | (lam > ratio * (1.0 + theta))
+    return lam[keep]
+
+
+def approx_error(ratio: float, order: int, damping: bool, theta: float = 0.1,
+                 n_grid: int = 10000) -> float:
+    """sup over order_grid of |h_{ratio}(lambda) - p_m(lambda)|, p_m the order-m polynomial
+    the filter applies (filter_coeffs on [0, 1]), evaluated in trigonometric form."""
+    lam = order_grid(ratio, theta, n_grid)
+    p = poly_eval(lam, filter_coeffs(ratio, 1.0, order, damping), 1.0)
+    return float(np.max(np.abs(ideal_lowpass(lam, ratio) - p)))
+
+
+def minimal_order(ratio: float, delta: float, damping: bool, m_max: int, theta: float = 0.1,
+                  n_grid: int = 10000):
+    """m*(lambda_c/lambda_N; delta) (§2.4 l.151-162, §4.1 step 3 l.312): the smallest
+    m in 1..m_max with approx_error <= delta, tried in increasing m; None if there is none."""
+    for m in range(1, m_max + 1):
+        if approx_error(ratio, m, damping, theta, n_grid) <= delta:
+            return m
+    return None
+
+
 def cheb_filter(L, R: np.ndarray, coeffs: np.ndarray, lambda_max: float) -> np.ndarray:
     """Y = sum_j coeffs_j T_j(L~) R by the three-term recurrence, fp64.
 

@@ -49,6 +49,7 @@ _F = {
     "sc_graph_strengths": _sig("sc_graph_strengths", c_vp, c_vp, c_vp),
     "sc_lambda_max": _sig("sc_lambda_max", c_vp, c_i32, c_dbl, c_u64, P(c_dbl), c_vp),
     "sc_cheby_coeffs": _sig("sc_cheby_coeffs", c_dbl, c_dbl, c_i32, c_i32, c_vp),
+    "sc_filter_order": _sig("sc_filter_order", c_dbl, c_dbl, c_i32, c_dbl, c_i32, c_i32, P(c_i32), P(c_dbl), c_vp),
     "sc_random_signals_f32": _sig("sc_random_signals_f32", c_i64, c_i32, c_i64, c_u64, c_i32, c_dbl, c_vp, c_vp),
     "sc_random_signals_f64": _sig("sc_random_signals_f64", c_i64, c_i32, c_i64, c_u64, c_i32, c_dbl, c_vp, c_vp),
     "sc_filter_apply_f32": _sig("sc_filter_apply_f32", c_vp, c_vp, c_i32, c_dbl, c_i32, c_vp, c_vp, c_vp),
@@ -184,6 +185,15 @@ def sc_cheby_coeffs(lambda_c, lambda_max, order, jackson) -> np.ndarray:
     return out
 
 
+def sc_filter_order(ratio, delta, jackson, theta=0.1, n_grid=10000, m_max=2000, stream=None):
+    """-> (m_star, err); m_star 0 if no order <= m_max meets delta."""
+    m = ctypes.c_int32(0)
+    e = ctypes.c_double(0.0)
+    _check(_F["sc_filter_order"](ratio, delta, int(jackson), theta, n_grid, m_max, ctypes.byref(m), ctypes.byref(e),
+                                 _stream(stream)))
+    return m.value, e.value
+
+
 def sc_random_signals_f32(n, R, row0, seed, stream_id, variance, out, stream=None):
     _check(_F["sc_random_signals_f32"](n, R, row0, seed, stream_id, variance, _ptr(out), _stream(stream)))
 
@@ -267,7 +277,7 @@ def sc_ari(a, b, n, stream=None) -> float:
 
 
 def sc_cluster(g, k, R, order, jackson, n_probe, seed, restarts, max_iter, normalize, labels, stream=None):
-    info = np.zeros(6, dtype=np.float64)
+    info = np.zeros(7, dtype=np.float64)
     _check(_F["sc_cluster"](g, k, R, order, int(jackson), n_probe, seed, restarts, max_iter, int(normalize),
                             _ptr(labels), info.ctypes.data, _stream(stream)))
     return info

@@ -276,6 +276,16 @@ int sc_cheby_coeffs(double lambda_c, double lambda_max, int order, int jackson, 
   return SC_OK;
 }
 
+int sc_filter_order(double ratio, double delta, int jackson, double theta, int n_grid, int m_max, int* m_star,
+                    double* err, void* stream) {
+  SC_CHECK_ARG(m_star, "null m_star");
+  SC_CHECK_ARG(ratio > 0.0 && ratio <= 1.0 && delta > 0.0 && theta >= 0.0 && theta < 1.0,
+               "0 < ratio <= 1, delta > 0, 0 <= theta < 1 required");
+  SC_CHECK_ARG(n_grid >= 2 && n_grid <= (1 << 24) && m_max >= 1 && m_max <= 4096,
+               "2 <= n_grid <= 2^24 and 1 <= m_max <= 4096 required");
+  return filter_order(ratio, delta, jackson != 0, theta, n_grid, m_max, m_star, err, as_stream(stream));
+}
+
 static int random_common_check(int64_t n, int R) {
   SC_CHECK_ARG(n >= 0 && R >= 1, "n >= 0 and R >= 1 required");
   return ensure_device();
@@ -516,11 +526,18 @@ int sc_profile_end(int64_t* launches, int64_t* step_launches, double* step_ms, d
   return profile_end(launches, step_launches, step_ms, algo_bytes);
 }
 
+// m* selection inside sc_cluster (order < 0): PAPER.md l.162 fixes delta = 0.1; the band and grid are
+// DESIGN.md reading R18's
+static constexpr double kOrderDelta = 0.1, kOrderTheta = 0.1;
+static constexpr int kOrderGrid = 10000, kOrderMax = 2000;
+
 int sc_cluster(sc_graph* g, int k, int R, int order, int jackson, int n_probe, uint64_t seed, int restarts,
                int max_iter, int normalize, int32_t* labels, double* info, void* stream) {
   SC_CHECK_ARG(g && labels, "null argument");
-  SC_CHECK_ARG(k >= 1 && k < g->n_rows && R >= 1 && order >= 1 && n_probe >= 1 && restarts >= 1 && max_iter >= 1,
+  SC_CHECK_ARG(k >= 1 && k < g->n_rows && R >= 1 && order != 0 && n_probe >= 1 && restarts >= 1 && max_iter >= 1,
                "bad arguments");
+  // order < 0: step 2 at order -order, step 3's m = m*(lambda~_k/lambda_N; delta = 0.1)
+  const int est_order = order > 0 ? order : -order;
   cudaStream_t s = as_stream(stream);
   // env SC_CLUSTER_TRACE: per-phase device-synchronised times on stderr (tooling)
   const bool trace = std::getenv("SC_CLUSTER_TRACE") != nullptr;
@@ -539,11 +556,17 @@ int sc_cluster(sc_graph* g, int k, int R, int order, int jackson, int n_probe, u
   double lmax = 0.0, lk = 0.0, ck = 0.0;
   SC_TRY(sc_lambda_max(g, 60, 0.01, seed ^ 0x1a2b3c4dULL, &lmax, stream));
   SC_TRY(phase(0));
-  SC_TRY(sc_estimate_lambda_k(g, k, lmax, order, 1, n_probe, seed ^ 0x5e5e5e5eULL, 40, 1e-4, &lk, &ck, stream));
+  SC_TRY(sc_estimate_lambda_k(g, k, lmax, est_order, 1, n_probe, seed ^ 0x5e5e5e5eULL, 40, 1e-4, &lk, &ck, stream));
+  int filt_order = order;
+  if (order < 0) {
+    SC_TRY(filter_order(std::min(1.0, lk / lmax), kOrderDelta, jackson != 0, kOrderTheta, kOrderGrid, kOrderMax,
+                        &filt_order, nullptr, s));
+    if (filt_order == 0) filt_order = kOrderMax;
+  }
   SC_TRY(phase(1));
   DevBuf feats;
   SC_TRY(feats.ensure(sizeof(float) * g->n_rows * R));
-  SC_TRY(sc_filter_lowpass_f32(g, lk, lmax, order, jackson, R, seed, nullptr, feats.as<float>(), stream));
+  SC_TRY(sc_filter_lowpass_f32(g, lk, lmax, filt_order, jackson, R, seed, nullptr, feats.as<float>(), stream));
   if (normalize) SC_TRY(normalize_rows_f32(feats.as<float>(), g->n_rows, R, s));
   SC_TRY(phase(2));
   double inertia = 0.0;
@@ -561,6 +584,7 @@ int sc_cluster(sc_graph* g, int k, int R, int order, int jackson, int n_probe, u
     info[3] = inertia;
     info[4] = it;
     info[5] = best;
+    info[6] = filt_order;
   }
   return SC_OK;
 }

@@ -310,6 +310,9 @@ int reduce_moment_partials(const double* part, int grid, double* out, cudaStream
 
 // host math (sc_host.cpp)
 void cheby_lowpass_coeffs(double lambda_c, double lambda_max, int order, bool jackson, double* out);
+// m*(ratio; delta) on the device (sc_order.cu); *m_star = 0 if no order <= m_max meets delta
+int filter_order(double ratio, double delta, bool jackson, double theta, int n_grid, int m_max, int* m_star,
+                 double* err_out, cudaStream_t s);
 double count_from_moments(const double* mu, int order, const double* d);
 int lambda_k_dichotomy(const double* mu, int order, int k, double lambda_max, bool jackson,
                        int max_iter, double rtol, double* lambda_k, double* count_k);

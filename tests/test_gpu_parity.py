@@ -654,6 +654,65 @@ def test_cluster_matches_oracle_pipeline(sc, normalize):
 
 
 # ---------------------------------------------------------------------------
+# filter order m* (§2.4 Eq. (4) l.151-162, §4.1 step 3 l.312; reading R18)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("ratio,jackson,delta,theta,n_grid", [
+    (1.0, False, 0.1, 0.1, 10000), (1.0, True, 0.1, 0.1, 10000), (0.5, False, 0.1, 0.1, 10000),
+    (0.5, True, 0.1, 0.1, 10000), (0.1, False, 0.1, 0.1, 10000), (0.1, True, 0.1, 0.1, 10000),
+    (0.03, False, 0.1, 0.1, 10000), (0.02, False, 0.05, 0.2, 3001), (0.3, True, 0.02, 0.05, 5000),
+    (0.77, False, 0.1, 0.1, 10000), (0.01, False, 0.1, 0.1, 10000), (0.2, True, 0.1, 0.0, 2)])
+def test_filter_order_matches_oracle(sc, ratio, jackson, delta, theta, n_grid):
+    """sc_filter_order (device Clenshaw over the grid, orders in batches) against
+    oracle.chebyshev.minimal_order (trigonometric form, one order at a time): the same m*, and
+    the grid error of m* equal to fp64 rounding.  Cases span batch boundaries (m* 1 .. ~150), a
+    tighter delta, a wider / no band, and a 2-point grid."""
+    m, err = sc.sc_filter_order(ratio, delta, jackson, theta, n_grid, 400)
+    mo = chebyshev.minimal_order(ratio, delta, jackson, 400, theta, n_grid)
+    assert m == (mo or 0)
+    if mo:
+        assert err == pytest.approx(chebyshev.approx_error(ratio, mo, jackson, theta, n_grid), abs=1e-10)
+        if mo > 1:    # not within rounding of delta, so the integer decision is unambiguous
+            assert chebyshev.approx_error(ratio, mo - 1, jackson, theta, n_grid) > delta + 1e-9
+
+
+def test_filter_order_none_found(sc):
+    """No order meets delta: m* = 0 and the error of the last order tried (theta = 0 with the cut on
+    the grid: the jump is between neighbouring grid points, reading R18)."""
+    m, err = sc.sc_filter_order(0.5, 0.1, False, 0.0, 10001, 100)
+    assert m == 0 and chebyshev.minimal_order(0.5, 0.1, False, 100, 0.0, 10001) is None
+    assert err == pytest.approx(chebyshev.approx_error(0.5, 100, False, 0.0, 10001), abs=1e-10)
+
+
+@pytest.mark.parametrize("jackson", [False, True])
+def test_cluster_with_selected_order_matches_oracle(sc, jackson):
+    """sc_cluster with order < 0 (§4.1 step 3, l.312): lambda~_k estimated at |order|,
+    then the filter at m*(lambda~_k/lambda_N; 0.1); the order it reports equals the oracle's m*
+    at the same lambda ratio, and the labels agree with the oracle pipeline run the same way."""
+    g = scinputs.sbm(2000, 5, 20, 0.05, seed=1234)
+    k, R, npr, seed, restarts, max_iter = 5, 32, 32, 2024, 10, 100
+    G = sc.Graph.from_csr(g)
+    lab = np.zeros(g.n, dtype=np.int32)
+    info = sc.sc_cluster(G.handle, k, R, -60, jackson, npr, seed, restarts, max_iter, False, lab)
+    lmax, lk, used = float(info[0]), float(info[1]), int(info[6])
+    want = chebyshev.minimal_order(min(1.0, lk / lmax), 0.1, jackson, 2000) or 2000
+    assert used == want
+    X = scinputs.gaussian_block(seed, g.n, R).astype(np.float64)
+    P = scinputs.gaussian_block(seed ^ 0x5E5E5E5E, g.n, npr, dtype=np.float64, stream=2)
+    u = np.stack([scinputs.uniforms(seed, k, offset=k * r) for r in range(restarts)])
+    out = pipeline.accelerated_sc(g, k, X, P, -60, jackson, u, lambda_max_value=lmax, max_iter=max_iter,
+                                  bisect_iter=40, bisect_rtol=1e-4)
+    if out["lambda_k"] == lk:
+        assert out["order"] == used
+    assert oari.ari(lab, out["labels"]) >= 0.99
+    # the same order given explicitly reproduces the labels bit for bit
+    lab2 = np.zeros(g.n, dtype=np.int32)
+    info2 = sc.sc_cluster(G.handle, k, R, used, jackson, npr, seed, restarts, max_iter, False, lab2)
+    if info2[1] == lk:
+        assert np.array_equal(lab, lab2)
+
+
+# ---------------------------------------------------------------------------
 # stability measure gamma(k) (PAPER.md §4.3 Eq.(11))
 # ---------------------------------------------------------------------------
 

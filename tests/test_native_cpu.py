@@ -91,6 +91,13 @@ def test_argument_errors(sc):
         sc.sc_cheby_coeffs(1.0, -1.0, 5, False)
     with pytest.raises(sc.SCError):
         sc.sc_lambda_k_from_moments(np.zeros(11), 5, 0, 4.0, True)
+    # sc_filter_order: ratio outside (0, 1], delta <= 0, theta outside [0, 1), n_grid < 2, m_max outside [1, 4096]
+    for bad in [dict(ratio=0.0), dict(ratio=1.5), dict(delta=0.0), dict(theta=-0.1), dict(theta=1.0),
+                dict(n_grid=1), dict(m_max=0), dict(m_max=5000)]:
+        kw = dict(ratio=0.1, delta=0.1, jackson=False, theta=0.1, n_grid=100, m_max=10)
+        kw.update(bad)
+        with pytest.raises(sc.SCError):
+            sc.sc_filter_order(**kw)
 
 
 def test_argument_errors_new_entry_points(sc):

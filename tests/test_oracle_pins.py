@@ -431,6 +431,58 @@ def test_poly_eval_against_chebval_and_hand_values():
     assert chebyshev.poly_eval(0.0, d, 4.0) == pytest.approx(npcheb.chebval(-1.0, d), rel=1e-12)
 
 
+def _recurrence_error(ratio, m, damping, theta=0.1, n_grid=10000):
+    """|h - p_m| on the order grid with p_m evaluated a second way: the three-term
+    recurrence of cheb_filter (pinned above on closed-form spectra) applied to the diagonal
+    matrix diag(grid), i.e. the filter's own route, not the trigonometric form."""
+    lam = chebyshev.order_grid(ratio, theta, n_grid)
+    D = sp.diags(lam).tocsr()
+    p = chebyshev.cheb_filter(D, np.ones((lam.size, 1)), chebyshev.filter_coeffs(ratio, 1.0, m, damping),
+                              1.0)[:, 0]
+    return np.max(np.abs((lam <= ratio).astype(float) - p))
+
+
+def test_minimal_order_special_cases_and_monotone():
+    """oracle/chebyshev.py minimal_order (§2.4 Eq. (4) l.151-162, reading R18).
+    ratio = 1: h = 1 on [0, 1], c = (1, 0, ...), so m* = 1 with zero error (damped or not);
+    sharper cuts need higher orders (m* non-increasing in the ratio on a decade grid; PAPER.md
+    §5 l.407-409: small lambda_k/lambda_N "necessitates a large m"); Jackson damping widens the
+    transition, so it never needs a lower order than the undamped series at these ratios; a
+    stricter delta never needs a lower order."""
+    for damping in (False, True):
+        assert chebyshev.minimal_order(1.0, 0.1, damping, 10) == 1
+        assert chebyshev.approx_error(1.0, 1, damping) == pytest.approx(0.0, abs=1e-15)
+    ms = [chebyshev.minimal_order(r, 0.1, False, 300) for r in (1e-2, 3e-2, 1e-1, 0.5)]
+    assert all(a > b for a, b in zip(ms, ms[1:])), ms
+    msd = [chebyshev.minimal_order(r, 0.1, True, 300) for r in (1e-1, 0.3, 0.5)]
+    assert all(a > b for a, b in zip(msd, msd[1:])), msd
+    assert msd[0] >= ms[2] and msd[2] >= ms[3]
+    assert chebyshev.minimal_order(0.1, 0.05, False, 300) >= ms[2]
+
+
+@pytest.mark.parametrize("ratio,damping", [(0.5, False), (0.1, False), (0.03, True), (0.3, True)])
+def test_minimal_order_against_recurrence_route(ratio, damping):
+    """The error approx_error measures equals the one of the recurrence route, and m* is
+    minimal under that route: m* meets delta, m* - 1 does not (a wrong band, coefficient or
+    damping flag in either route fails this)."""
+    m = chebyshev.minimal_order(ratio, 0.1, damping, 400)
+    assert m is not None and m >= 2
+    for mm in (m - 1, m, m + 3):
+        assert chebyshev.approx_error(ratio, mm, damping) == pytest.approx(
+            _recurrence_error(ratio, mm, damping), abs=1e-9)
+    assert _recurrence_error(ratio, m, damping) <= 0.1
+    assert _recurrence_error(ratio, m - 1, damping) > 0.1
+
+
+def test_minimal_order_band_is_required():
+    """Without the transition band (theta = 0) and with lambda_c on the grid, h jumps between
+    grid points 1/(n_grid-1) apart, and a continuous polynomial of moderate order cannot stay
+    within 0.1 of both sides (its value at the cut and the neighbour differ by < 0.8 for
+    m <= 300): no order is found -- the reason for reading R18."""
+    assert chebyshev.minimal_order(0.5, 0.1, False, 300, theta=0.0, n_grid=10001) is None
+    assert chebyshev.minimal_order(0.5, 0.1, False, 300, theta=0.1, n_grid=10001) is not None
+
+
 def test_kmeans_inertia_monotone():
     X = _blobs(7, spread=2.0).astype(np.float64)
     C = X[:4].copy()
