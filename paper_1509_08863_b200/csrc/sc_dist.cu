@@ -594,9 +594,10 @@ int sc_dist_filter_f32(sc_dist* d, const double* coeffs, int order, double lambd
   const std::vector<int> chunks = chunk_widths<float>(Rp, nc);
   int cwmax = 0;
   for (int w : chunks) cwmax = std::max(cwmax, w);
-  SC_TRY(d->tA.ensure(sizeof(float) * nc * cwmax));
-  SC_TRY(d->tB.ensure(sizeof(float) * nc * cwmax));
-  SC_TRY(d->tC.ensure(sizeof(float) * nc * cwmax));
+  // + one row: the all-zero row n_cols that the SELL kernel's padding gathers
+  SC_TRY(d->tA.ensure(sizeof(float) * (nc + 1) * cwmax));
+  SC_TRY(d->tB.ensure(sizeof(float) * (nc + 1) * cwmax));
+  SC_TRY(d->tC.ensure(sizeof(float) * (nc + 1) * cwmax));
   SC_TRY(d->sendbuf.ensure(sizeof(float) * std::max<int64_t>(1, d->n_send) * cwmax));
   float* Yw = Yd;
   int64_t ldy = R;
@@ -612,6 +613,7 @@ int sc_dist_filter_f32(sc_dist* d, const double* coeffs, int order, double lambd
     float* bufs[2] = {d->tC.as<float>(), d->tB.as<float>()};   // T_j (j >= 1) in bufs[j & 1]
     // T_0 = X[:, col0 : col0 + w] (zero beyond R), halo rows filled by the step-0 exchange
     SC_CUDA_TRY(cudaMemsetAsync(A, 0, sizeof(float) * nl * w, cs));
+    for (float* b : {A, bufs[0], bufs[1]}) SC_CUDA_TRY(cudaMemsetAsync(b + nc * w, 0, sizeof(float) * w, cs));
     const int wx = std::min(w, R - col0);
     if (wx > 0) {
       if (wx == w) {
@@ -651,11 +653,11 @@ int sc_dist_filter_f32(sc_dist* d, const double* coeffs, int order, double lambd
       }
       p.row_begin = 0;
       p.row_end = d->n_interior;
-      SC_TRY(launch_step<float>(d->g, p, cs));
+      SC_TRY(launch_step_any<float>(d->g, p, cs));
       if (d->c->world > 1 && (d->n_send || d->n_halo)) SC_CUDA_TRY(cudaStreamWaitEvent(cs, d->c->ev_comm, 0));
       p.row_begin = d->n_interior;
       p.row_end = nl;
-      SC_TRY(launch_step<float>(d->g, p, cs));
+      SC_TRY(launch_step_any<float>(d->g, p, cs));
     }
     col0 += w;
   }

@@ -585,6 +585,8 @@ void setaside_once() {
   (void)done;
 }
 
+}  // namespace
+
 // dynamic tile scheduling of the step kernel (env SC_DYN_TILES=0 disables)
 bool dyn_tiles_on() {
   static const bool v = env_int("SC_DYN_TILES", 1) != 0;
@@ -604,6 +606,8 @@ unsigned* next_tile_ctr(const sc_graph* g, cudaStream_t s) {
   const int idx = static_cast<int>(g->tile_ctr_seq++ % kTileCtrRing);
   return g->tile_ctr_ring.as<unsigned>() + idx;
 }
+
+namespace {
 
 // step launches with programmatic dependent launch (env SC_PDL=0 disables; measured neutral on
 // configs[3]: 115.2 vs 115.3 ms per pass -- a ~290 us launch has little prologue to hide)

@@ -250,6 +250,13 @@ int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end
                 int64_t split_col = 0);
 int64_t sell_split_col(const sc_graph* g, int width, size_t elem);   // 0: no split gather
 void sell_release(const sc_graph* g);      // drop the graph's cached SELL plans
+bool dyn_tiles_on();                       // env SC_DYN_TILES (default 1)
+unsigned* next_tile_ctr(const sc_graph* g, cudaStream_t s);   // a self-resetting tile counter slot
+// one fused step of the row-partitioned paths: the SELL kernel when it can run this chunk width
+// and row range (the caller keeps row n_cols of p.tcur, stride p.ld_cur, zero), else the
+// plain-CSR kernel; fused-exchange epilogue (p.p2p) on either
+template <typename T>
+int launch_step_any(const sc_graph* g, StepParams p, cudaStream_t s);
 
 // degree-sorted row order of every tile of tr rows over [row_begin, row_end) (cached on g)
 const uint16_t* tile_order(const sc_graph* g, int tr, int64_t row_begin, int64_t row_end, cudaStream_t s);

@@ -127,6 +127,11 @@ int chunk_start(RankRun& r, int col0, int w, int R, cudaStream_t s) {
   const int wx = std::max(0, std::min(w, R - col0));
   p2p_take_cols_kernel<<<p->g->num_sms * 4, 256, 0, s>>>(r.X, R, col0, wx, p->n_local, w, A);
   SC_CUDA_TRY(cudaGetLastError());
+  // row n_cols of every buffer (stride w): the zero row the SELL kernel's padding gathers (peers
+  // store only into rows [n_local, n_cols); an earlier chunk of another width may have left
+  // data here)
+  const int64_t nc = p->n_local + p->n_halo;
+  for (int b = 0; b < 3; ++b) SC_CUDA_TRY(cudaMemsetAsync(p->buf[b].as<float>() + nc * w, 0, sizeof(float) * w, s));
   return SC_OK;
 }
 
@@ -182,7 +187,7 @@ int step(RankRun& r, const double* coeffs, int order, double lambda_max, int Rp,
   q.p2p = p->world > 1 ? p->dev.as<P2PDev>() : nullptr;   // one rank: nothing to send or signal
   q.p2p_next = bidx[(st + 1) & 1];
   q.p2p_signal = ++p->seq;
-  return launch_step<float>(p->g, q, s);
+  return launch_step_any<float>(p->g, q, s);
 }
 
 int prepare(sc_p2p* p, int R, float* Y, float*& Yw, int64_t& ldy, cudaStream_t s) {
@@ -228,9 +233,9 @@ int sc_p2p_create(sc_graph* g, int world, int rank, int64_t n_global, const int6
   p->rp_max = (max_R + 3) / 4 * 4;
   const int64_t nc = g->n_cols;
   int rc;
-  for (int b = 0; b < 3; ++b) {
-    if ((rc = p->buf[b].ensure(sizeof(float) * std::max<int64_t>(1, nc) * p->rp_max)) != SC_OK) return bail(rc);
-    if (cudaMemset(p->buf[b].ptr, 0, sizeof(float) * std::max<int64_t>(1, nc) * p->rp_max) != cudaSuccess)
+  for (int b = 0; b < 3; ++b) {   // + one row: the SELL kernel's zero row n_cols
+    if ((rc = p->buf[b].ensure(sizeof(float) * (nc + 1) * p->rp_max)) != SC_OK) return bail(rc);
+    if (cudaMemset(p->buf[b].ptr, 0, sizeof(float) * (nc + 1) * p->rp_max) != cudaSuccess)
       return bail(fail(SC_ERR_CUDA, "buffer init failed"));
   }
   if ((rc = p->flags.ensure(sizeof(int64_t) * kP2PMaxWorld)) != SC_OK) return bail(rc);

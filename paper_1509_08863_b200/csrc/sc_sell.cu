@@ -261,7 +261,7 @@ template <int RPW, int NB, bool UNIT> struct Gather<double, RPW, NB, UNIT> {
   }
 };
 
-template <typename T, int VPR, int NB, bool UNIT>
+template <typename T, int VPR, int NB, bool UNIT, bool P2P>
 __global__ void __launch_bounds__(kThreads, SC_SELL_MIN_CTAS)
 cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int cap, int cfg) {
   constexpr int W = Vec<T>::W;
@@ -453,11 +453,40 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
         tn[w] = a * lt + bc * own[w] + bp * prv[w];      // T_{s+1}[i]
       }
       if (tnext) Vec<T>::st(tnext + (int64_t)row * p.ld_next + c, tn);   // gathered next step: normal L2 policy
+      if (P2P && tnext && row >= p.p2p->row0) {
+        // fused halo exchange (multi-GPU): the peers that read this row get it straight into
+        // their halo rows of the same buffer (NVLink stores from the epilogue)
+        const P2PDev* x = p.p2p;
+        const int64_t e1 = x->sd_ptr[row + 1];
+        for (int64_t e = x->sd_ptr[row]; e < e1; ++e) {
+          const int q = x->sd_peer[e];
+          T* dst = static_cast<T*>(x->peer_buf[p.p2p_next][q]) + (x->peer_nl[q] + x->sd_slot[e]) * p.ld_next + c;
+          Vec<T>::st(dst, tn);
+        }
+      }
       if (p.y_mode) {
         const T cyp = static_cast<T>(p.cy_prev), cyc = static_cast<T>(p.cy_cur), cyn = static_cast<T>(p.cy_next);
 #pragma unroll
         for (int w = 0; w < W; ++w) yv[w] += cyp * prv[w] + cyc * own[w] + cyn * tn[w];
         Stream<T>::st(y + (int64_t)row * p.ld_y + c, yv, policy_evict_first());
+      }
+    }
+  }
+
+  if (P2P) {
+    // publish completion to the peers (as cheb_step_kernel): every consumer thread fences its
+    // remote stores, the last CTA to finish writes p2p_signal into each peer's flags (release)
+    __threadfence_system();
+    asm volatile("bar.sync 2, %0;" ::"r"(kNC * 32) : "memory");
+    if (threadIdx.x == 0) {
+      const P2PDev* x = p.p2p;
+      if (atomicAdd(x->done_ctr, 1u) == gridDim.x - 1) {
+        *x->done_ctr = 0u;
+        __threadfence_system();
+        for (int q = 0; q < x->world; ++q)
+          if (q != x->rank)
+            asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(x->peer_flags[q] + x->rank), "l"(p.p2p_signal)
+                         : "memory");
       }
     }
   }
@@ -911,29 +940,33 @@ HubFn<T> pick_hub(int vpr, bool unit) {
 }
 
 template <typename T, int VPR>
-SellFn<T> pick_sell_unit(bool unit) {
+SellFn<T> pick_sell_unit(bool unit, bool p2p) {
+  // P2P: the fused-exchange epilogue of the row-partitioned fp32 path (a separate
+  // instantiation: the single-GPU kernels keep their register allocation)
   if constexpr (sizeof(T) == 4) {
-    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB, true>;
-    return cheb_sell_kernel<T, VPR, SC_SELL_NB_W, false>;
+    if (p2p) return unit ? cheb_sell_kernel<T, VPR, SC_SELL_NB, true, true> : cheb_sell_kernel<T, VPR, SC_SELL_NB_W, false, true>;
+    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB, true, false>;
+    return cheb_sell_kernel<T, VPR, SC_SELL_NB_W, false, false>;
   } else {
-    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, true>;
-    return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, false>;
+    if (p2p) return nullptr;
+    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, true, false>;
+    return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, false, false>;
   }
 }
 
 template <typename T>
-SellFn<T> pick_sell(int vpr, bool unit) {
+SellFn<T> pick_sell(int vpr, bool unit, bool p2p = false) {
   switch (vpr) {
-    case 1: return pick_sell_unit<T, 1>(unit);
-    case 2: return pick_sell_unit<T, 2>(unit);
-    case 3: return pick_sell_unit<T, 3>(unit);
-    case 4: return pick_sell_unit<T, 4>(unit);
-    case 6: return pick_sell_unit<T, 6>(unit);
-    case 8: return pick_sell_unit<T, 8>(unit);
-    case 12: return pick_sell_unit<T, 12>(unit);
-    case 16: return pick_sell_unit<T, 16>(unit);
-    case 24: return pick_sell_unit<T, 24>(unit);
-    case 32: return pick_sell_unit<T, 32>(unit);
+    case 1: return pick_sell_unit<T, 1>(unit, p2p);
+    case 2: return pick_sell_unit<T, 2>(unit, p2p);
+    case 3: return pick_sell_unit<T, 3>(unit, p2p);
+    case 4: return pick_sell_unit<T, 4>(unit, p2p);
+    case 6: return pick_sell_unit<T, 6>(unit, p2p);
+    case 8: return pick_sell_unit<T, 8>(unit, p2p);
+    case 12: return pick_sell_unit<T, 12>(unit, p2p);
+    case 16: return pick_sell_unit<T, 16>(unit, p2p);
+    case 24: return pick_sell_unit<T, 24>(unit, p2p);
+    case 32: return pick_sell_unit<T, 32>(unit, p2p);
     default: return nullptr;
   }
 }
@@ -1032,7 +1065,7 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
   constexpr int W = Vec<T>::W;
   if (p.width % W) return fail(SC_ERR_ARG, "unsupported chunk width " + std::to_string(p.width));
   const int vpr = p.width / W;
-  SellFn<T> k = pick_sell<T>(vpr, g->unit_weights);
+  SellFn<T> k = pick_sell<T>(vpr, g->unit_weights, p.p2p != nullptr);
   if (!k) return fail(SC_ERR_ARG, "unsupported chunk width " + std::to_string(p.width));
   const int tr = sell_tile_rows(vpr);
   SellPlan* pl = nullptr;
@@ -1111,6 +1144,17 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
   }
   return SC_OK;
 }
+template <typename T>
+int launch_step_any(const sc_graph* g, StepParams p, cudaStream_t s) {
+  bool ok = false;
+  if (sell_enabled() && (sizeof(T) == 4 || !p.p2p)) SC_TRY(sell_usable<T>(g, p.width, p.row_begin, p.row_end, s, &ok));
+  if (!ok) return launch_step<T>(g, p, s);
+  p.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
+  return launch_sell_step<T>(g, p, s, nullptr);
+}
+template int launch_step_any<float>(const sc_graph*, StepParams, cudaStream_t);
+template int launch_step_any<double>(const sc_graph*, StepParams, cudaStream_t);
+
 template int launch_sell_step<float>(const sc_graph*, const StepParams&, cudaStream_t, double*);
 template int launch_sell_step<double>(const sc_graph*, const StepParams&, cudaStream_t, double*);
 

@@ -959,14 +959,17 @@ def test_partitioned_pipeline_emulated(sc, world, normalize):
     assert oari.ari(lab, g.labels) > 0.95
 
 
+@pytest.mark.parametrize("sell", ["1", "0"])
 @pytest.mark.parametrize("world,R,chunk,waits", [(2, 16, None, False), (3, 6, None, False), (4, 16, "8", False),
                                                  (2, 12, "4", False), (1, 8, None, False), (3, 16, "8", True)])
-def test_p2p_fused_exchange_emulated(sc, world, R, chunk, waits, monkeypatch):
+def test_p2p_fused_exchange_emulated(sc, world, R, chunk, waits, sell, monkeypatch):
     """The fused-exchange filter (sc_p2p_*): every rank's step kernel stores its boundary rows
     of T_{s+1} straight into the peers' halos.  All ranks held by this process on one GPU
     (sc_p2p_filter_group_f32: dependency-ordered launches on one stream, nothing waits), incl.
-    several column chunks, a ragged R and world 1 -- vs the oracle on the whole graph."""
+    several column chunks, a ragged R and world 1 -- vs the oracle on the whole graph.  Both
+    step kernels carry the exchange epilogue: the SELL kernel (default) and the CSR kernel."""
     from paper_1509_08863_b200 import dist as pdist
+    monkeypatch.setenv("SC_SELL", sell)
     if chunk:
         monkeypatch.setenv("SC_CHUNK", chunk)
     if waits:   # also run the flag waits of the multi-process path (each already satisfied)
@@ -991,6 +994,42 @@ def test_p2p_fused_exchange_emulated(sc, world, R, chunk, waits, monkeypatch):
             assert rel(Y, Yo) <= F32_TOL
         if world > 1:
             assert all(p.n_halo > 0 for p in grp.parts)
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("world,hub", [(2, "8"), (3, "4"), (2, "100000")])
+def test_p2p_fused_exchange_weighted_split_rows(sc, world, hub, monkeypatch):
+    """The SELL kernel's fused-exchange epilogue on a weighted graph with hub rows: rows above
+    the split threshold (SC_SELL_HUB_DEG) are summed in chunks by hub_chunk_kernel and still
+    stored into the peers' halos by the epilogue; two column chunks (SC_CHUNK 8, R = 16)."""
+    from paper_1509_08863_b200 import dist as pdist
+    monkeypatch.setenv("SC_SELL_HUB_DEG", hub)
+    monkeypatch.setenv("SC_CHUNK", "8")
+    base = scinputs.random_connected(1500, 0.01, seed=9, weighted=True)
+    # a star on top: node 0 joined to every 3rd node (degree ~500: a split row)
+    src = np.repeat(np.arange(base.n), np.diff(base.row_ptr))
+    keep = src < base.col_idx
+    star = np.arange(3, base.n, 3)
+    g = scinputs.from_edges(base.n, np.concatenate([src[keep], np.zeros(star.size, np.int64)]),
+                            np.concatenate([base.col_idx[keep], star]),
+                            np.concatenate([base.values[keep], np.full(star.size, 0.7, np.float32)]))
+    assert g.degrees()[0] > 400
+    R, order = 16, 25
+    L = laplacian.laplacian(g)
+    lmax = 2.0 * float(L.diagonal().max())   # Gershgorin: 2 max_i s_i
+    d = chebyshev.filter_coeffs(0.1 * lmax, lmax, order, False)
+    X = scinputs.gaussian_block(6, g.n, R)
+    grp = pdist.P2PGroup(g.row_ptr, g.col_idx, g.values, g.n, world, R)
+    try:
+        Xs = [torch.from_numpy(np.ascontiguousarray(X[p.r0:p.r1][p.perm])).cuda() for p in grp.parts]
+        Ys = [torch.full_like(x, float("nan")) for x in Xs]
+        grp.filter(d, order, lmax, Xs, Ys)
+        torch.cuda.synchronize()
+        Y = np.zeros((g.n, R))
+        for p, y in zip(grp.parts, Ys):
+            Y[p.r0 + p.perm] = y.cpu().numpy()
+        assert rel(Y, chebyshev.cheb_filter(L, X.astype(np.float64), d, lmax)) <= F32_TOL
     finally:
         grp.close()
 
