@@ -1081,6 +1081,18 @@ template int filter_apply<double>(sc_graph*, const double*, int, double, int, co
 // ---------------------------------------------------------------------------
 // Chebyshev moments mu_0..mu_{2p} (fp64), DESIGN.md "eigencount"
 // ---------------------------------------------------------------------------
+// Sum of fixed-point limbs (see mom_limb in sc_sell.cu): V = sum_l acc_l 2^(32 l) mod 2^128 is
+// the exact two's-complement sum of the partials x 2^80; returned as a double (V x 2^-80).
+double limbs_to_double(const unsigned long long* acc) {
+  unsigned __int128 v = 0;
+  for (int l = 0; l < 4; ++l) v += static_cast<unsigned __int128>(acc[l]) << (32 * l);
+  const bool neg = (v >> 127) != 0;
+  const unsigned __int128 m = neg ? (~v + 1) : v;
+  const double d = std::ldexp(static_cast<double>(static_cast<uint64_t>(m >> 64)), 64) +
+                   static_cast<double>(static_cast<uint64_t>(m));
+  return std::ldexp(neg ? -d : d, -80);
+}
+
 int cheb_moments(sc_graph* g, double lambda_max, int order, int R, const double* X,
                  std::vector<double>& mu, cudaStream_t s) {
   using T = double;
@@ -1112,6 +1124,50 @@ int cheb_moments(sc_graph* g, double lambda_max, int order, int R, const double*
   for (int w : chunks) {
     T* bufs[2] = {g->ws_b.as<T>(), g->ws_a.as<T>()};
     const T* Xc = Xw + col0;
+    bool use_sell = false;
+    if (sell_enabled()) SC_TRY(sell_usable<T>(g, w, 0, n, s, &use_sell));
+    if (use_sell) {
+      // SELL path (the filter's kernel with the moment epilogue): T_0 = the X chunk copied into
+      // bufs[0] (row stride w), zero row n_cols in both buffers; the three sums of every step
+      // as exact fixed-point limbs [order][3][4] (order independent: dynamic tiles stay
+      // deterministic), converted on the host
+      SC_TRY(g->ws_a.ensure((size_t)(g->n_cols + 1) * cwmax * sizeof(T)));
+      SC_TRY(g->ws_b.ensure((size_t)(g->n_cols + 1) * cwmax * sizeof(T)));
+      bufs[0] = g->ws_b.as<T>();
+      bufs[1] = g->ws_a.as<T>();
+      SC_TRY(g->ws_limbs.ensure(sizeof(unsigned long long) * 12 * (size_t)order));
+      unsigned long long* limbs = g->ws_limbs.as<unsigned long long>();
+      SC_CUDA_TRY(cudaMemsetAsync(limbs, 0, sizeof(unsigned long long) * 12 * (size_t)order, s));
+      SC_CUDA_TRY(cudaMemsetAsync(bufs[0] + (size_t)g->n_cols * w, 0, sizeof(T) * w, s));
+      SC_CUDA_TRY(cudaMemsetAsync(bufs[1] + (size_t)g->n_cols * w, 0, sizeof(T) * w, s));
+      copy_cols_kernel<T><<<g->num_sms * 8, 256, 0, s>>>(Xc, Rp, bufs[0], w, n, w);
+      SC_CUDA_TRY(cudaGetLastError());
+      for (int st = 0; st < order; ++st) {
+        StepParams p{};
+        p.row_begin = 0;
+        p.row_end = n;
+        p.width = w;
+        p.total_width = Rp;
+        p.tcur = bufs[st & 1];
+        p.ld_cur = w;
+        p.tprev = st == 0 ? nullptr : (const void*)bufs[(st - 1) & 1];
+        p.ld_prev = w;
+        p.tnext = st == order - 1 ? nullptr : (void*)bufs[(st + 1) & 1];
+        p.ld_next = w;
+        p.a = (st == 0 ? 2.0 : 4.0) / lambda_max;
+        p.b_cur = st == 0 ? -1.0 : -2.0;
+        p.b_prev = st == 0 ? 0.0 : -1.0;
+        p.mom_limbs = limbs + 12 * (size_t)st;
+        p.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
+        SC_TRY(launch_sell_step<T>(g, p, s, nullptr));
+      }
+      std::vector<unsigned long long> hl((size_t)12 * order);
+      SC_CUDA_TRY(cudaMemcpyAsync(hl.data(), limbs, sizeof(unsigned long long) * hl.size(), cudaMemcpyDeviceToHost, s));
+      SC_CUDA_TRY(cudaStreamSynchronize(s));
+      for (size_t i = 0; i < (size_t)3 * order; ++i) acc[i] += limbs_to_double(&hl[4 * i]);
+      col0 += w;
+      continue;
+    }
     for (int st = 0; st < order; ++st) {
       StepParams p{};
       p.row_begin = 0;

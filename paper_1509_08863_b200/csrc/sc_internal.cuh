@@ -160,7 +160,7 @@ struct sc_graph {
   sc::DevBuf strength64;  // double [n_rows]
   sc::DevBuf strength32;  // float  [n_rows]
   // workspace (grow-only)
-  sc::DevBuf ws_a, ws_b, ws_sig, ws_part, ws_misc, ws_split;
+  sc::DevBuf ws_a, ws_b, ws_sig, ws_part, ws_misc, ws_split, ws_limbs;
   // per (tile rows, row_begin, row_end): degree-sorted row order inside each tile (uint16)
   mutable std::map<std::tuple<int, int64_t, int64_t>, std::unique_ptr<sc::DevBuf>> tile_orders;
   mutable std::mutex tile_orders_mu;
@@ -216,6 +216,9 @@ struct StepParams {
   int total_width;   // all columns of the block (for the profiler's CSR share)
   // moments mode (fp64 only): per-block partial sums written to `part`
   double* part;      // [gridDim.x][3] : <Tc,Tc>, <Tn,Tc>, <Tn,Tn>
+  // moments on the SELL kernel (fp64): the three sums as exact fixed-point integers (value
+  // x 2^80, four 32-bit limbs each accumulated in a uint64 -- order independent), [3][4]
+  unsigned long long* mom_limbs;
   // fused exchange (nullptr: none): T_{s+1} rows also stored into the peers' buffer
   // p2p_next; after the launch the last CTA publishes p2p_signal in every peer's flags
   const P2PDev* p2p;

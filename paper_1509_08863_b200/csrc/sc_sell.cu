@@ -261,7 +261,20 @@ template <int RPW, int NB, bool UNIT> struct Gather<double, RPW, NB, UNIT> {
   }
 };
 
-template <typename T, int VPR, int NB, bool UNIT, bool P2P>
+// Fixed-point image of a moment partial for the order-independent sums: v x 2^80 as a signed
+// 128-bit integer (hi x 2^64 + lo), returned as limb `l` (32 bits) of its two's complement.
+// |v| < 2^47 (moment partials are bounded by ||X||_F^2); bits below 2^-80 are dropped (floor).
+__device__ __forceinline__ unsigned long long mom_limb(double v, int l) {
+  const double x = v * 0x1.0p80;
+  const double hi = floor(x * 0x1.0p-64);
+  const double r = x - hi * 0x1.0p64;          // exact, in [0, 2^64)
+  const unsigned long long lo = __double2ull_rz(r);
+  const unsigned long long h = static_cast<unsigned long long>(__double2ll_rz(hi));
+  const unsigned long long w = (l < 2) ? lo : h;
+  return (l & 1) ? (w >> 32) : (w & 0xffffffffull);
+}
+
+template <typename T, int VPR, int NB, bool UNIT, bool P2P, bool MOM>
 __global__ void __launch_bounds__(kThreads, SC_SELL_MIN_CTAS)
 cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int cap, int cfg) {
   constexpr int W = Vec<T>::W;
@@ -359,6 +372,9 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
   T* d_own = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 0) * 32 + lane) * 16);
   T* d_prv = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 1) * 32 + lane) * 16);
   T* d_y = reinterpret_cast<T*>(dense + ((size_t)(warp * 3 + 2) * 32 + lane) * 16);
+  // MOM: lane l < 12 accumulates limb l % 4 of moment sum l / 4 over the warp's tiles (exact
+  // integer adds: the result does not depend on which tiles the warp got)
+  unsigned long long mom_acc = 0;
 
   for (int i = 0;; ++i) {
     const int s = i % S;
@@ -385,6 +401,7 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
       if (p.y_mode == 2) cp_async16_nohint(d_y, y + (int64_t)row * p.ld_y + c);
     }
     const int lsub = sub < RPW ? sub : 0;
+    double m_cc = 0.0, m_nc = 0.0, m_nn = 0.0;   // MOM: this lane's terms of the tile
     T acc[W];
     {
       // every tile fits a stage (launch_sell_step checks the plan's largest tile)
@@ -470,9 +487,40 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
         for (int w = 0; w < W; ++w) yv[w] += cyp * prv[w] + cyc * own[w] + cyn * tn[w];
         Stream<T>::st(y + (int64_t)row * p.ld_y + c, yv, policy_evict_first());
       }
+      if (MOM) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          m_cc += (double)own[w] * (double)own[w];
+          m_nc += (double)tn[w] * (double)own[w];
+          m_nn += (double)tn[w] * (double)tn[w];
+        }
+      }
+    }
+    if (MOM) {
+      // the warp's tile partial (fixed shuffle order), then its fixed-point limbs
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        m_cc += __shfl_xor_sync(0xffffffffu, m_cc, o);
+        m_nc += __shfl_xor_sync(0xffffffffu, m_nc, o);
+        m_nn += __shfl_xor_sync(0xffffffffu, m_nn, o);
+      }
+      const int comp = lane >> 2;
+      const double v = comp == 0 ? m_cc : (comp == 1 ? m_nc : m_nn);
+      if (lane < 12) mom_acc += mom_limb(v, lane & 3);
+      m_cc = m_nc = m_nn = 0.0;
     }
   }
 
+  if (MOM) {
+    // CTA: the warps' limbs added in shared memory (integers: any order), then one global add
+    // per limb
+    __shared__ unsigned long long s_mom[12];
+    if (threadIdx.x < 12) s_mom[threadIdx.x] = 0ull;
+    asm volatile("bar.sync 3, %0;" ::"r"(kNC * 32) : "memory");
+    if (lane < 12) atomicAdd(&s_mom[lane], mom_acc);
+    asm volatile("bar.sync 3, %0;" ::"r"(kNC * 32) : "memory");
+    if (threadIdx.x < 12) atomicAdd(p.mom_limbs + threadIdx.x, s_mom[threadIdx.x]);
+  }
   if (P2P) {
     // publish completion to the peers (as cheb_step_kernel): every consumer thread fences its
     // remote stores, the last CTA to finish writes p2p_signal into each peer's flags (release)
@@ -940,33 +988,38 @@ HubFn<T> pick_hub(int vpr, bool unit) {
 }
 
 template <typename T, int VPR>
-SellFn<T> pick_sell_unit(bool unit, bool p2p) {
+SellFn<T> pick_sell_unit(bool unit, bool p2p, bool mom) {
   // P2P: the fused-exchange epilogue of the row-partitioned fp32 path (a separate
   // instantiation: the single-GPU kernels keep their register allocation)
+  // MOM: the eigencount moments (fp64 only)
   if constexpr (sizeof(T) == 4) {
-    if (p2p) return unit ? cheb_sell_kernel<T, VPR, SC_SELL_NB, true, true> : cheb_sell_kernel<T, VPR, SC_SELL_NB_W, false, true>;
-    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB, true, false>;
-    return cheb_sell_kernel<T, VPR, SC_SELL_NB_W, false, false>;
+    if (mom) return nullptr;
+    if (p2p) return unit ? cheb_sell_kernel<T, VPR, SC_SELL_NB, true, true, false>
+                         : cheb_sell_kernel<T, VPR, SC_SELL_NB_W, false, true, false>;
+    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB, true, false, false>;
+    return cheb_sell_kernel<T, VPR, SC_SELL_NB_W, false, false, false>;
   } else {
     if (p2p) return nullptr;
-    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, true, false>;
-    return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, false, false>;
+    if (mom) return unit ? cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, true, false, true>
+                         : cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, false, false, true>;
+    if (unit) return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, true, false, false>;
+    return cheb_sell_kernel<T, VPR, SC_SELL_NB_F64, false, false, false>;
   }
 }
 
 template <typename T>
-SellFn<T> pick_sell(int vpr, bool unit, bool p2p = false) {
+SellFn<T> pick_sell(int vpr, bool unit, bool p2p = false, bool mom = false) {
   switch (vpr) {
-    case 1: return pick_sell_unit<T, 1>(unit, p2p);
-    case 2: return pick_sell_unit<T, 2>(unit, p2p);
-    case 3: return pick_sell_unit<T, 3>(unit, p2p);
-    case 4: return pick_sell_unit<T, 4>(unit, p2p);
-    case 6: return pick_sell_unit<T, 6>(unit, p2p);
-    case 8: return pick_sell_unit<T, 8>(unit, p2p);
-    case 12: return pick_sell_unit<T, 12>(unit, p2p);
-    case 16: return pick_sell_unit<T, 16>(unit, p2p);
-    case 24: return pick_sell_unit<T, 24>(unit, p2p);
-    case 32: return pick_sell_unit<T, 32>(unit, p2p);
+    case 1: return pick_sell_unit<T, 1>(unit, p2p, mom);
+    case 2: return pick_sell_unit<T, 2>(unit, p2p, mom);
+    case 3: return pick_sell_unit<T, 3>(unit, p2p, mom);
+    case 4: return pick_sell_unit<T, 4>(unit, p2p, mom);
+    case 6: return pick_sell_unit<T, 6>(unit, p2p, mom);
+    case 8: return pick_sell_unit<T, 8>(unit, p2p, mom);
+    case 12: return pick_sell_unit<T, 12>(unit, p2p, mom);
+    case 16: return pick_sell_unit<T, 16>(unit, p2p, mom);
+    case 24: return pick_sell_unit<T, 24>(unit, p2p, mom);
+    case 32: return pick_sell_unit<T, 32>(unit, p2p, mom);
     default: return nullptr;
   }
 }
@@ -1065,7 +1118,7 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
   constexpr int W = Vec<T>::W;
   if (p.width % W) return fail(SC_ERR_ARG, "unsupported chunk width " + std::to_string(p.width));
   const int vpr = p.width / W;
-  SellFn<T> k = pick_sell<T>(vpr, g->unit_weights, p.p2p != nullptr);
+  SellFn<T> k = pick_sell<T>(vpr, g->unit_weights, p.p2p != nullptr, p.mom_limbs != nullptr);
   if (!k) return fail(SC_ERR_ARG, "unsupported chunk width " + std::to_string(p.width));
   const int tr = sell_tile_rows(vpr);
   SellPlan* pl = nullptr;
@@ -1146,8 +1199,13 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
 }
 template <typename T>
 int launch_step_any(const sc_graph* g, StepParams p, cudaStream_t s) {
+  // With the fused exchange the SELL kernel pays register spills in its epilogue; measured per
+  // rank (tools/grid_emulate.py, profiles/r02_grid_emulate_c4_sell.txt): 32-column chunks
+  // equal or faster than the CSR kernel (c3, 8 ranks 21.9 vs 21.7 ms, 4 ranks 33.9 vs 35.2),
+  // 48-column chunks 12-13 % slower (c4, 4 and 8 ranks) -- wider exchange chunks stay on CSR
   bool ok = false;
-  if (sell_enabled() && (sizeof(T) == 4 || !p.p2p)) SC_TRY(sell_usable<T>(g, p.width, p.row_begin, p.row_end, s, &ok));
+  const bool p2p_wide = p.p2p && (sizeof(T) != 4 || p.width > 32);
+  if (sell_enabled() && !p2p_wide) SC_TRY(sell_usable<T>(g, p.width, p.row_begin, p.row_end, s, &ok));
   if (!ok) return launch_step<T>(g, p, s);
   p.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
   return launch_sell_step<T>(g, p, s, nullptr);

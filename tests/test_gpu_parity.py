@@ -363,7 +363,11 @@ def test_full_size_c4_oracle_columns(sc):
 # eigencount moments and lambda_k dichotomy
 # ---------------------------------------------------------------------------
 
-def test_moments_counts_match_oracle(sc):
+@pytest.mark.parametrize("sell", ["1", "0"])
+def test_moments_counts_match_oracle(sc, sell, monkeypatch):
+    """Eigencounts from the GPU moments (SELL kernel with exact fixed-point sums, or the CSR
+    kernel's fixed-order partials) against the oracle's count on the same probes."""
+    monkeypatch.setenv("SC_SELL", sell)
     g = scinputs.sbm(2000, 5, 10, 0.1, seed=1234)
     G = sc.Graph.from_csr(g)
     L = laplacian.laplacian(g)
@@ -378,15 +382,26 @@ def test_moments_counts_match_oracle(sc):
         assert abs(c - o) <= 1e-9 * mu[0]
 
 
-def test_moments_and_lambda_k_deterministic(sc):
-    """Moments are reduced in a fixed order (static tile schedule, per-CTA partials summed in
-    CTA order): repeated calls with the same seed give the same bits, at a size where many
-    CTAs share the tiles; so does the lambda_k estimate built on them."""
+@pytest.mark.parametrize("sell", ["1", "0"])
+def test_moments_and_lambda_k_deterministic(sc, sell, monkeypatch):
+    """Moments do not depend on the tile schedule -- SELL kernel: per-(warp, tile) partials
+    summed as exact fixed-point integers (dynamic tiles); CSR kernel: static tile schedule,
+    per-CTA partials summed in CTA order: repeated calls with the same seed give the same bits,
+    at a size where many CTAs share the tiles; so does the lambda_k estimate built on them
+    (ADVICE r01)."""
+    monkeypatch.setenv("SC_SELL", sell)
     g = scinputs.sbm(150_000, 20, 16, 0.05, seed=8)
     G = sc.Graph.from_csr(g)
     lmax = 2.0 * G.info()[3]
     mus = [sc.sc_cheb_moments(G.handle, lmax, 60, 16, 42) for _ in range(3)]
     assert np.array_equal(mus[0], mus[1]) and np.array_equal(mus[0], mus[2])
+    # the exact sums of the SELL path and the CSR path's rounded ones agree to fp64 rounding
+    os.environ["SC_SELL"] = "0" if sell == "1" else "1"
+    try:
+        other = sc.sc_cheb_moments(G.handle, lmax, 60, 16, 42)
+    finally:
+        os.environ["SC_SELL"] = sell
+    assert np.allclose(mus[0], other, rtol=0, atol=1e-11 * mus[0][0])
     lks = [sc.sc_estimate_lambda_k(G.handle, 20, lmax, 60, True, 16, 42, 40, 1e-4) for _ in range(2)]
     assert lks[0] == lks[1]
 
