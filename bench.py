@@ -539,11 +539,15 @@ def run_ours(args):
         ari = sc.sc_ari(labels, torch.from_numpy(g.labels).to(dev), n) if g.labels is not None else None
         # the order PAPER.md §4.1 step 3 would select at this cut (m*(lambda~_k/lambda_N; 0.1), reading
         # R18); the bench keeps the config's p (BASELINE configs fix it)
+        torch.cuda.synchronize()
+        t_ms = time.perf_counter()
         m_star, m_err = sc.sc_filter_order(min(1.0, info[1] / info[0]), 0.1, w.jackson)
+        m_star_ms = (time.perf_counter() - t_ms) * 1e3
         out["cluster_e2e"] = {"seconds": wall, "device_ms": dms, "runs_s": [round(x, 4) for x in walls], "k": w.k,
                               "restarts": w.kmeans_restarts, "lambda_max": info[0], "lambda_k": info[1],
                               "count_k": info[2], "kmeans_iters": int(info[4]), "ari_vs_planted": ari,
                               "order": int(info[6]), "m_star_at_cut": m_star, "m_star_err": m_err,
+                              "m_star_ms": round(m_star_ms, 2),
                               "api": "sc_cluster (device-resident graph)"}
 
     # ---- stability measure gamma(k) on configs[2] (§4.3 Eq.(11)): k in [10, 30],

@@ -29,8 +29,13 @@ g = configs.build_graph(wl, cache=True)
 n, R, order = g.n, w.R, w.order
 lmax = 2.0 * float(g.degrees().max())
 d = sc.sc_cheby_coeffs(0.05 * lmax, lmax, order, w.jackson)
+# optional third argument: the column-group counts to try (e.g. 1,2,4,8); default: the pure row
+# partition and the grid bench.py picks (dist.grid_shape)
+cg_list = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else None
 for world in worlds:
-    for label, cgs in (("rows", 1), ("grid", None)):
+    variants = ((("rows", 1), ("grid", None)) if cg_list is None else
+                tuple((f"grid{c}", c) for c in cg_list if world % c == 0 and R % c == 0 and (R // c) % 4 == 0))
+    for label, cgs in variants:
         n_cg, n_row = pdist.grid_shape(world, R, col_groups=cgs)
         if label == "grid" and n_cg == 1:
             continue
