@@ -550,7 +550,11 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
 // has chunks.
 // ---------------------------------------------------------------------------
 constexpr int kHubChunk = 512;
-constexpr int kHubU = 16;  // gathers in flight per lane in hub_chunk_kernel
+#ifndef SC_HUB_U
+#define SC_HUB_U 4    // gathers in flight per lane in hub_chunk_kernel: Chung-Lu 143.0 / 133.9 / 129.4 /
+#endif                // 129.6 ms per pass at 16 / 8 / 4 / 2 (profiles/r02_hub.txt, r02_hub2.txt); the
+                      // launch caps at 16 blocks per SM (env SC_HUB_BPS; 8: 129.4, 16: 127.7 ms)
+constexpr int kHubU = SC_HUB_U;
 
 struct HubChunk {
   int64_t e0;     // first edge (CSR position)
@@ -1168,7 +1172,7 @@ int launch_sell_step(const sc_graph* g, const StepParams& p, cudaStream_t s, dou
     SC_TRY(pl->hubpart.ensure(sizeof(T) * (size_t)pl->n_chunks * p.width));
     sd.hubpart = pl->hubpart.ptr;
     HubFn<T> hk = pick_hub<T>(vpr, g->unit_weights);
-    const int hgrid = (int)std::min<int64_t>((pl->n_chunks + 7) / 8, (int64_t)g->num_sms * 8);
+    const int hgrid = (int)std::min<int64_t>((pl->n_chunks + 7) / 8, (int64_t)g->num_sms * env_int_s("SC_HUB_BPS", 16));
     hk<<<hgrid, 256, 0, s>>>(pl->chunks.as<HubChunk>(), pl->n_chunks, g->col_idx.as<int32_t>(),
                              g->unit_weights ? nullptr : g->values.as<float>(), p, static_cast<T*>(pl->hubpart.ptr));
     SC_CUDA_TRY(cudaGetLastError());
