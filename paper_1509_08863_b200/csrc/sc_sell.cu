@@ -549,7 +549,10 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
 // row's chunk partials in chunk order -- deterministic, and a hub costs as many warps as it
 // has chunks.
 // ---------------------------------------------------------------------------
-constexpr int kHubChunk = 512;
+#ifndef SC_HUB_CHUNK
+#define SC_HUB_CHUNK 256   // Chung-Lu 127.4 (512) -> 126.2 ms (profiles/r02_hub3.txt)
+#endif
+constexpr int kHubChunk = SC_HUB_CHUNK;   // edges per split-row chunk (one warp each)
 #ifndef SC_HUB_U
 #define SC_HUB_U 4    // gathers in flight per lane in hub_chunk_kernel: Chung-Lu 143.0 / 133.9 / 129.4 /
 #endif                // 129.6 ms per pass at 16 / 8 / 4 / 2 (profiles/r02_hub.txt, r02_hub2.txt); the
