@@ -261,15 +261,21 @@ template <int RPW, int NB, bool UNIT> struct Gather<double, RPW, NB, UNIT> {
   }
 };
 
-// Fixed-point image of a moment partial for the order-independent sums: v x 2^80 as a signed
-// 128-bit integer (hi x 2^64 + lo), returned as limb `l` (32 bits) of its two's complement.
-// |v| < 2^47 (moment partials are bounded by ||X||_F^2); bits below 2^-80 are dropped (floor).
+// Fixed-point image of a moment partial for the order-independent sums: v x 2^80 truncated
+// toward zero to a signed 128-bit integer (hi x 2^64 + lo), returned as limb `l` (32 bits) of its
+// two's complement.  |v| < 2^47 (moment partials are bounded by ||X||_F^2).  The magnitude is
+// split exactly (r = a - hi 2^64 is exact: a itself when hi = 0, Sterbenz when hi >= 1), then
+// negated in 128-bit arithmetic.
 __device__ __forceinline__ unsigned long long mom_limb(double v, int l) {
-  const double x = v * 0x1.0p80;
-  const double hi = floor(x * 0x1.0p-64);
-  const double r = x - hi * 0x1.0p64;          // exact, in [0, 2^64)
-  const unsigned long long lo = __double2ull_rz(r);
-  const unsigned long long h = static_cast<unsigned long long>(__double2ll_rz(hi));
+  const double a = fabs(v) * 0x1.0p80;
+  const double hi = floor(a * 0x1.0p-64);
+  const double r = a - hi * 0x1.0p64;          // exact, in [0, 2^64)
+  unsigned long long lo = __double2ull_rz(r);
+  unsigned long long h = __double2ull_rz(hi);
+  if (v < 0.0) {                               // two's complement of (h, lo)
+    lo = ~lo + 1ull;
+    h = ~h + (lo == 0ull ? 1ull : 0ull);
+  }
   const unsigned long long w = (l < 2) ? lo : h;
   return (l & 1) ? (w >> 32) : (w & 0xffffffffull);
 }
