@@ -908,6 +908,84 @@ int reduce_moment_partials(const double* part, int grid, double* out, cudaStream
 // ---------------------------------------------------------------------------
 // whole filter on device buffers
 // ---------------------------------------------------------------------------
+// edges (i, j) with |i - j| < band (the ordering's locality), one pass over the CSR
+__global__ void local_edges_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, int64_t n,
+                                   int64_t band, unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      const int64_t d = (int64_t)col[e] - i;
+      c += (d < band && d > -band) ? 1ull : 0ull;
+    }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+
+// Chunk width from the graph's structure (round 2).  When the L2-budget rule of chunk_plan picks
+// 32-column chunks (the 32-column gathered table fits the budget, a 64-column one does not:
+// graphs of ~0.5-1M nodes) and the block has >= 64 columns, 64-column chunks are used instead
+// when the gathers concentrate -- power-law degrees (max degree > 8x the mean, the SELL plan's
+// skew test) or a local ordering (>= half of the edges within n/64 rows) -- so that the hot rows
+// of the 256 MB table stay in L2 and the per-row work halves.  Measured (ms per p = 200 pass,
+// R = 64, one box): Chung-Lu 119.6 vs 125.3, RCM-ordered kNN 89.8 vs 99.7, but the uniform
+// random configs[3] 110.4 vs 103.5 (`profiles/r02_tune.txt`, `r02_c3_64.txt`).  A structural
+// rule, not a timing, so a graph always gets the same width (hub rows' sums depend on it in the
+// last bits, R15).  Cached per graph; env SC_CHUNK_WIDE = 0 / 1 forces it off / on.
+int wide_chunks(sc_graph* g, cudaStream_t s, bool* wide) {
+  *wide = false;
+  const int forced = env_int("SC_CHUNK_WIDE", -1);
+  if (forced >= 0) {
+    *wide = forced != 0;
+    return SC_OK;
+  }
+  auto it = g->chunk_tuned.find(std::make_pair(0, 0));
+  if (it != g->chunk_tuned.end()) {
+    *wide = it->second != 0;
+    return SC_OK;
+  }
+  const double mean = (double)g->nnz / std::max<int64_t>(1, g->n_rows);
+  bool w = (double)max_row_degree(g, 0, g->n_rows, s) > 8.0 * std::max(1.0, mean);
+  if (!w && g->nnz > 0) {
+    DevBuf b;
+    SC_TRY(b.ensure(sizeof(unsigned long long)));
+    unsigned long long h = 0;
+    SC_CUDA_TRY(cudaMemsetAsync(b.ptr, 0, sizeof(h), s));
+    local_edges_kernel<<<g->num_sms * 8, 256, 0, s>>>(g->row_ptr.as<int64_t>(), g->col_idx.as<int32_t>(), g->n_rows,
+                                                       std::max<int64_t>(1, g->n_rows / 64),
+                                                       b.as<unsigned long long>());
+    SC_CUDA_TRY(cudaGetLastError());
+    SC_CUDA_TRY(cudaMemcpyAsync(&h, b.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SC_CUDA_TRY(cudaStreamSynchronize(s));
+    w = 2 * h >= (unsigned long long)g->nnz;
+  }
+  g->chunk_tuned[std::make_pair(0, 0)] = w ? 1 : 0;
+  *wide = w;
+  return SC_OK;
+}
+
+template <typename T>
+int tuned_chunk_plan(sc_graph* g, int Rp, cudaStream_t s, std::vector<int>* out) {
+  *out = chunk_plan<T>(Rp, g->n_cols);
+  if (sizeof(T) != 4 || Rp < 64 || env_int("SC_CHUNK", 0) > 0 || !sell_enabled() || out->empty() ||
+      (*out)[0] != 32 || g->n_cols != g->n_rows)
+    return SC_OK;
+  bool wide = false;
+  SC_TRY(wide_chunks(g, s, &wide));
+  if (!wide) return SC_OK;
+  std::vector<int> c;
+  int rem = Rp;
+  while (rem >= 64) {
+    c.push_back(64);
+    rem -= 64;
+  }
+  if (rem > 0) {
+    const std::vector<int> tail = chunk_plan<T>(rem, g->n_cols);
+    c.insert(c.end(), tail.begin(), tail.end());
+  }
+  *out = c;
+  return SC_OK;
+}
+
 template <typename T>
 int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int R, const T* X,
                  T* Y, cudaStream_t s) {
@@ -942,7 +1020,8 @@ int filter_apply(sc_graph* g, const double* d, int order, double lambda_max, int
     Xw = xp;
     Yw = yp;
   }
-  const std::vector<int> chunks = chunk_plan<T>(Rp, g->n_cols);
+  std::vector<int> chunks;
+  SC_TRY(tuned_chunk_plan<T>(g, Rp, s, &chunks));
   int cwmax = 0;
   for (int w : chunks) cwmax = std::max(cwmax, w);
   // + one row: the all-zero row n_cols that the SELL padding gathers

@@ -169,6 +169,8 @@ struct sc_graph {
   std::map<std::pair<int, int>, std::vector<int64_t>> resident_plans;
   std::map<std::pair<int, int>, std::unique_ptr<sc::DevBuf>> resident_tiles;
   sc::DevBuf resident_coef;
+  // filter_apply's structural chunk-width choice (key (0, 0): 1 = 64-column chunks)
+  std::map<std::pair<int, int>, int> chunk_tuned;
   // dynamic tile scheduling of the step kernel: one tile counter per launch from a ring of
   // kTileCtrRing slots, zeroed once; the last tile request of a launch resets its slot
   mutable sc::DevBuf tile_ctr_ring;
@@ -253,6 +255,7 @@ int sell_usable(const sc_graph* g, int width, int64_t row_begin, int64_t row_end
                 int64_t split_col = 0);
 int64_t sell_split_col(const sc_graph* g, int width, size_t elem);   // 0: no split gather
 void sell_release(const sc_graph* g);      // drop the graph's cached SELL plans
+int64_t max_row_degree(const sc_graph* g, int64_t r0, int64_t r1, cudaStream_t s);
 bool dyn_tiles_on();                       // env SC_DYN_TILES (default 1)
 unsigned* next_tile_ctr(const sc_graph* g, cudaStream_t s);   // a self-resetting tile counter slot
 // one fused step of the row-partitioned paths: the SELL kernel when it can run this chunk width

@@ -825,6 +825,8 @@ __global__ void max_degree_kernel(const int64_t* __restrict__ row_ptr, int64_t r
   if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
+}  // namespace
+
 int64_t max_row_degree(const sc_graph* g, int64_t r0, int64_t r1, cudaStream_t s) {
   DevBuf b;
   if (r1 <= r0 || b.ensure(sizeof(unsigned long long)) != SC_OK) return 0;
@@ -835,6 +837,8 @@ int64_t max_row_degree(const sc_graph* g, int64_t r0, int64_t r1, cudaStream_t s
   cudaStreamSynchronize(s);
   return (int64_t)h;
 }
+
+namespace {
 
 // split-row threshold: a row of degree > this is cut into chunks (env SC_SELL_HUB_DEG)
 int64_t hub_threshold() {

@@ -359,6 +359,39 @@ def test_full_size_c4_oracle_columns(sc):
     assert rel(Yg, Yo) <= F32_TOL
 
 
+def test_chunk_width_structural_choice(sc, monkeypatch):
+    """filter_apply's chunk width on graphs of ~0.5-1M nodes (32-column chunks by the L2-budget
+    rule): a power-law graph (max degree > 8x the mean) gets 64-column chunks -- the default run
+    is bit-identical to SC_CHUNK=64 and SC_CHUNK_WIDE=0 to SC_CHUNK=32; the two widths agree to
+    fp32 rounding (hub rows' chunk sums group edges by the width's lane groups, R15) and match
+    the oracle on sampled columns."""
+    g = scinputs.chung_lu(700_000, 20, 2.1, seed=11)
+    G = sc.Graph.from_csr(g)
+    R, order = 64, 30
+    lmax = 2.0 * G.info()[3]
+    d = chebyshev.filter_coeffs(0.05 * lmax, lmax, order, False)
+    X = torch.from_numpy(scinputs.gaussian_block(8, g.n, R)).cuda()
+    outs = {}
+    for tag, env in (("32", {"SC_CHUNK": "32"}), ("64", {"SC_CHUNK": "64"}), ("auto", {}),
+                     ("narrow", {"SC_CHUNK_WIDE": "0"})):
+        for k in ("SC_CHUNK", "SC_CHUNK_WIDE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        Y = torch.empty_like(X)
+        sc.sc_filter_apply_f32(G.handle, d, order, lmax, R, X, Y)
+        torch.cuda.synchronize()
+        outs[tag] = Y.cpu().numpy()
+    assert np.array_equal(outs["auto"], outs["64"])
+    assert np.array_equal(outs["narrow"], outs["32"])
+    assert rel(outs["32"], outs["64"]) <= 1e-6
+    L = laplacian.laplacian(g)
+    cols = [0, 37, 63]
+    Yo = chebyshev.cheb_filter(L, X.cpu().numpy()[:, cols].astype(np.float64), d, lmax)
+    for t in ("32", "64"):
+        assert rel(outs[t][:, cols], Yo) <= F32_TOL
+
+
 # ---------------------------------------------------------------------------
 # eigencount moments and lambda_k dichotomy
 # ---------------------------------------------------------------------------

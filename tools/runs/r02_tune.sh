@@ -1,0 +1,10 @@
+#!/bin/bash
+o=gpurun_out/r02_tune.txt; : > $o
+timeout 900 python -m pytest tests -m gpu -x -q -k "chunk_width or filter_f32 or filter_random or full_size_c3 or chunking" 2>&1 | tail -3 >> $o
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv,noheader >> $o
+for wl in c3_sbm1m x_chunglu1m x_gmm2d1m_rcm c3_sbm1m x_chunglu1m; do
+  timeout 600 python tools/sweep_filter.py --workload $wl --chunks 0 --reps 3 --tag tuned_$wl >> $o 2>&1
+done
+SC_CHUNK_TUNE=0 timeout 600 python tools/sweep_filter.py --workload x_gmm2d1m_rcm --chunks 0 --reps 3 --tag untuned_rcm >> $o 2>&1
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv,noheader >> $o
+cut -c1-200 $o
