@@ -1225,7 +1225,13 @@ int launch_step_any(const sc_graph* g, StepParams p, cudaStream_t s) {
   if (sell_enabled() && !p2p_wide) SC_TRY(sell_usable<T>(g, p.width, p.row_begin, p.row_end, s, &ok));
   if (!ok) return launch_step<T>(g, p, s);
   p.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
-  return launch_sell_step<T>(g, p, s, nullptr);
+  // the bench's per-launch events (sc_profile_begin), as launch_step records them
+  cudaEvent_t e0 = nullptr;
+  prof_launch_begin(s, &e0);
+  double ab = 0.0;
+  SC_TRY(launch_sell_step<T>(g, p, s, e0 ? &ab : nullptr));
+  prof_launch_end(s, e0, ab, 1);
+  return SC_OK;
 }
 template int launch_step_any<float>(const sc_graph*, StepParams, cudaStream_t);
 template int launch_step_any<double>(const sc_graph*, StepParams, cudaStream_t);

@@ -1241,3 +1241,31 @@ def test_filter_random_cases(sc, i, path, monkeypatch):
     Y = gpu_filter(sc, g, X, ratio * lmax, lmax, order, jackson)
     Yo = chebyshev.lowpass_filter(L, X.astype(np.float64), ratio * lmax, lmax, order, jackson)
     assert rel(Y, Yo) <= F32_TOL, (g.n, g.nnz, R, order)
+
+
+# ---------------------------------------------------------------------------
+# bench.py contract on the GPU (small workload): the single-GPU line and the partitioned path
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("extra", [[], ["--dist-path"], ["--dist-path", "--exchange", "nccl"]])
+def test_bench_json_line_gpu(sc, extra):
+    """`bench.py` prints one JSON line with the driver's keys, a positive roofline from the
+    per-launch events (also on the partitioned paths, whose SELL steps record them) and a
+    positive kernel count -- on configs[2] (100k nodes: streaming kernels, L2 flushed)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--workload", "c2_sbm100k", "--steps", "3",
+                        "--warmup", "3", "--no-cluster", "--no-stability", "--no-cpu-baseline", *extra],
+                       capture_output=True, text=True, timeout=900, cwd=root,
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1", SC_RESIDENT="0"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "roofline", "clocks", "e2e",
+                "gpu_launches", "config"):
+        assert key in d, key
+    assert d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["roofline"]["achieved"] > 0 and 0 < d["roofline"]["frac"] < 1.5
