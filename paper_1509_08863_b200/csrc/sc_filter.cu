@@ -938,6 +938,7 @@ int wide_chunks(sc_graph* g, cudaStream_t s, bool* wide) {
     *wide = forced != 0;
     return SC_OK;
   }
+  std::lock_guard<std::mutex> lock(g->chunk_tuned_mu);   // concurrent filter calls on one graph
   auto it = g->chunk_tuned.find(std::make_pair(0, 0));
   if (it != g->chunk_tuned.end()) {
     *wide = it->second != 0;

@@ -171,6 +171,7 @@ struct sc_graph {
   sc::DevBuf resident_coef;
   // filter_apply's structural chunk-width choice (key (0, 0): 1 = 64-column chunks)
   std::map<std::pair<int, int>, int> chunk_tuned;
+  std::mutex chunk_tuned_mu;
   // dynamic tile scheduling of the step kernel: one tile counter per launch from a ring of
   // kTileCtrRing slots, zeroed once; the last tile request of a launch resets its slot
   mutable sc::DevBuf tile_ctr_ring;
