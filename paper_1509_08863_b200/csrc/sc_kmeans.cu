@@ -248,11 +248,11 @@ __device__ __forceinline__ void block_inclusive_scan(double v, double* s_w, doub
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kSel) seed_select_kernel(const double* __restrict__ bsum, int G,
-                                                           const double* __restrict__ v, int64_t n, int64_t chunk,
-                                                           double u, const float* __restrict__ F, int d,
-                                                           double* __restrict__ c_out, int tseed,
-                                                           double* __restrict__ half_gap) {
+__device__ __forceinline__ void seed_select_dev(const double* __restrict__ bsum, int G,
+                                                const double* __restrict__ v, int64_t n, int64_t chunk,
+                                                double u, const float* __restrict__ F, int d,
+                                                double* __restrict__ c_out, int tseed,
+                                                double* __restrict__ half_gap) {
   __shared__ double s_w[64];
   __shared__ double s_inc[kSel];
   __shared__ int s_first;
@@ -322,6 +322,126 @@ __global__ void __launch_bounds__(kSel) seed_select_kernel(const double* __restr
       half_gap[j] = 0.5 * sqrt(s2) * (1.0 - 1e-9);
     }
   }
+}
+
+__global__ void __launch_bounds__(kSel) seed_select_kernel(const double* __restrict__ bsum, int G,
+                                                           const double* __restrict__ v, int64_t n, int64_t chunk,
+                                                           double u, const float* __restrict__ F, int d,
+                                                           double* __restrict__ c_out, int tseed,
+                                                           double* __restrict__ half_gap) {
+  seed_select_dev(bsum, G, v, n, chunk, u, F, d, c_out, tseed, half_gap);
+}
+
+// ---- k-means++ of several restarts at once (kmeans_run with parallel restarts): the draws of
+// all restarts advance together, one launch per step for all of them, and a feature row is read
+// once per draw index for every restart that needs it (the per-restart path reads it once per
+// restart).  Each restart's arithmetic is exactly the per-restart path's -- the same row_dist,
+// range sums, selection and skip test -- so the seeds are identical (restart r's arrays at
+// offset r of the batch).
+__global__ void __launch_bounds__(kSel) seed_select_batch_kernel(const double* __restrict__ bsum_all, int G,
+                                                                 const double* __restrict__ v_all, int64_t n,
+                                                                 int64_t chunk, const double* __restrict__ u_all,
+                                                                 int ustride, const float* __restrict__ F, int d,
+                                                                 double* __restrict__ C_all, int64_t cstride, int tseed,
+                                                                 double* __restrict__ gap_all, int gstride) {
+  const int r = blockIdx.x;
+  seed_select_dev(bsum_all + (size_t)r * G, G, v_all + (size_t)r * n, n, chunk, u_all[(size_t)r * ustride + tseed], F,
+                  d, C_all + (size_t)r * cstride + (size_t)tseed * d, tseed, gap_all + (size_t)r * gstride);
+}
+
+// d2 of every restart to its first seed (d2_update_kernel with first = 1, per restart)
+__global__ void __launch_bounds__(kSP) d2_first_batch_kernel(const float* __restrict__ F, int64_t n, int d,
+                                                             const double* __restrict__ C_all, int64_t cstride, int nr,
+                                                             double* __restrict__ d2_all, int32_t* __restrict__ near_all) {
+  extern __shared__ unsigned char smb[];
+  double* sc_ = reinterpret_cast<double*>(smb);        // [nr][d]
+  float* sx = reinterpret_cast<float*>(sc_ + (size_t)nr * d);
+  for (int j = threadIdx.x; j < nr * d; j += blockDim.x) sc_[j] = C_all[(size_t)(j / d) * cstride + j % d];
+  const int64_t p0 = (int64_t)blockIdx.x * kSP;
+  const bool v4 = rows_v4(F, d);
+  stage_rows(F, n, d, p0, sx, v4);
+  __syncthreads();
+  const int64_t i = p0 + threadIdx.x;
+  if (i < n) {
+    const float* x = sx + threadIdx.x * rows_ld(v4, d);
+    for (int r = 0; r < nr; ++r) {
+      d2_all[(size_t)r * n + i] = row_dist(x, sc_ + (size_t)r * d, d, v4);
+      near_all[(size_t)r * n + i] = 0;
+    }
+  }
+}
+
+// seed t of every restart: d2_update_skip_kernel's test per (point, restart); a row is staged
+// once if any restart needs it, then each needing restart's exact distance (R8) is taken
+__global__ void __launch_bounds__(kSP) d2_skip_batch_kernel(const float* __restrict__ F, int64_t n, int d,
+                                                            const double* __restrict__ C_all, int64_t cstride, int t,
+                                                            int nr, const double* __restrict__ gap_all, int gstride,
+                                                            double* __restrict__ d2_all,
+                                                            int32_t* __restrict__ near_all) {
+  extern __shared__ unsigned char smk2[];
+  double* sct = reinterpret_cast<double*>(smk2);   // [nr][d]: seed t of every restart
+  float* sx = reinterpret_cast<float*>(sct + (size_t)nr * d);
+  __shared__ int s_cnt;
+  __shared__ int s_rows[kSP];
+  __shared__ unsigned s_mask[kSP];
+  for (int j = threadIdx.x; j < nr * d; j += blockDim.x)
+    sct[j] = C_all[(size_t)(j / d) * cstride + (size_t)t * d + j % d];
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int64_t p0 = (int64_t)blockIdx.x * kSP;
+  const int64_t i = p0 + threadIdx.x;
+  unsigned mask = 0;
+  if (i < n) {
+    for (int r = 0; r < nr; ++r) {
+      const double cur = d2_all[(size_t)r * n + i];
+      if (!(sqrt(cur) * (1.0 + 1e-9) <= gap_all[(size_t)r * gstride + near_all[(size_t)r * n + i]])) mask |= 1u << r;
+    }
+    if (mask) {
+      const int slot = atomicAdd(&s_cnt, 1);
+      s_rows[slot] = threadIdx.x;
+      s_mask[slot] = mask;
+    }
+  }
+  __syncthreads();
+  const int cnt = s_cnt;
+  if (cnt == 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool v4 = rows_v4(F, d);
+  const int ld = rows_ld(v4, d);
+  for (int q = warp; q < cnt; q += nw) stage_row(F + (p0 + s_rows[q]) * d, sx + q * ld, d, v4, lane);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if ((int)threadIdx.x < cnt) {
+    const int64_t gi = p0 + s_rows[threadIdx.x];
+    unsigned m = s_mask[threadIdx.x];
+    const float* x = sx + threadIdx.x * ld;
+    while (m) {
+      const int r = __ffs(m) - 1;
+      m &= m - 1;
+      const double acc = row_dist(x, sct + (size_t)r * d, d, v4);
+      if (acc < d2_all[(size_t)r * n + gi]) {
+        d2_all[(size_t)r * n + gi] = acc;
+        near_all[(size_t)r * n + gi] = t;
+      }
+    }
+  }
+}
+
+// per-block sums of every restart's d2 (range_sums_kernel per restart: blockIdx.y)
+__global__ void range_sums_batch_kernel(const double* __restrict__ v_all, int64_t n, int64_t chunk, int G,
+                                        double* __restrict__ out_all) {
+  __shared__ double sh[kB];
+  const double* v = v_all + (size_t)blockIdx.y * n;
+  const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+  double s = 0.0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) s += v[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kB / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out_all[(size_t)blockIdx.y * G + blockIdx.x] = sh[0];
 }
 
 // ---- distributed k-means++ (kmeans_run_dist): the points are the ranks' rows in rank-major
@@ -1537,7 +1657,10 @@ struct PinnedSlot {
 // ties -> lowest r) goes to *res and its labels to labels_dev.
 static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rstep, int restarts, int max_iter,
                          uint64_t seed, const double* uniforms_host, int32_t* labels_dev, KmResult* res,
-                         cudaStream_t s, Coll* coll = nullptr, int64_t row_off = 0, int64_t n_global = -1) {
+                         cudaStream_t s, Coll* coll = nullptr, int64_t row_off = 0, int64_t n_global = -1,
+                         const double* init_C = nullptr) {
+  // init_C (device, restarts x k x d): the k-means++ seeds of every restart, already drawn by
+  // seed_batch (kmeans_run); the worker then only runs Lloyd
   // coll != nullptr: distributed over the ranks of a row partition (kmeans_run_dist) -- the
   // same kernels on the local rows; the fixed-point scale, the changed-label counts, the exact
   // member sums and counts, the inertia and the k-means++ draws are reduced over the ranks
@@ -1874,16 +1997,20 @@ static int kmeans_worker(const float* F, int64_t n, int d, int k, int r0, int rs
       u[t] = uniforms_host ? uniforms_host[(size_t)r * k + t] : uniform_host(seed, 1, (uint64_t)r * k + t);
     // ---- k-means++ seeding (device-resident: block sums, then one selection kernel per draw)
     int64_t idx = std::min<int64_t>((int64_t)std::floor(u[0] * n_global), n_global - 1);
-    if (!coll) {
+    if (init_C) {
+      SC_CUDA_TRY(cudaMemcpyAsync(C, init_C + (size_t)r * k * d, sizeof(double) * k * d, cudaMemcpyDeviceToDevice, s));
+    } else if (!coll) {
       row_to_centroid_kernel<<<1, 128, 0, s>>>(F, idx, d, C);
     } else {
       row_or_zero_kernel<<<1, 128, 0, s>>>(F, (idx >= row_off && idx < row_off + n) ? idx - row_off : -1, d, C);
       SC_TRY(coll->sum_f64(C, (size_t)d, s));
     }
+    if (!init_C) {
     d2_update_kernel<<<(unsigned)((n + kSP - 1) / kSP), kSP, smem_d2, s>>>(F, n, d, C, b_d2.as<double>(), 1,
                                                                           b_near.as<int32_t>());
     SC_CUDA_TRY(cudaGetLastError());
-    for (int t = 1; t < k; ++t) {
+    }
+    for (int t = 1; t < k && !init_C; ++t) {
       range_sums_kernel<<<G, kB, 0, s>>>(b_d2.as<double>(), n, chunk, b_part.as<double>());
       if (!coll) {
         seed_select_kernel<<<1, kSel, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk, u[t], F, d,
@@ -1993,6 +2120,55 @@ int kmeans_run_dist(const float* F, int64_t n_local, int64_t row_off, int64_t n_
   return SC_OK;
 }
 
+// k-means++ seeds of restarts [0, restarts) drawn together (the kernels above), into C_all
+// (device, restarts x k x d).  Same uniforms, chunking and arithmetic as kmeans_worker's
+// per-restart seeding, so the seeds are identical; batches of up to kSeedBatch restarts.
+constexpr int kSeedBatch = 16;
+static int seed_batch(const float* F, int64_t n, int d, int k, int restarts, uint64_t seed,
+                      const double* uniforms_host, double* C_all, cudaStream_t s) {
+  const int sms = num_sms_current();
+  const int G = std::min(sms * 2, 1024);                  // as kmeans_worker
+  const int64_t chunk = (n + G - 1) / G;
+  const int64_t cstride = (int64_t)k * d;
+  const int nb = std::min(restarts, kSeedBatch);
+  PoolBuf b_d2, b_near, b_gap, b_part, b_u;
+  SC_TRY(b_d2.ensure(sizeof(double) * (size_t)nb * n, s));
+  SC_TRY(b_near.ensure(sizeof(int32_t) * (size_t)nb * n, s));
+  SC_TRY(b_gap.ensure(sizeof(double) * (size_t)nb * (k + 1), s));
+  SC_TRY(b_part.ensure(sizeof(double) * (size_t)nb * G, s));
+  SC_TRY(b_u.ensure(sizeof(double) * (size_t)nb * k, s));
+  const size_t smem = sizeof(double) * (size_t)nb * d + sizeof(float) * kSP * (size_t)(d + 4);
+  SC_TRY(smem_attr_at_least(reinterpret_cast<const void*>(d2_first_batch_kernel), (int)smem));
+  SC_TRY(smem_attr_at_least(reinterpret_cast<const void*>(d2_skip_batch_kernel), (int)smem));
+  std::vector<double> u((size_t)nb * k);
+  for (int r0 = 0; r0 < restarts; r0 += nb) {
+    const int nr = std::min(nb, restarts - r0);
+    for (int r = 0; r < nr; ++r)
+      for (int t = 0; t < k; ++t)
+        u[(size_t)r * k + t] = uniforms_host ? uniforms_host[(size_t)(r0 + r) * k + t]
+                                             : uniform_host(seed, 1, (uint64_t)(r0 + r) * k + t);
+    SC_CUDA_TRY(cudaMemcpyAsync(b_u.ptr, u.data(), sizeof(double) * (size_t)nr * k, cudaMemcpyHostToDevice, s));
+    double* Cb = C_all + (size_t)r0 * cstride;
+    for (int r = 0; r < nr; ++r) {
+      const int64_t idx = std::min<int64_t>((int64_t)std::floor(u[(size_t)r * k] * n), n - 1);
+      row_to_centroid_kernel<<<1, 128, 0, s>>>(F, idx, d, Cb + (size_t)r * cstride);
+    }
+    const unsigned pb = (unsigned)((n + kSP - 1) / kSP);
+    d2_first_batch_kernel<<<pb, kSP, smem, s>>>(F, n, d, Cb, cstride, nr, b_d2.as<double>(), b_near.as<int32_t>());
+    SC_CUDA_TRY(cudaGetLastError());
+    for (int t = 1; t < k; ++t) {
+      range_sums_batch_kernel<<<dim3(G, nr), kB, 0, s>>>(b_d2.as<double>(), n, chunk, G, b_part.as<double>());
+      seed_select_batch_kernel<<<nr, kSel, 0, s>>>(b_part.as<double>(), G, b_d2.as<double>(), n, chunk,
+                                                   b_u.as<double>(), k, F, d, Cb, cstride, t, b_gap.as<double>(),
+                                                   k + 1);
+      d2_skip_batch_kernel<<<pb, kSP, smem, s>>>(F, n, d, Cb, cstride, t, nr, b_gap.as<double>(), k + 1,
+                                                 b_d2.as<double>(), b_near.as<int32_t>());
+      SC_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  return SC_OK;
+}
+
 int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_iter, uint64_t seed,
                const double* uniforms_host, int32_t* labels_dev, double* centroids_host, double* inertia_out,
                int* iters_out, int* best_out, cudaStream_t s, int max_workers) {
@@ -2012,6 +2188,15 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
   } else {
     int dev = 0;
     cudaGetDevice(&dev);
+    // every restart's k-means++ seeds in one batched pass (env SC_KMEANS_SEED_BATCH=0: each
+    // worker seeds its own restarts)
+    PoolBuf b_init;
+    const bool batch_seed = !(std::getenv("SC_KMEANS_SEED_BATCH") && std::atoi(std::getenv("SC_KMEANS_SEED_BATCH")) == 0);
+    if (batch_seed) {
+      SC_TRY(b_init.ensure(sizeof(double) * (size_t)restarts * k * d, s));
+      SC_TRY(seed_batch(F, n, d, k, restarts, seed, uniforms_host, b_init.as<double>(), s));
+    }
+    const double* init_C = batch_seed ? b_init.as<double>() : nullptr;
     cudaEvent_t ready;
     SC_CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     SC_CUDA_TRY(cudaEventRecord(ready, s));
@@ -2032,7 +2217,7 @@ int kmeans_run(const float* F, int64_t n, int d, int k, int restarts, int max_it
         int rc = labs[w].ensure(sizeof(int32_t) * n, streams[w]);
         if (rc == SC_OK)
           rc = kmeans_worker(F, n, d, k, w, P, restarts, max_iter, seed, uniforms_host, labs[w].as<int32_t>(),
-                             &res[w], streams[w]);
+                             &res[w], streams[w], nullptr, 0, -1, init_C);
         if (rc != SC_OK) {
           rcs[w] = rc;
           msgs[w] = sc_last_error();

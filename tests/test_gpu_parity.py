@@ -510,6 +510,28 @@ def test_kmeans_bit_exact(sc, n, k, d, spread, restarts, max_iter):
     assert inertia == pytest.approx(io, rel=1e-12)
 
 
+@pytest.mark.parametrize("n,k,d,spread,restarts", [
+    (90000, 32, 48, 0.8, 6),       # 16-byte staged rows
+    (150000, 20, 29, -1.0, 4),     # d % 4 != 0 (4-byte staging), integer grid: ties, duplicate points
+    (100000, 40, 64, 0.5, 17)])    # more restarts than one seeding batch (16)
+def test_kmeans_batched_seeding_identical(sc, n, k, d, spread, restarts, monkeypatch):
+    """Parallel restarts draw their k-means++ seeds in one batched pass (seed_batch: one launch
+    per draw index for all restarts, rows read once): the result -- labels, centroids, inertia,
+    iterations, best restart -- is bit-identical to every worker seeding its own restarts."""
+    X = _features(n + 3 * k + d, n, k, d, spread)
+    u = np.stack([scinputs.uniforms(11, k, offset=k * r) for r in range(restarts)])
+    out = {}
+    for batch in ("1", "0"):
+        monkeypatch.setenv("SC_KMEANS_SEED_BATCH", batch)
+        lab = torch.empty(n, dtype=torch.int32, device="cuda")
+        C = np.zeros((k, d), dtype=np.float64)
+        inertia, it, best = sc.sc_kmeans(torch.from_numpy(X).cuda(), n, d, k, restarts, 3, 0, u, lab, C)
+        out[batch] = (lab.cpu().numpy(), C, inertia, it, best)
+    a, b = out["1"], out["0"]
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert a[2] == b[2] and a[3] == b[3] and a[4] == b[4]
+
+
 @pytest.mark.parametrize("n,k,d,spread", [
     (100, 2, 4, 0.5),        # one partial tile, N = 16 (k padded), K = 8 (d padded)
     (257, 17, 12, 0.4),      # tiles of 1-128 points, clusters of a few points
