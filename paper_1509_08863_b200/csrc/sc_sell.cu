@@ -476,6 +476,12 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
         tn[w] = a * lt + bc * own[w] + bp * prv[w];      // T_{s+1}[i]
       }
       if (tnext) Vec<T>::st(tnext + (int64_t)row * p.ld_next + c, tn);   // gathered next step: normal L2 policy
+      if (p.y_mode) {
+        const T cyp = static_cast<T>(p.cy_prev), cyc = static_cast<T>(p.cy_cur), cyn = static_cast<T>(p.cy_next);
+#pragma unroll
+        for (int w = 0; w < W; ++w) yv[w] += cyp * prv[w] + cyc * own[w] + cyn * tn[w];
+        Stream<T>::st(y + (int64_t)row * p.ld_y + c, yv, policy_evict_first());
+      }
       if (P2P && tnext && row >= p.p2p->row0) {
         // fused halo exchange (multi-GPU): the peers that read this row get it straight into
         // their halo rows of the same buffer (NVLink stores from the epilogue)
@@ -486,12 +492,6 @@ cheb_sell_kernel(SellDev sd, const T* __restrict__ strength, StepParams p, int c
           T* dst = static_cast<T*>(x->peer_buf[p.p2p_next][q]) + (x->peer_nl[q] + x->sd_slot[e]) * p.ld_next + c;
           Vec<T>::st(dst, tn);
         }
-      }
-      if (p.y_mode) {
-        const T cyp = static_cast<T>(p.cy_prev), cyc = static_cast<T>(p.cy_cur), cyn = static_cast<T>(p.cy_next);
-#pragma unroll
-        for (int w = 0; w < W; ++w) yv[w] += cyp * prv[w] + cyc * own[w] + cyn * tn[w];
-        Stream<T>::st(y + (int64_t)row * p.ld_y + c, yv, policy_evict_first());
       }
       if (MOM) {
 #pragma unroll
@@ -1221,7 +1221,7 @@ int launch_step_any(const sc_graph* g, StepParams p, cudaStream_t s) {
   // equal or faster than the CSR kernel (c3, 8 ranks 21.9 vs 21.7 ms, 4 ranks 33.9 vs 35.2),
   // 48-column chunks 12-13 % slower (c4, 4 and 8 ranks) -- wider exchange chunks stay on CSR
   bool ok = false;
-  const bool p2p_wide = p.p2p && (sizeof(T) != 4 || p.width > 32);
+  const bool p2p_wide = p.p2p && (sizeof(T) != 4 || (p.width > 32 && !env_int_s("SC_P2P_SELL_WIDE", 0)));
   if (sell_enabled() && !p2p_wide) SC_TRY(sell_usable<T>(g, p.width, p.row_begin, p.row_end, s, &ok));
   if (!ok) return launch_step<T>(g, p, s);
   p.tile_ctr = dyn_tiles_on() ? next_tile_ctr(g, s) : nullptr;
