@@ -95,6 +95,7 @@ struct TcArgs {
   const int64_t* goff;   // [k + 1] cluster offsets in gperm
   const int32_t* gperm;  // points grouped by current label
   int k, d, Dp, NT, tmem_cols;
+  int tmem_tile;         // TMEM columns per 128-point tile (the second tile's accumulator offset)
   int v4;                // rows and centroids 16-byte aligned (d % 4 == 0): vector staging
   const float* panels;   // [k][panel_floats]: per current cluster a, see tc_panel_kernel
   const double* pscal;   // [k][16]: see tc_panel_kernel
@@ -110,14 +111,18 @@ struct TcArgs {
   int* amb_len;
 };
 
-constexpr int kPV = 16;   // prefetched 16-byte chunks per point (d <= 64)
+// prefetched 16-byte chunks per point: 16 (d <= 64, 3 CTAs per SM) or 32 (d <= 128, the
+// one-CTA-per-SM instantiation large k x d needs: registers are not the limit there)
+constexpr int kPV = 16;
+constexpr int kPVWide = 32;
 constexpr double kKappa = 0x1p-20;   // fp32 evaluation budget of the per-column bound (above)
 constexpr float kKappaF = 0x1p-20f;
 constexpr int kChunk = 4; // items a CTA takes per counter increment
 
 // shared-memory bytes of assign_tc_kernel
-__host__ __device__ inline size_t tc_smem_bytes(int NT, int Dp) {
-  return (size_t)(kTM + NT) * Dp * 4 + (size_t)(3 * NT + Dp) * 4 + (size_t)(kTM + Dp) * 8;
+// (TP points per CTA: one or two 128-point MMA tiles sharing the cluster's panel)
+__host__ __device__ inline size_t tc_smem_bytes(int NT, int Dp, int TP = kTM) {
+  return (size_t)(TP + NT) * Dp * 4 + (size_t)(3 * NT + Dp) * 4 + (size_t)(TP + Dp) * 8;
 }
 
 // Per-cluster panels, once per assignment (grid k x NT/32, a warp per 4 centroids): for the
@@ -228,16 +233,21 @@ __device__ __forceinline__ void tc_columns(uint32_t taddr, int c0, const float4*
   }
 }
 
-__global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
+// TP = 128: one MMA tile per CTA.  TP = 256 (large k x d, where shared memory allows one CTA per
+// SM): two 128-point tiles of the same cluster per CTA, both multiplied by the one staged panel
+// into two TMEM accumulators (columns [0, tmem_tile) and [tmem_tile, 2 tmem_tile)); warps w and
+// w + 4 read the same TMEM lanes (w % 4) of their own accumulator -- 8 warps per SM instead of 4.
+template <int PV, int MINB, int TP>
+__global__ void __launch_bounds__(TP, MINB) assign_tc_kernel(TcArgs a) {
   const int KC = a.Dp / 4;
   extern __shared__ __align__(1024) unsigned char tsm[];
   float* sA = reinterpret_cast<float*>(tsm);                    // [128][Dp] canonical
-  float* sB = sA + (size_t)kTM * a.Dp;                          // [NT][Dp] canonical, then:
+  float* sB = sA + (size_t)TP * a.Dp;                           // [NT][Dp] canonical, then:
   const float2* sWZ = reinterpret_cast<const float2*>(sB + (size_t)a.NT * a.Dp);   // [NT] {W_j, zn_j}
   const float* sZ2f = sB + (size_t)a.NT * a.Dp + 2 * a.NT;      // [NT] fl32(||z_j||^2)
   float* s_caf = sB + (size_t)a.NT * a.Dp + 3 * a.NT;           // [Dp] fl32(c_a)
   double* sY2 = reinterpret_cast<double*>(s_caf + a.Dp);        // [128]
-  double* s_ca = sY2 + kTM;                                     // [Dp]: c_a (fp64)
+  double* s_ca = sY2 + TP;                                      // [Dp]: c_a (fp64)
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tmem_base;
   __shared__ double s_ca_norm, s_zmax;
@@ -259,7 +269,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   const int items = *a.n_items;
-  for (int c = tid; c <= a.k; c += kTM) {
+  for (int c = tid; c <= a.k; c += TP) {
     s_ioff[c] = a.ioff[c];
     s_goff[c] = a.goff[c];
   }
@@ -272,7 +282,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
       if (s_ioff[mid] <= i) lo = mid; else hi = mid - 1;
     }
     ca = lo;
-    start = (i - s_ioff[lo]) * kTM;
+    start = (i - s_ioff[lo]) * TP;
   };
   const double u = 0x1p-24;
   const double eps_s = 0x1p-10 + 0x1p-22 + (a.Dp + 2) * 0x1p-23 * (1.0 + 0x1p-10);
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   const int nval = a.d / 4;
   // d <= 64 with 16-byte rows: the next tile's rows are loaded into registers while the
   // tensor cores and the epilogue work on the current one
-  const bool pref = a.v4 && nval <= kPV;
+  const bool pref = a.v4 && nval <= PV;
   int cur = -1;   // cluster whose panel sits in sB
   uint32_t phase = 0;
   // dynamic schedule: chunks of kChunk consecutive tiles (consecutive tiles mostly share a
@@ -296,8 +306,8 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   // the next non-empty cluster
   auto walk = [&](int c, int st, int& c_n, int& st_n) {
     c_n = c;
-    st_n = st + kTM;
-    if (st_n >= (s_ioff[c + 1] - s_ioff[c]) * kTM) {
+    st_n = st + TP;
+    if (st_n >= (s_ioff[c + 1] - s_ioff[c]) * TP) {
       c_n = c + 1;
       while (s_ioff[c_n + 1] == s_ioff[c_n]) ++c_n;
       st_n = 0;
@@ -319,14 +329,14 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   }
   auto load_idx = [&](int c, int st) -> int64_t {
     const int64_t g0 = s_goff[c] + st;
-    const int cnt = (int)min((int64_t)kTM, (int64_t)(s_goff[c + 1] - g0));
+    const int cnt = (int)min((int64_t)TP, (int64_t)(s_goff[c + 1] - g0));
     return tid < cnt ? (int64_t)a.gperm[g0 + tid] : (int64_t)-1;
   };
-  float4 xv[kPV];
+  float4 xv[PV];
   auto load_rows = [&](int64_t gi) {
     const float4* xr = reinterpret_cast<const float4*>(a.F + (gi >= 0 ? gi : 0) * a.d);
 #pragma unroll
-    for (int t = 0; t < kPV; ++t)
+    for (int t = 0; t < PV; ++t)
       xv[t] = (gi >= 0 && t < nval) ? __ldg(xr + t) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
   int64_t gi_cur = -1, gi1 = -1;
@@ -345,16 +355,16 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
   while (it < items) {
     mark(6);
     const int64_t g0 = s_goff[ca] + start;
-    const int cnt = (int)min((int64_t)kTM, (int64_t)(s_goff[ca + 1] - g0));
+    const int cnt = (int)min((int64_t)TP, (int64_t)(s_goff[ca + 1] - g0));
     const int32_t* pts = a.gperm + g0;
     // ---- the cluster's panel (tc_panel_kernel), c_a in fp64 and fp32
     if (ca != cur) {
       const float* P = a.panels + (size_t)ca * a.panel_floats;
-      for (int e = tid; e < a.panel_floats / 4; e += kTM)
+      for (int e = tid; e < a.panel_floats / 4; e += TP)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sB + 4 * e)), "l"(P + 4 * e)
                      : "memory");
       asm volatile("cp.async.commit_group;" ::: "memory");
-      for (int q = tid; q < a.Dp; q += kTM) {
+      for (int q = tid; q < a.Dp; q += TP) {
         s_ca[q] = q < a.d ? a.C[(size_t)ca * a.d + q] : 0.0;
         s_caf[q] = q < a.d ? a.Cf[(size_t)ca * a.d + q] : 0.f;
       }
@@ -382,7 +392,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
       const int r = tid;
       float s2 = 0.f;   // ||y||^2 in fp32, sequential: within (K + 2) 2^-24 relative (epilogue)
 #pragma unroll
-      for (int t = 0; t < kPV; ++t) {
+      for (int t = 0; t < PV; ++t) {
         if (t >= KC) break;
         float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
         if (t < nval) {
@@ -430,7 +440,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
       }
       sY2[r] = s2;
     } else {
-      for (int r = warp; r < kTM; r += 4) {
+      for (int r = warp; r < TP; r += TP / 32) {
         double s2 = 0.0;
         const int64_t gi = r < cnt ? pts[r] : -1;
         for (int q = lane; q < a.Dp; q += 32) {
@@ -462,14 +472,18 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
     }
     if (tid == 0) {
       const uint32_t id = idesc_tf32(kTM, a.NT);
-      for (int ks = 0; ks < a.Dp / 8; ++ks) {   // one MMA per 8 tf32 of K (two 16-byte chunks)
-        const uint64_t da = umma_desc(smem_u32(sA) + ks * 256, 128, KC * 128);
-        const uint64_t db = umma_desc(smem_u32(sB) + ks * 256, 128, KC * 128);
-        const uint32_t acc = ks > 0;
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-            "l"(da), "l"(db), "r"(id), "r"(acc));
+#pragma unroll
+      for (int h = 0; h < TP / kTM; ++h) {   // the CTA's 128-point tiles, one accumulator each
+        const uint32_t sa = smem_u32(sA) + (uint32_t)(h * kTM * a.Dp * 4);
+        for (int ks = 0; ks < a.Dp / 8; ++ks) {   // one MMA per 8 tf32 of K (two 16-byte chunks)
+          const uint64_t da = umma_desc(sa + ks * 256, 128, KC * 128);
+          const uint64_t db = umma_desc(smem_u32(sB) + ks * 256, 128, KC * 128);
+          const uint32_t acc = ks > 0;
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(h * a.tmem_tile)),
+              "l"(da), "l"(db), "r"(id), "r"(acc));
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_u32(&bar))
@@ -488,7 +502,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     mark(3);
-    // ---- epilogue: thread tid owns point tid (TMEM lane tid); per column the fp32 lower
+    // ---- epilogue: thread tid owns point tid (TMEM lane tid % 128 of tile tid / 128); per column the fp32 lower
     // bound L_j of rho_j^2 (bound above), tracking the smallest (index b, its S) and the
     // second smallest
     // ||y||^2 as computed (fp32 sequential on the prefetch path, fp64 otherwise) and its
@@ -506,7 +520,7 @@ __global__ void __launch_bounds__(kTM, 3) assign_tc_kernel(TcArgs a) {
     // rounded up to 16 (padding columns: L = +inf): 32-column loads, a 16-column tail
     ColTrack tr;
     const float4* sWZ2 = reinterpret_cast<const float4*>(sWZ);   // column pairs
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((tid / kTM) * a.tmem_tile);
     int c0 = 0;
     for (; c0 + 32 <= a.NT; c0 += 32) tc_columns<32>(trow + (uint32_t)c0, c0, sWZ2, Eaf, V, tr);
     if (c0 < a.NT) tc_columns<16>(trow + (uint32_t)c0, c0, sWZ2, Eaf, V, tr);
@@ -615,17 +629,18 @@ __global__ void __launch_bounds__(256) group_hist_kernel(const int32_t* __restri
     if (sh_cnt[c]) atomicAdd(&cnt[c], sh_cnt[c]);
 }
 
-// offsets (exclusive scan of the counts) and the tiles' prefix ioff (tiles of <= 128 points
+// offsets (exclusive scan of the counts) and the tiles' prefix ioff (tiles of <= tp points
 // of one cluster), cursors and counters zeroed; one block, k <= 256
 __global__ void __launch_bounds__(256) group_plan_kernel(const unsigned* __restrict__ cnt, int k,
                                                          int64_t* __restrict__ off, unsigned* __restrict__ cursor,
                                                          int* __restrict__ ioff, int* __restrict__ n_items,
-                                                         int* __restrict__ ctr, int* __restrict__ fix_len) {
+                                                         int* __restrict__ ctr, int* __restrict__ fix_len,
+                                                         int tp) {
   __shared__ long long s_c[256];
   __shared__ int s_i[256];
   const int tid = threadIdx.x;
   const long long cc = tid < k ? (long long)cnt[tid] : 0;
-  const int ni = (int)((cc + kTM - 1) / kTM);
+  const int ni = (int)((cc + tp - 1) / tp);
   s_c[tid] = cc;
   s_i[tid] = ni;
   __syncthreads();
@@ -692,7 +707,6 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
               const int32_t* old_lab, const int32_t* list, const int* list_len, int32_t* lab, double* dmin,
               double* lo, int32_t* amb, int* amb_len, TcWork& w, cudaStream_t s) {
   const int NT = (k + 15) / 16 * 16, Dp = (d + 7) / 8 * 8;
-  const int max_items = (int)((n + kTM - 1) / kTM) + k;
   SC_TRY(w.cnt.ensure(sizeof(unsigned) * 2 * (size_t)k, s));
   SC_TRY(w.off.ensure(sizeof(int64_t) * (size_t)(k + 1), s));
   SC_TRY(w.items.ensure(sizeof(int) * ((size_t)k + 4), s));   // ioff[k + 1], n_items, ctr, fix_len
@@ -709,10 +723,60 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // kernel attributes once per process and instantiation (thread-safe static initialisation:
+  // restarts call this from several worker threads): the largest dynamic shared memory any
+  // supported (k, d) needs (tc_screen_supported caps it at 200 KB), the full shared-memory
+  // carve-out, and the registers per thread for the occupancy below
+  auto attrs = [](auto kern) {
+    cudaFuncAttributes f{};
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&f, kern);
+    return std::make_pair(e, f);
+  };
+  static const std::pair<cudaError_t, cudaFuncAttributes> kattr = attrs(assign_tc_kernel<kPV, 3, kTM>);
+  static const std::pair<cudaError_t, cudaFuncAttributes> kattr_w = attrs(assign_tc_kernel<kPVWide, 1, kTM>);
+  static const std::pair<cudaError_t, cudaFuncAttributes> kattr_p = attrs(assign_tc_kernel<kPVWide, 1, 2 * kTM>);
+  SC_CUDA_TRY(kattr.first);
+  SC_CUDA_TRY(kattr_w.first);
+  SC_CUDA_TRY(kattr_p.first);
+  const int tmem_tile = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
+  const bool v4 = (d % 4 == 0) && ((uintptr_t)F % 16 == 0) && ((uintptr_t)Cf % 16 == 0);
+  // resident CTAs per SM: shared memory (228 KB per SM, 1 KB reserved per CTA), registers and
+  // TMEM (512 columns per SM), computed here: the occupancy API answered 1 for this kernel
+  // where the hardware fits 3 (ncu "Block Limit Shared Mem" / "Block Limit Registers" = 3 / 4
+  // at k = 100, d = 64)
+  auto occupancy = [&](const cudaFuncAttributes& fa, int tp) {
+    const int sm = (int)tc_smem_bytes(NT, Dp, tp);
+    const int regs_cta = std::max(1, fa.numRegs) * tp;
+    const int o = std::min((227 * 1024) / (sm + (int)fa.sharedSizeBytes + 1024), 65536 / regs_cta);
+    return std::min(o, 512 / (tmem_tile * (tp / kTM)));
+  };
+  const int occ = std::max(1, occupancy(kattr.second, kTM));
+  // rows of 17-32 16-byte chunks (64 < d <= 128) where shared memory or TMEM already allow one
+  // CTA per SM only (configs[4]: k = 200, d = 96): the wide instantiation keeps the next tile's
+  // rows in registers too, and, when two tiles' rows fit beside the panel, takes two tiles of
+  // the cluster per CTA (8 warps per SM).  Env (tooling): SC_KMEANS_TC_WIDE=0 the narrow
+  // kernel's staging loads, SC_KMEANS_TC_PAIR=0 one tile per CTA.
+  auto env_on = [](const char* name) {
+    const char* e = std::getenv(name);
+    return !(e && std::atoi(e) == 0);
+  };
+  const int nval = d / 4;
+  const bool wide = env_on("SC_KMEANS_TC_WIDE") && v4 && nval > kPV && nval <= kPVWide && occ == 1 &&
+                    occupancy(kattr_w.second, kTM) == 1;
+  const bool pair = wide && env_on("SC_KMEANS_TC_PAIR") && tc_smem_bytes(NT, Dp, 2 * kTM) <= 200 * 1024 &&
+                    occupancy(kattr_p.second, 2 * kTM) == 1;
+  const int TP = pair ? 2 * kTM : kTM;
+  const int smem = (int)tc_smem_bytes(NT, Dp, TP);
+  if (std::getenv("SC_KMEANS_TRACE"))
+    std::fprintf(stderr, "[sc_kmeans] tensor screen: %d CTAs per SM, smem %d B%s%s\n", pair ? 1 : occ, smem,
+                 wide ? ", wide prefetch" : "", pair ? ", two tiles per CTA" : "");
+  const int max_items = (int)((n + TP - 1) / TP) + k;
   SC_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * k, s));
   const int pgrid = (int)std::max<int64_t>(1, (n + kGChunk - 1) / kGChunk);   // (list: <= n entries)
   group_hist_kernel<<<pgrid, 256, sizeof(unsigned) * k, s>>>(old_lab, list, list_len, n, k, cnt);
-  group_plan_kernel<<<1, 256, 0, s>>>(cnt, k, w.off.as<int64_t>(), cursor, w.items.as<int>(), n_items, ctr, fix_len);
+  group_plan_kernel<<<1, 256, 0, s>>>(cnt, k, w.off.as<int64_t>(), cursor, w.items.as<int>(), n_items, ctr, fix_len, TP);
   tc_panel_kernel<<<dim3(k, (NT + 31) / 32), 256, 0, s>>>(C, k, d, Dp, NT, w.panels.as<float>(), w.pscal.as<double>(),
                                                     panel_floats);
   group_scatter_kernel<<<pgrid, 256, sizeof(unsigned) * 3 * k, s>>>(old_lab, list, list_len, n, k,
@@ -733,8 +797,9 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   a.d = d;
   a.Dp = Dp;
   a.NT = NT;
-  a.tmem_cols = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
-  a.v4 = (d % 4 == 0) && ((uintptr_t)F % 16 == 0) && ((uintptr_t)Cf % 16 == 0);
+  a.tmem_tile = tmem_tile;
+  a.tmem_cols = tmem_tile * (TP / kTM);
+  a.v4 = v4;
   a.panels = w.panels.as<float>();
   a.pscal = w.pscal.as<double>();
   a.panel_floats = panel_floats;
@@ -755,30 +820,10 @@ int tc_screen(const float* F, int64_t n, int d, const double* C, const float* Cf
   a.lo = lo;
   a.amb = amb;
   a.amb_len = amb_len;
-  const int smem = (int)tc_smem_bytes(NT, Dp);
-  // kernel attributes once per process (thread-safe static initialisation: restarts call this
-  // from several worker threads): the largest dynamic shared memory any supported (k, d) needs
-  // (tc_screen_supported caps it at 200 KB), the full shared-memory carve-out, and the
-  // registers per thread for the occupancy below
-  static const std::pair<cudaError_t, cudaFuncAttributes> kattr = [] {
-    cudaFuncAttributes f{};
-    cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&f, assign_tc_kernel);
-    return std::make_pair(e, f);
-  }();
-  SC_CUDA_TRY(kattr.first);
-  const cudaFuncAttributes& fa = kattr.second;
-  // resident CTAs per SM: shared memory (228 KB per SM, 1 KB reserved per CTA), registers and
-  // TMEM (512 columns per SM), computed here: the occupancy API answered 1 for this kernel
-  // where the hardware fits 3 (ncu "Block Limit Shared Mem" / "Block Limit Registers" = 3 / 4
-  // at k = 100, d = 64)
-  const int regs_cta = std::max(1, fa.numRegs) * kTM;
-  int occ = std::min((227 * 1024) / (smem + (int)fa.sharedSizeBytes + 1024), 65536 / regs_cta);
-  occ = std::max(1, std::min(occ, 512 / a.tmem_cols));
-  if (std::getenv("SC_KMEANS_TRACE")) std::fprintf(stderr, "[sc_kmeans] tensor screen: %d CTAs per SM, smem %d B\n", occ, smem);
-  const int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * occ);
-  assign_tc_kernel<<<grid, kTM, smem, s>>>(a);
+  const int grid = (int)std::min<int64_t>(max_items, (int64_t)sms * (pair || wide ? 1 : occ));
+  if (pair) assign_tc_kernel<kPVWide, 1, 2 * kTM><<<grid, 2 * kTM, smem, s>>>(a);
+  else if (wide) assign_tc_kernel<kPVWide, 1, kTM><<<grid, kTM, smem, s>>>(a);
+  else assign_tc_kernel<kPV, 3, kTM><<<grid, kTM, smem, s>>>(a);
   SC_CUDA_TRY(cudaGetLastError());
   tc_fix_kernel<<<sms * 2, 256, 0, s>>>(F, C, d, a.v4, lab, a.fix, fix_len, dmin);
   SC_CUDA_TRY(cudaGetLastError());

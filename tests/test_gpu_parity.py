@@ -537,7 +537,8 @@ def test_kmeans_batched_seeding_identical(sc, n, k, d, spread, restarts, monkeyp
     (257, 17, 12, 0.4),      # tiles of 1-128 points, clusters of a few points
     (1000, 3, 8, -1.0),      # integer grid: ties everywhere -> the exact rescan decides
     (3000, 40, 64, 0.6),     # the register-prefetch staging at its widest (d = 64)
-    (2000, 30, 68, 0.6),     # d = 68: 16-byte rows wider than the prefetch
+    (2000, 30, 68, 0.6),     # d = 68: 16-byte rows wider than the narrow prefetch
+    (2500, 180, 100, 0.6),   # k x d that allow one CTA per SM: the wide (32-chunk) prefetch, two tiles per CTA
     (1500, 9, 20, 0.05)])    # tight clusters: most points decided, few change
 def test_kmeans_screens_forced_small(sc, n, k, d, spread, monkeypatch):
     """The screens (tensor-core and fp32) and the Hamerly check forced on small problems
@@ -549,8 +550,10 @@ def test_kmeans_screens_forced_small(sc, n, k, d, spread, monkeypatch):
     restarts, max_iter = 3, 30
     u = np.stack([scinputs.uniforms(3, k, offset=k * r) for r in range(restarts)])
     lo, Co, io, ito, ro, _ = kmeans.kmeans(X, k, u, max_iter)
-    for tc in ("1", "0"):
+    for tc, wide, pair in (("1", "1", "1"), ("1", "1", "0"), ("1", "0", "1"), ("0", "1", "1")):
         monkeypatch.setenv("SC_KMEANS_TC", tc)
+        monkeypatch.setenv("SC_KMEANS_TC_WIDE", wide)
+        monkeypatch.setenv("SC_KMEANS_TC_PAIR", pair)
         lab = torch.empty(n, dtype=torch.int32, device="cuda")
         C = np.zeros((k, d), dtype=np.float64)
         inertia, it, best = sc.sc_kmeans(torch.from_numpy(X).cuda(), n, d, k, restarts, max_iter, 0, u, lab, C)

@@ -1,5 +1,6 @@
 """k-means on configs[4]-shaped features (GPU box, tooling): the tensor screen with the wide
-register prefetch (SC_KMEANS_TC_WIDE=1) against the narrow kernel's staging loads; labels,
+register prefetch (SC_KMEANS_TC_WIDE=1), with two tiles per CTA (SC_KMEANS_TC_PAIR=1), against the narrow
+kernel's staging loads; labels,
 centroids and inertia must be identical."""
 import os, sys, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -22,8 +23,9 @@ Y = torch.empty((n, R), dtype=torch.float32, device="cuda")
 sc.sc_filter_lowpass_f32(G.handle, 0.005 * lmax, lmax, w.order, w.jackson, R, 3, None, Y)
 del G
 out = {}
-for wide in ("1", "0", "1"):
+for wide, pair in (("1", "1"), ("1", "0"), ("0", "1"), ("1", "1")):
     os.environ["SC_KMEANS_TC_WIDE"] = wide
+    os.environ["SC_KMEANS_TC_PAIR"] = pair
     lab = torch.empty(n, dtype=torch.int32, device="cuda")
     C = np.zeros((w.k, R), dtype=np.float64)
     torch.cuda.synchronize()
@@ -31,8 +33,9 @@ for wide in ("1", "0", "1"):
     res = sc.sc_kmeans(Y, n, R, w.k, restarts, iters, 4, None, lab, C)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    print(json.dumps({"workload": wl, "wide": wide, "restarts": restarts, "max_iter": iters, "seconds": dt,
+    print(json.dumps({"workload": wl, "wide": wide, "pair": pair, "restarts": restarts, "max_iter": iters, "seconds": dt,
                       "inertia": res[0], "iters": res[1], "best": res[2]}), flush=True)
-    out[wide] = (lab.cpu().numpy(), C, res)
-a, b = out["1"], out["0"]
-print("identical:", bool(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]))
+    out[(wide, pair)] = (lab.cpu().numpy(), C, res)
+a = out[("1", "1")]
+for key, b in out.items():
+    print(key, "identical:", bool(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]))
