@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(TP, MINB) assign_tc_kernel(TcArgs a) {
   __shared__ int s_zbad, s_chunk;
   __shared__ int s_ioff[257];
   __shared__ long long s_goff[257];
+  __shared__ long long s_nidx[TP];   // point of each row of the tile whose rows are copied next
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
@@ -332,17 +333,34 @@ __global__ void __launch_bounds__(TP, MINB) assign_tc_kernel(TcArgs a) {
     const int cnt = (int)min((int64_t)TP, (int64_t)(s_goff[c + 1] - g0));
     return tid < cnt ? (int64_t)a.gperm[g0 + tid] : (int64_t)-1;
   };
-  float4 xv[PV];
-  auto load_rows = [&](int64_t gi) {
-    const float4* xr = reinterpret_cast<const float4*>(a.F + (gi >= 0 ? gi : 0) * a.d);
-#pragma unroll
-    for (int t = 0; t < PV; ++t)
-      xv[t] = (gi >= 0 && t < nval) ? __ldg(xr + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+  // the next tile's raw rows are copied into sA, at their canonical positions, while the
+  // epilogue of the current tile runs (sA is free once its MMA completed); a warp copies G rows
+  // per instruction, lane = 16-byte chunk, so the loads are coalesced along each row (with one
+  // row per thread they touched 32 lines per instruction).  Chunks past the row (padding to
+  // Dp) and rows past the tile are zero-filled (src-size 0).
+  const int G = KC <= 16 ? 2 : 1, LPR = 32 / G;
+  auto copy_rows = [&]() {
+    const int j = lane % LPR;
+    for (int r = warp * G + lane / LPR; r < TP; r += (TP / 32) * G) {
+      const int64_t gi = s_nidx[r];
+      if (j < KC) {
+        const bool ok = gi >= 0 && j < nval;
+        const float* src = a.F + (ok ? gi * a.d + 4 * j : 0);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sA + canon(r, 4 * j, KC))),
+                     "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   int64_t gi_cur = -1, gi1 = -1;
   if (it < items) gi_cur = load_idx(ca, start);
   if (it1 < items) gi1 = load_idx(ca1, st1);
-  if (pref && it < items) load_rows(gi_cur);
+  if (pref && it < items) {
+    s_nidx[tid] = gi_cur;
+    __syncthreads();
+    copy_rows();
+  }
   unsigned long long pt[7] = {0, 0, 0, 0, 0, 0, 0};
   long long tprev = clock64();
   auto mark = [&](int i) {
@@ -380,6 +398,10 @@ __global__ void __launch_bounds__(TP, MINB) assign_tc_kernel(TcArgs a) {
       __syncthreads();
       cur = ca;
     }
+    if (pref) {   // this tile's raw rows (copy_rows) have landed in sA
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+    }
     // the tile after next: the next of its chunk, else the first of a new chunk (taken before
     // the barrier below, read after it)
     const bool need_grab = it1 < items && it1 + 1 >= chunk_end1;
@@ -395,11 +417,12 @@ __global__ void __launch_bounds__(TP, MINB) assign_tc_kernel(TcArgs a) {
       for (int t = 0; t < PV; ++t) {
         if (t >= KC) break;
         float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4* slot = reinterpret_cast<float4*>(sA + ((r & 7) + (r >> 3) * (8 * KC) + t * 8) * 4);
         if (t < nval) {
+          const float4 x = *slot;   // raw row (copy_rows), replaced in place by tf32(y) below
           const float4 c = *reinterpret_cast<const float4*>(s_caf + 4 * t);
-          y = make_float4(__fsub_rn(xv[t].x, c.x), __fsub_rn(xv[t].y, c.y), __fsub_rn(xv[t].z, c.z),
-                          __fsub_rn(xv[t].w, c.w));
-          const float xs[4] = {xv[t].x, xv[t].y, xv[t].z, xv[t].w};
+          y = make_float4(__fsub_rn(x.x, c.x), __fsub_rn(x.y, c.y), __fsub_rn(x.z, c.z), __fsub_rn(x.w, c.w));
+          const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const double diff = __dsub_rn((double)xs[e], s_ca[4 * t + e]);
@@ -407,8 +430,7 @@ __global__ void __launch_bounds__(TP, MINB) assign_tc_kernel(TcArgs a) {
           }
         }
         s2 = fmaf(y.w, y.w, fmaf(y.z, y.z, fmaf(y.y, y.y, fmaf(y.x, y.x, s2))));
-        *reinterpret_cast<float4*>(sA + ((r & 7) + (r >> 3) * (8 * KC) + t * 8) * 4) =
-            make_float4(to_tf32(y.x), to_tf32(y.y), to_tf32(y.z), to_tf32(y.w));
+        *slot = make_float4(to_tf32(y.x), to_tf32(y.y), to_tf32(y.z), to_tf32(y.w));
       }
       sY2[r] = (double)s2;
     } else if (a.v4) {
@@ -455,6 +477,7 @@ __global__ void __launch_bounds__(TP, MINB) assign_tc_kernel(TcArgs a) {
       }
     }
     mark(1);
+    if (pref) s_nidx[tid] = gi1;   // rows copied after this tile's MMA (read after the barrier)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // smem writes -> tensor core
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -489,9 +512,7 @@ __global__ void __launch_bounds__(TP, MINB) assign_tc_kernel(TcArgs a) {
                        smem_u32(&bar))
                    : "memory");
     }
-    // the next tile's rows in flight during the MMA and the epilogue; the index of the tile
-    // after next
-    if (pref && it1 < items) load_rows(gi1);
+    // the index of the tile after next (its rows are copied one tile later)
     const int64_t gi2 = it2 < items ? load_idx(ca2, st2) : -1;
     mark(2);
     asm volatile(
@@ -501,6 +522,8 @@ __global__ void __launch_bounds__(TP, MINB) assign_tc_kernel(TcArgs a) {
         : "memory");
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // sA is free: the next tile's rows land during this tile's epilogue
+    if (pref && it1 < items) copy_rows();
     mark(3);
     // ---- epilogue: thread tid owns point tid (TMEM lane tid % 128 of tile tid / 128); per column the fp32 lower
     // bound L_j of rho_j^2 (bound above), tracking the smallest (index b, its S) and the
