@@ -62,6 +62,10 @@ def parse():
                     help="row-partitioned runs: also time the whole pipeline (PAPER.md §4.1 steps 1-6: lambda "
                          "estimates, filter, k-means over the ranks; configs[4]'s 'full pipeline including "
                          "k-means'); implies --col-groups 1 (k-means needs whole feature rows)")
+    ap.add_argument("--selftest-exchange", action="store_true",
+                    help="internal: run the fused peer-store exchange and the NCCL exchange once on a small "
+                         "partitioned workload over the launched ranks, compare them, exit 0 if they agree "
+                         "(spawned by the multi-GPU bench before it trusts the fused path)")
     ap.add_argument("--dist-path", action="store_true",
                     help="use the row-partitioned NCCL filter even on one rank (exercises the multi-GPU path)")
     return ap.parse_args()
@@ -263,6 +267,90 @@ def grid_label(args, w, world):
 # ---------------------------------------------------------------------------
 # our implementation
 # ---------------------------------------------------------------------------
+# ---------------------------------------------------------------------------
+# multi-GPU: self-test of the fused peer-store exchange in a child process
+# ---------------------------------------------------------------------------
+SELFTEST_WORKLOAD = "c2_sbm100k"
+
+
+def run_selftest(args):
+    """Child of a multi-rank bench (same RANK / WORLD_SIZE / LOCAL_RANK, its own MASTER_PORT): the
+    pure row partition of a small SBM filtered three times through the fused peer-store exchange
+    (the flag waits run against live peers) and once through the NCCL exchange; exit 0 iff the two
+    agree to fp32 rounding on every rank.  A deadlock trips the library's watchdog (trap, non-zero
+    exit); the parent then takes the NCCL exchange."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1509_08863_b200 as sc
+    from paper_1509_08863_b200 import dist as pdist
+    from scinputs import configs
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    have_pg = "WORLD_SIZE" in os.environ and "MASTER_PORT" in os.environ
+    if have_pg:
+        dist.init_process_group("nccl", device_id=dev)
+    w = configs.WORKLOADS[SELFTEST_WORKLOAD]
+    g = configs.build_graph(SELFTEST_WORKLOAD, seed=args.seed)
+    n, R, order = g.n, w.R, w.order
+    part = pdist.local_part(g.row_ptr, g.col_idx, g.values, n, rank, world)
+    part = (pdist.exchange_send_lists(part) if world > 1 else pdist.send_lists_from_halos(part, [part.halo_gid]))
+    Gl = sc.Graph(part.n_local, part.row_ptr, part.col_idx, part.values, n_cols=part.n_local + part.n_halo)
+    est = pdist.NcclFilter(part, Gl.handle)
+    lmax = est.lambda_max(40, 0.01, args.seed)
+    d = sc.sc_cheby_coeffs(0.1 * lmax, lmax, order, w.jackson)
+    Xl = torch.empty((part.n_local, R), dtype=torch.float32, device=dev)
+    sc.sc_random_signals_f32(part.n_local, R, part.r0, args.seed, 0, 0.0, Xl)
+    Xp = Xl[torch.as_tensor(part.perm, device=dev)].contiguous()
+    Yn, Yf = torch.empty_like(Xp), torch.empty_like(Xp)
+    est.filter(d, order, lmax, Xp, Yn)
+    torch.cuda.synchronize()
+    nf = pdist.P2PFilter(part, Gl.handle, n, R)
+    for _ in range(3):
+        Yf.zero_()
+        nf.filter(d, order, lmax, Xp, Yf)
+    torch.cuda.synchronize()
+    num = float((Yf.double() - Yn.double()).norm())
+    den = float(Yn.double().norm())
+    ok = bool(np.isfinite(num) and den > 0 and num <= 1e-5 * den)
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    if have_pg:
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    print(f"[bench selftest] rank {rank}/{world}: fused vs NCCL exchange rel diff {num / max(den, 1e-300):.2e} "
+          f"-> {'ok' if ok else 'MISMATCH'}", file=sys.stderr, flush=True)
+    nf.close()
+    est.close()
+    verdict = int(flag.item())
+    if have_pg:
+        dist.barrier()
+        dist.destroy_process_group()
+    sys.exit(0 if verdict == 1 else 3)
+
+
+def p2p_selftest_child(args, timeout_s=420):
+    """Spawn run_selftest on this rank (every rank does, with MASTER_PORT shifted); returns
+    (ok, reason).  SC_BENCH_SELFTEST=0 skips it."""
+    import subprocess
+    if os.environ.get("SC_BENCH_SELFTEST", "1") == "0":
+        return True, "skipped"
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TORCHELASTIC_")}
+    port = int(env.get("MASTER_PORT", "29500")) + 29
+    env["MASTER_PORT"] = str(port if port < 65000 else port - 2000)
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(args.gpus), "--selftest-exchange",
+           "--seed", str(args.seed)]
+    try:
+        r = subprocess.run(cmd, env=env, timeout=timeout_s, stdout=subprocess.DEVNULL, stderr=subprocess.PIPE)
+    except subprocess.TimeoutExpired:
+        return False, f"timed out after {timeout_s} s"
+    if r.returncode != 0:
+        tail = r.stderr.decode(errors="replace").strip().splitlines()[-1:] or [""]
+        return False, f"exit {r.returncode}: {tail[0][:120]}"
+    return True, "ok"
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -330,6 +418,18 @@ def run_ours(args):
         del Xl
         Yp = torch.empty_like(Xp)
         exchange = args.exchange
+        selftest = None
+        if exchange == "p2p" and world > 1 and n_row > 1:
+            # the fused exchange's flag protocol against live peers, first in a child process (a
+            # deadlock would trap and take this process's context with it): all ranks must pass
+            ok, why = p2p_selftest_child(args)
+            t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            selftest = "ok" if int(t.item()) == 1 else f"failed ({why})"
+            if int(t.item()) != 1:
+                print(f"[bench] fused-exchange self-test failed on some rank (this rank: {why}); using NCCL",
+                      file=sys.stderr)
+                exchange = "nccl (fused-exchange self-test failed)"
         if exchange == "p2p":
             try:
                 nf = pdist.P2PFilter(part, handle, n, c1 - c0, group=rgroup)
@@ -429,7 +529,8 @@ def run_ours(args):
             "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(base_config(args, g, w, world), lambda_max=lmax, lambda_cut=lam_k,
-                           lambda_cut_count=count_k, **({"exchange": exchange} if partitioned else {})),
+                           lambda_cut_count=count_k, **({"exchange": exchange} if partitioned else {}),
+                           **({"exchange_selftest": selftest} if partitioned and selftest else {})),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": ("cheb_sell_kernel (fused sliced-CSR SpMM + 3-term recurrence + Y accumulation)"
@@ -593,6 +694,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.selftest_exchange:
+        run_selftest(args)
     else:
         run_ours(args)
 

@@ -1294,3 +1294,30 @@ def test_bench_json_line_gpu(sc, extra):
         assert key in d, key
     assert d["value"] > 0 and d["gpu_launches"] > 0
     assert d["roofline"]["achieved"] > 0 and 0 < d["roofline"]["frac"] < 1.5
+
+
+def test_bench_exchange_selftest_child(sc):
+    """`bench.py`'s multi-GPU arm first runs the fused peer-store exchange against the NCCL
+    exchange in a child process (`--selftest-exchange`, spawned by `p2p_selftest_child` with its
+    own MASTER_PORT and without torchrun's agent-store variables) and falls back to NCCL if the
+    child fails.  On the one GPU here: the child as the parent spawns it, with one rank -- it
+    must rendezvous on the shifted port, run both exchanges and exit 0."""
+    import importlib.util
+    import types
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    env = dict(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT="29611",
+               TORCHELASTIC_USE_AGENT_STORE="True")
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        ok, why = bench.p2p_selftest_child(types.SimpleNamespace(gpus=1, seed=1234), timeout_s=600)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert ok, why
